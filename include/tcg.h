@@ -1,0 +1,182 @@
+/*
+ * tcg.h -- C ABI of the B200-native pruned color-coding DP ("treecount-b200").
+ *
+ * This is the drop-in boundary for the reference's vectorized engine
+ * (/root/reference/proj/include/treecount/engines.hpp:302-307 run_iteration,
+ * estimator.hpp:49-93 estimate).  Plain pointers and sizes only; no
+ * exceptions cross the ABI.  Status codes mirror the reference's exception
+ * classes:
+ *   TCG_OK        0  success
+ *   TCG_EINVAL    1  std::invalid_argument / parse_error (bad graph, template,
+ *                    k, iterations < 1, coloring size mismatch)
+ *   TCG_ERESOURCE 2  memory_budget_error (engines.hpp:37-44) or device OOM --
+ *                    the CLI's exit code 2 class (treecount_cli.cpp:501-503)
+ *   TCG_ECUDA     3  CUDA failure
+ *   TCG_ENONFINITE 4 non-finite rooted total (overflow guard, SURVEY finding 2)
+ *   TCG_ELOGIC    5  std::logic_error (liveness / internal invariant)
+ * The message of the last failure is available from tcg_last_error().
+ *
+ * Ownership: inputs are caller-owned and copied; outputs are caller-allocated.
+ * A context is single-threaded and blocks until results are on the host.
+ */
+#ifndef TCG_H
+#define TCG_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+  TCG_OK = 0,
+  TCG_EINVAL = 1,
+  TCG_ERESOURCE = 2,
+  TCG_ECUDA = 3,
+  TCG_ENONFINITE = 4,
+  TCG_ELOGIC = 5
+};
+
+#define TCG_MAX_K 20                   /* color_index.hpp:15 kMaxTemplateSize */
+#define TCG_MAX_NODES (2 * TCG_MAX_K - 1)
+
+/* Message of the most recent failure on this thread (any entry point). */
+const char* tcg_last_error(void);
+/* Library build string (arch, version). */
+const char* tcg_version(void);
+
+/* ------------------------------------------------------------------------
+ * Host graph: symmetric CSR (== treecount::Graph::csc_col_ptr / csc_rows,
+ * graph.hpp:27-42): int64 row_ptr[n+1], int32 col[nnz], rows sorted,
+ * deduplicated, no self-loops.
+ * ---------------------------------------------------------------------- */
+typedef struct tcg_graph tcg_graph;
+
+/* graph.hpp:65-95 from_edges: symmetrize by union, drop self-loops, dedup,
+ * sort.  edges = m (u,v) int32 pairs; n_hint < 0 -> max id + 1.  Built by a
+ * multithreaded radix sort on the host. */
+int tcg_graph_from_edges(const int32_t* edges, int64_t m, int32_t n_hint, tcg_graph** out);
+/* Adopt an existing CSR (validated: symmetric, sorted, no loops/duplicates). */
+int tcg_graph_from_csr(int32_t n, const int64_t* row_ptr, const int32_t* col, tcg_graph** out);
+/* synthgen.hpp:40-74 generate_rmat / 76-85 generate_erdos_renyi, bit-identical
+ * edge streams (std::mt19937_64 + Rng::unit).  Harness input generators. */
+int tcg_generate_rmat(int scale, int64_t edges, double a, double b, double c, double d,
+                      uint64_t seed, tcg_graph** out);
+int tcg_generate_erdos_renyi(int32_t n, double p, uint64_t seed, tcg_graph** out);
+int tcg_graph_info(const tcg_graph* g, int32_t* n, int64_t* m, int64_t* nnz,
+                   int32_t* max_degree);
+/* Zero-copy views of the host CSR (valid until tcg_graph_destroy). */
+const int64_t* tcg_graph_row_ptr(const tcg_graph* g);
+const int32_t* tcg_graph_col(const tcg_graph* g);
+void tcg_graph_destroy(tcg_graph* g);
+
+/* ------------------------------------------------------------------------
+ * Host template pieces (templates.hpp, color_index.hpp), exposed for tests
+ * and plan inspection.  edges = k-1 (u,v) pairs; root < 0 = default root
+ * (max-degree vertex, smallest id; templates.hpp:67-74).
+ * ---------------------------------------------------------------------- */
+typedef struct {
+  int k, root, num_nodes;
+  int size[TCG_MAX_NODES];
+  int node_root[TCG_MAX_NODES];
+  int active_child[TCG_MAX_NODES];
+  int passive_child[TCG_MAX_NODES];
+  int parent[TCG_MAX_NODES];
+  int dp_order[TCG_MAX_NODES];
+} tcg_plan;
+
+/* templates.hpp:249-259 partition (validated as make_template does, :80-90) */
+int tcg_partition(int k, const int32_t* edges, int root, tcg_plan* out);
+/* templates.hpp:326-339 automorphism_count */
+int tcg_automorphisms(int k, const int32_t* edges, uint64_t* out);
+/* color_index.hpp:103-180 build_split_table: by-parent (active_index,
+ * passive_index [C(k,ps) * C(ps,as)]) and grouped (grouped_parent,
+ * grouped_active [C(k,ps-as) * C(k-(ps-as),as)]) views; any may be NULL. */
+int tcg_split_table(int k, int parent_size, int active_size, int32_t* active_index,
+                    int32_t* passive_index, int32_t* grouped_parent, int32_t* grouped_active);
+/* color_index.hpp:44-56 / 60-72 */
+int64_t tcg_color_index_of(int k, const int32_t* colors, int h);
+int tcg_color_set_of(int k, int64_t index, int h, int32_t* colors);
+/* count_table.hpp:113-133 estimate_bytes (the reference's fp64 model) */
+int64_t tcg_estimate_bytes(const tcg_plan* plan, int64_t n);
+/* estimator.hpp:29-33 */
+double tcg_colorful_probability(int k);
+
+/* ------------------------------------------------------------------------
+ * Device engine (one GPU).  == the vectorized engine of engines.hpp:224-268.
+ * ---------------------------------------------------------------------- */
+typedef struct tcg_ctx tcg_ctx;
+
+typedef struct {
+  int device;              /* CUDA ordinal */
+  int64_t memory_budget;   /* bytes of device tables; 0 = unlimited
+                              (EngineConfig::memory_budget, engines.hpp:48) */
+  int flags;               /* TCG_KEEP_TABLES: keep every node table and SpMM
+                              output of the last coloring for inspection */
+  int reserved[5];
+} tcg_config;
+
+#define TCG_KEEP_TABLES 1
+
+/* NodeStats (engines.hpp:53-61) + device time. */
+typedef struct {
+  double seconds;            /* CUDA-event time of the node's kernels */
+  double spmm_seconds;
+  double ema_seconds;
+  uint64_t neighbor_passes;  /* one per passive column (pruned/vectorized) */
+  uint64_t traversals;       /* neighbor_passes * n */
+  uint64_t flops;            /* reference counting: C_p*nnz + 2*n*pairs */
+  uint64_t spmm_bytes;       /* SURVEY 8(d) algorithmic bytes */
+  uint64_t ema_bytes;
+  uint64_t ema_flops;
+} tcg_node_stats;
+
+int tcg_create(const tcg_config* cfg, tcg_ctx** out);
+void tcg_destroy(tcg_ctx* ctx);
+
+/* Upload the graph (copied host -> device; builds the SpMM row schedule). */
+int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t* col);
+int tcg_set_graph_handle(tcg_ctx* ctx, const tcg_graph* g);
+/* Validate + partition + split tables + |Aut| on the host; upload tables. */
+int tcg_set_template(tcg_ctx* ctx, int k, const int32_t* edges, int root);
+/* Device bytes one coloring needs (arena peak + graph + schedules). */
+int tcg_required_device_bytes(tcg_ctx* ctx, int64_t* bytes);
+int tcg_get_plan(tcg_ctx* ctx, tcg_plan* out, uint64_t* aut);
+
+/* count_table.hpp:90-99 random_coloring, generated ON DEVICE
+ * (MT19937-64 + rejection), bit-exact; colors = n bytes. */
+int tcg_coloring(tcg_ctx* ctx, uint64_t seed, uint8_t* colors);
+
+/* One coloring == run_iteration(vectorized, ..., keep_full_table).
+ * colors != NULL: use the caller's coloring (Coloring argument of
+ * run_iteration); else generate on device from `seed`.
+ * per_vertex (n doubles, nullable) = M_root[:,0]; stats (num_nodes entries
+ * indexed by plan node id, nullable). */
+int tcg_run_coloring(tcg_ctx* ctx, uint64_t seed, const uint8_t* colors, double* rooted_total,
+                     double* per_vertex, tcg_node_stats* stats);
+
+/* == estimate(): colorings seed, seed+1, ... (estimator.hpp:66).
+ * rooted_totals[iterations]; per_vertex_estimate (n, nullable) =
+ * mean_i M_root^(i)[v,0] / (aut * k!/k^k). */
+int tcg_estimate(tcg_ctx* ctx, uint64_t seed, int iterations, double* rooted_totals,
+                 double* estimate, double* stderr_of_mean, double* per_vertex_estimate);
+
+/* Inspection (TCG_KEEP_TABLES): node table of the last coloring as
+ * vertex-major fp64 n x C(k,|T_s|); which = 0 node table, 1 the SpMM output
+ * P' computed from it (passive children only).  Root: C = 1. */
+int tcg_node_table(tcg_ctx* ctx, int node_id, int which, double* out);
+/* Kernel-level hook: Y = A X for a vertex-major fp32 n x C host matrix,
+ * through the production SpMM kernel (la_kernels.hpp:83-102 semantics). */
+int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y);
+/* Test hook: override the rejection threshold (UINT64_MAX/k)*k of
+ * Rng::below (rng.hpp:21-27); 0 restores the reference value. */
+int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit);
+/* Kernel launches issued by this context since creation (evidence for
+ * bench.py's gpu_launches). */
+int64_t tcg_kernel_launches(const tcg_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* TCG_H */

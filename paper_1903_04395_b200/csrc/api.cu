@@ -1,0 +1,314 @@
+// api.cu -- the extern "C" boundary (include/tcg.h).  Every entry point
+// catches the host library's exception classes and maps them to the status
+// codes documented in tcg.h (mirroring the reference's exception types,
+// SURVEY 8(b)); no C++ exception crosses the ABI.
+#include <cstring>
+#include <memory>
+#include <string>
+
+#include "../../include/tcg.h"
+#include "engine.hpp"
+
+struct tcg_graph {
+  tcg::Csr csr;
+};
+struct tcg_ctx {
+  std::unique_ptr<tcg::Engine> eng;
+};
+
+namespace {
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TCG_OK;
+  } catch (const tcg::invalid_argument& e) {
+    g_err = e.what();
+    return TCG_EINVAL;
+  } catch (const tcg::resource_error& e) {
+    g_err = e.what();
+    return TCG_ERESOURCE;
+  } catch (const tcg::nonfinite_error& e) {
+    g_err = e.what();
+    return TCG_ENONFINITE;
+  } catch (const tcg::cuda_error& e) {
+    g_err = e.what();
+    return TCG_ECUDA;
+  } catch (const tcg::logic_error& e) {
+    g_err = e.what();
+    return TCG_ELOGIC;
+  } catch (const std::bad_alloc&) {
+    g_err = "host allocation failed";
+    return TCG_ERESOURCE;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return TCG_ELOGIC;
+  }
+}
+
+void need(const void* p, const char* what) {
+  if (!p) throw tcg::invalid_argument(std::string(what) + " is NULL");
+}
+
+void fill_plan(const tcg::Plan& p, tcg_plan* out) {
+  std::memset(out, 0, sizeof(*out));
+  out->k = p.k;
+  out->root = p.root;
+  out->num_nodes = p.num_nodes;
+  for (int i = 0; i < p.num_nodes; ++i) {
+    out->size[i] = p.size[i];
+    out->node_root[i] = p.node_root[i];
+    out->active_child[i] = p.active[i];
+    out->passive_child[i] = p.passive[i];
+    out->parent[i] = p.parent[i];
+    out->dp_order[i] = p.dp_order[i];
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* tcg_last_error(void) { return g_err.c_str(); }
+
+const char* tcg_version(void) {
+  return "treecount-b200 0.1 (sm_100a; fp32 panel tables Z=16, fp64 accumulation/root)";
+}
+
+// ------------------------------------------------------------------ graph
+int tcg_graph_from_edges(const int32_t* edges, int64_t m, int32_t n_hint, tcg_graph** out) {
+  return guarded([&] {
+    need(out, "out");
+    if (m < 0) throw tcg::invalid_argument("negative edge count");
+    if (m > 0) need(edges, "edges");
+    auto g = std::make_unique<tcg_graph>();
+    g->csr = tcg::csr_from_edges(edges, m, n_hint);
+    *out = g.release();
+  });
+}
+
+int tcg_graph_from_csr(int32_t n, const int64_t* row_ptr, const int32_t* col, tcg_graph** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(row_ptr, "row_ptr");
+    if (row_ptr[n] > 0) need(col, "col");
+    auto g = std::make_unique<tcg_graph>();
+    g->csr = tcg::csr_adopt(n, row_ptr, col);
+    *out = g.release();
+  });
+}
+
+int tcg_generate_rmat(int scale, int64_t edges, double a, double b, double c, double d,
+                      uint64_t seed, tcg_graph** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto g = std::make_unique<tcg_graph>();
+    g->csr = tcg::generate_rmat(scale, edges, a, b, c, d, seed);
+    *out = g.release();
+  });
+}
+
+int tcg_generate_erdos_renyi(int32_t n, double p, uint64_t seed, tcg_graph** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto g = std::make_unique<tcg_graph>();
+    g->csr = tcg::generate_erdos_renyi(n, p, seed);
+    *out = g.release();
+  });
+}
+
+int tcg_graph_info(const tcg_graph* g, int32_t* n, int64_t* m, int64_t* nnz, int32_t* max_degree) {
+  return guarded([&] {
+    need(g, "graph");
+    if (n) *n = g->csr.n;
+    if (m) *m = g->csr.nnz() / 2;
+    if (nnz) *nnz = g->csr.nnz();
+    if (max_degree) *max_degree = g->csr.max_degree();
+  });
+}
+
+const int64_t* tcg_graph_row_ptr(const tcg_graph* g) { return g ? g->csr.row_ptr.data() : nullptr; }
+const int32_t* tcg_graph_col(const tcg_graph* g) { return g ? g->csr.col.data() : nullptr; }
+void tcg_graph_destroy(tcg_graph* g) { delete g; }
+
+// --------------------------------------------------------------- template
+int tcg_partition(int k, const int32_t* edges, int root, tcg_plan* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (k > 1) need(edges, "edges");
+    fill_plan(tcg::partition(tcg::make_template(k, edges, root)), out);
+  });
+}
+
+int tcg_automorphisms(int k, const int32_t* edges, uint64_t* out) {
+  return guarded([&] {
+    need(out, "out");
+    if (k > 1) need(edges, "edges");
+    *out = tcg::automorphism_count(tcg::make_template(k, edges, -1));
+  });
+}
+
+int tcg_split_table(int k, int parent_size, int active_size, int32_t* ai, int32_t* pi,
+                    int32_t* gp, int32_t* ga) {
+  return guarded([&] {
+    if (k < 1 || k > tcg::kMaxK) throw tcg::invalid_argument("color count k must be in [1, 20]");
+    tcg::SplitTable st = tcg::build_split_table(k, parent_size, active_size);
+    const size_t bytes = st.active_index.size() * sizeof(int32_t);
+    if (ai) std::memcpy(ai, st.active_index.data(), bytes);
+    if (pi) std::memcpy(pi, st.passive_index.data(), bytes);
+    if (gp) std::memcpy(gp, st.grouped_parent.data(), bytes);
+    if (ga) std::memcpy(ga, st.grouped_active.data(), bytes);
+  });
+}
+
+int64_t tcg_color_index_of(int k, const int32_t* colors, int h) {
+  int64_t r = -1;
+  const int st = guarded([&] {
+    if (k < 1 || k > tcg::kMaxK) throw tcg::invalid_argument("color count k must be in [1, 20]");
+    int c[tcg::kMaxK];
+    for (int i = 0; i < h; ++i) {
+      c[i] = colors[i];
+      if (c[i] >= k || (i && c[i] <= c[i - 1]) || c[i] < 0)
+        throw tcg::invalid_argument("color set must be strictly increasing in [0, k)");
+    }
+    r = tcg::index_of(c, h);
+  });
+  return st == TCG_OK ? r : -1;
+}
+
+int tcg_color_set_of(int k, int64_t index, int h, int32_t* colors) {
+  return guarded([&] {
+    if (k < 1 || k > tcg::kMaxK) throw tcg::invalid_argument("color count k must be in [1, 20]");
+    if (h < 0 || h > k || index < 0 || index >= tcg::binom()(k, h))
+      throw tcg::invalid_argument("color set index out of range");
+    int c[tcg::kMaxK];
+    tcg::set_of(k, index, h, c);
+    for (int i = 0; i < h; ++i) colors[i] = c[i];
+  });
+}
+
+int64_t tcg_estimate_bytes(const tcg_plan* plan, int64_t n) {
+  if (!plan) return -1;
+  tcg::Plan p;
+  p.k = plan->k;
+  p.num_nodes = plan->num_nodes;
+  p.size.assign(plan->size, plan->size + plan->num_nodes);
+  p.active.assign(plan->active_child, plan->active_child + plan->num_nodes);
+  p.passive.assign(plan->passive_child, plan->passive_child + plan->num_nodes);
+  p.dp_order.assign(plan->dp_order, plan->dp_order + plan->num_nodes);
+  return tcg::estimate_bytes(p, n);
+}
+
+double tcg_colorful_probability(int k) { return tcg::colorful_probability(k); }
+
+// ----------------------------------------------------------------- engine
+int tcg_create(const tcg_config* cfg, tcg_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    tcg_config c{};
+    if (cfg) c = *cfg;
+    auto ctx = std::make_unique<tcg_ctx>();
+    ctx->eng = std::make_unique<tcg::Engine>(c);
+    *out = ctx.release();
+  });
+}
+
+void tcg_destroy(tcg_ctx* ctx) { delete ctx; }
+
+int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t* col) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(row_ptr, "row_ptr");
+    ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col));
+  });
+}
+
+int tcg_set_graph_handle(tcg_ctx* ctx, const tcg_graph* g) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(g, "graph");
+    ctx->eng->set_graph(g->csr);
+  });
+}
+
+int tcg_set_template(tcg_ctx* ctx, int k, const int32_t* edges, int root) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (k > 1) need(edges, "edges");
+    ctx->eng->set_template(k, edges, root);
+  });
+}
+
+int tcg_required_device_bytes(tcg_ctx* ctx, int64_t* bytes) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(bytes, "bytes");
+    *bytes = ctx->eng->required_bytes();
+  });
+}
+
+int tcg_get_plan(tcg_ctx* ctx, tcg_plan* out, uint64_t* aut) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (out) fill_plan(ctx->eng->plan(), out);
+    if (aut) *aut = ctx->eng->aut();
+  });
+}
+
+int tcg_coloring(tcg_ctx* ctx, uint64_t seed, uint8_t* colors) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(colors, "colors");
+    ctx->eng->coloring(seed, colors);
+  });
+}
+
+int tcg_run_coloring(tcg_ctx* ctx, uint64_t seed, const uint8_t* colors, double* rooted_total,
+                     double* per_vertex, tcg_node_stats* stats) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(rooted_total, "rooted_total");
+    *rooted_total = ctx->eng->run_coloring(seed, colors, per_vertex, stats);
+  });
+}
+
+int tcg_estimate(tcg_ctx* ctx, uint64_t seed, int iterations, double* rooted_totals,
+                 double* estimate, double* stderr_of_mean, double* per_vertex_estimate) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(rooted_totals, "rooted_totals");
+    need(estimate, "estimate");
+    need(stderr_of_mean, "stderr_of_mean");
+    ctx->eng->estimate(seed, iterations, rooted_totals, estimate, stderr_of_mean,
+                       per_vertex_estimate);
+  });
+}
+
+int tcg_node_table(tcg_ctx* ctx, int node_id, int which, double* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->eng->node_table(node_id, which, out);
+  });
+}
+
+int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(x, "x");
+    need(y, "y");
+    ctx->eng->spmm_host(x, cols, y);
+  });
+}
+
+int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->set_rejection_limit(limit);
+  });
+}
+
+int64_t tcg_kernel_launches(const tcg_ctx* ctx) { return ctx ? ctx->eng->launches() : -1; }
+
+}  // extern "C"

@@ -1,0 +1,586 @@
+// engine.cu -- per-GPU DP engine (see engine.hpp).
+#include "engine.hpp"
+#include "kernels.cuh"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <map>
+
+namespace tcg {
+
+#define TCG_CUDA(call)                                                                    \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess) {                                                              \
+      if (e_ == cudaErrorMemoryAllocation) {                                              \
+        cudaGetLastError();                                                               \
+        throw resource_error(std::string("device allocation failed: ") + #call);          \
+      }                                                                                   \
+      throw cuda_error(std::string(cudaGetErrorString(e_)) + " at " + __FILE__ + ":" +   \
+                       std::to_string(__LINE__));                                         \
+    }                                                                                     \
+  } while (0)
+
+namespace {
+constexpr int64_t kAlign = 256;
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+template <typename T>
+void dfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// First-fit arena planner over the reference's liveness sequence.
+struct ArenaPlanner {
+  std::map<int64_t, int64_t> used;  // offset -> bytes
+  int64_t peak = 0;
+  int64_t alloc(int64_t bytes) {
+    bytes = align_up(std::max<int64_t>(bytes, kAlign));
+    int64_t off = 0;
+    for (auto& [o, b] : used) {
+      if (o - off >= bytes) break;
+      off = std::max(off, o + b);
+    }
+    used[off] = bytes;
+    peak = std::max(peak, off + bytes);
+    return off;
+  }
+  void free(int64_t off) { used.erase(off); }
+};
+}  // namespace
+
+Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
+  int ndev = 0;
+  TCG_CUDA(cudaGetDeviceCount(&ndev));
+  if (cfg.device < 0 || cfg.device >= ndev)
+    throw invalid_argument("CUDA device " + std::to_string(cfg.device) + " not present (" +
+                           std::to_string(ndev) + " visible)");
+  TCG_CUDA(cudaSetDevice(cfg.device));
+  cudaDeviceProp prop;
+  TCG_CUDA(cudaGetDeviceProperties(&prop, cfg.device));
+  if (prop.major != 10)
+    throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
+                     std::to_string(prop.major) + std::to_string(prop.minor));
+  TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  TCG_CUDA(cudaMalloc(&d_scalars_, 64));
+  TCG_CUDA(cudaMalloc(&d_seeds_, 1024 * sizeof(uint64_t)));
+}
+
+Engine::~Engine() {
+  cudaSetDevice(cfg_.device);
+  release_template();
+  release_graph();
+  dfree(d_scalars_);
+  dfree(d_seeds_);
+  dfree(d_colors_);
+  if (stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::release_graph() {
+  dfree(d_row_ptr_);
+  dfree(d_col_);
+  dfree(d_segs_);
+  dfree(d_split_rows_);
+  dfree(d_split_slot_begin_);
+  dfree(d_tile_tot_);
+  n_ = -1;
+}
+
+void Engine::release_template() {
+  for (auto& e : exec_) dfree(e.d_split);
+  exec_.clear();
+  dfree(arena_);
+  arena_alloc_ = 0;
+  dfree(d_partial_);
+  partial_bytes_ = partial_alloc_ = 0;
+  have_template_ = false;
+  tables_valid_ = false;
+}
+
+int64_t Engine::table_bytes(int64_t cols) const {
+  return (cols + dev::Z - 1) / dev::Z * static_cast<int64_t>(n_) * dev::Z * 4;
+}
+
+// ------------------------------------------------------------------ graph
+void Engine::set_graph(const Csr& g) {
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  release_graph();
+  n_ = g.n;
+  nnz_ = g.nnz();
+  TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (n_ + 1)));
+  TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
+  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, g.row_ptr.data(), sizeof(int64_t) * (n_ + 1),
+                           cudaMemcpyHostToDevice, stream_));
+  if (nnz_)
+    TCG_CUDA(cudaMemcpyAsync(d_col_, g.col.data(), sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice,
+                             stream_));
+
+  // SpMM schedule: rows cut into segments of <= kSegMax neighbours, counting-
+  // sorted by length (descending) so the 8 groups of a warp are balanced and
+  // the longest work is issued first.  Split rows get fp64 partial slots.
+  std::vector<int64_t> cnt(dev::kSegMax + 2, 0);
+  std::vector<dev::Seg> segs;
+  segs.reserve(static_cast<size_t>(n_) + static_cast<size_t>(nnz_ / dev::kSegMax) + 8);
+  std::vector<int32_t> split_rows, slot_begin{0};
+  int slot = 0;
+  for (int32_t v = 0; v < n_; ++v) {
+    const int64_t b = g.row_ptr[v], d = g.row_ptr[v + 1] - b;
+    if (d <= dev::kSegMax) {
+      segs.push_back({b, static_cast<int32_t>(d), v});
+    } else {
+      split_rows.push_back(v);
+      for (int64_t o = 0; o < d; o += dev::kSegMax)
+        segs.push_back({b + o, static_cast<int32_t>(std::min<int64_t>(dev::kSegMax, d - o)), -1 - slot++});
+      slot_begin.push_back(slot);
+    }
+  }
+  for (auto& s : segs) cnt[dev::kSegMax - s.len]++;
+  std::vector<int64_t> pos(cnt.size(), 0);
+  for (size_t i = 1; i < cnt.size(); ++i) pos[i] = pos[i - 1] + cnt[i - 1];
+  const int64_t nseg = static_cast<int64_t>(segs.size());
+  const int64_t padded = (nseg + 7) / 8 * 8;
+  std::vector<dev::Seg> sorted(static_cast<size_t>(std::max<int64_t>(padded, 8)),
+                               dev::Seg{0, 0, dev::kSkip});
+  for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
+  ntasks_ = std::max<int64_t>(padded, 8) / 8;
+  nsplit_rows_ = static_cast<int>(split_rows.size());
+  nsplit_slots_ = slot;
+  TCG_CUDA(cudaMalloc(&d_segs_, sizeof(dev::Seg) * sorted.size()));
+  TCG_CUDA(cudaMemcpyAsync(d_segs_, sorted.data(), sizeof(dev::Seg) * sorted.size(),
+                           cudaMemcpyHostToDevice, stream_));
+  if (nsplit_rows_) {
+    TCG_CUDA(cudaMalloc(&d_split_rows_, sizeof(int32_t) * nsplit_rows_));
+    TCG_CUDA(cudaMalloc(&d_split_slot_begin_, sizeof(int32_t) * (nsplit_rows_ + 1)));
+    TCG_CUDA(cudaMemcpyAsync(d_split_rows_, split_rows.data(), sizeof(int32_t) * nsplit_rows_,
+                             cudaMemcpyHostToDevice, stream_));
+    TCG_CUDA(cudaMemcpyAsync(d_split_slot_begin_, slot_begin.data(),
+                             sizeof(int32_t) * (nsplit_rows_ + 1), cudaMemcpyHostToDevice, stream_));
+  }
+  const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
+  TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+  if (have_template_) plan_arena();
+  tables_valid_ = false;
+}
+
+// --------------------------------------------------------------- template
+void Engine::set_template(int k, const int32_t* edges, int root) {
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  Template t = make_template(k, edges, root);
+  Plan p = partition(t);
+  release_template();
+  tpl_ = t;
+  plan_ = p;
+  aut_ = automorphism_count(t);
+  const Binom& B = binom();
+  need_hist_ = false;
+  for (int id : plan_.dp_order) {
+    if (plan_.is_leaf(id)) continue;
+    NodeExec e;
+    e.id = id;
+    e.a = plan_.active[id];
+    e.p = plan_.passive[id];
+    e.size = plan_.size[id];
+    e.sa = plan_.size[e.a];
+    e.sp = plan_.size[e.p];
+    e.Cs = static_cast<int32_t>(B(k, e.size));
+    e.Ca = static_cast<int32_t>(B(k, e.sa));
+    e.Cp = static_cast<int32_t>(B(k, e.sp));
+    e.a_leaf = e.sa == 1;
+    e.p_leaf = e.sp == 1;
+    e.root = id == plan_.full_node();
+    need_hist_ |= e.p_leaf;
+    SplitTable st = build_split_table(k, e.size, e.sa);
+    e.pairs = st.pairs_per_parent;
+    std::vector<int2> pr(st.active_index.size());
+    for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(st.active_index[i], st.passive_index[i]);
+    TCG_CUDA(cudaMalloc(&e.d_split, sizeof(int2) * std::max<size_t>(pr.size(), 1)));
+    TCG_CUDA(cudaMemcpy(e.d_split, pr.data(), sizeof(int2) * pr.size(), cudaMemcpyHostToDevice));
+    // eMA shared memory: staged inputs + per-warp transpose buffers
+    const int64_t pitch = dev::kTileV + 1;
+    const int64_t staged = ((e.a_leaf ? 0 : e.Ca) + e.Cp) * pitch * 4 +
+                           dev::kEmaWarps * dev::kTileV * (dev::Z + 1) * 4;
+    e.ema_staged = staged <= 200 * 1024;
+    e.ema_smem = e.ema_staged ? staged : dev::kEmaWarps * dev::kTileV * (dev::Z + 1) * 4;
+    exec_.push_back(e);
+  }
+  have_template_ = true;
+  if (n_ >= 0) plan_arena();
+  tables_valid_ = false;
+}
+
+void Engine::plan_arena() {
+  const bool keep = cfg_.flags & TCG_KEEP_TABLES;
+  ArenaPlanner ap;
+  table_off_.assign(plan_.num_nodes, -1);
+  pprime_off_.assign(plan_.num_nodes, -1);
+  hist_off_ = need_hist_ ? ap.alloc(table_bytes(plan_.k)) : -1;
+  int max_pp_panels = 0;
+  for (auto& e : exec_) {
+    if (!e.p_leaf) {
+      e.pp_off = ap.alloc(table_bytes(e.Cp));
+      pprime_off_[e.p] = e.pp_off;
+      max_pp_panels = std::max(max_pp_panels, (e.Cp + dev::Z - 1) / dev::Z);
+      if (!keep) ap.free(table_off_[e.p]);
+    }
+    e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(e.Cs));
+    table_off_[e.id] = e.out_off;
+    if (!keep) {
+      if (!e.p_leaf) ap.free(e.pp_off);
+      if (!e.a_leaf) ap.free(table_off_[e.a]);
+    }
+  }
+  arena_bytes_ = ap.peak;
+  partial_bytes_ = static_cast<int64_t>(nsplit_slots_) * max_pp_panels * dev::Z * 8;
+}
+
+int64_t Engine::required_bytes() const {
+  require_ready();
+  const int64_t graph = 8 * (static_cast<int64_t>(n_) + 1) + 4 * nnz_ +
+                        static_cast<int64_t>(sizeof(dev::Seg)) * ntasks_ * 8;
+  return arena_bytes_ + partial_bytes_ + graph + n_ + 8 * ((n_ + 31) / 32);
+}
+
+void Engine::require_ready() const {
+  if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
+  if (!have_template_) throw invalid_argument("no template set (tcg_set_template)");
+}
+
+void Engine::ensure_arena() {
+  require_ready();
+  if (cfg_.memory_budget > 0 && arena_bytes_ > cfg_.memory_budget)
+    throw resource_error("count tables need " + std::to_string(arena_bytes_) +
+                         " bytes, over the budget of " + std::to_string(cfg_.memory_budget));
+  if (arena_alloc_ != arena_bytes_ || !arena_) {
+    dfree(arena_);
+    arena_alloc_ = 0;
+    TCG_CUDA(cudaMalloc(&arena_, std::max<int64_t>(arena_bytes_, kAlign)));
+    arena_alloc_ = arena_bytes_;
+  }
+  if (partial_alloc_ != partial_bytes_) {
+    dfree(d_partial_);
+    partial_alloc_ = 0;
+    if (partial_bytes_) TCG_CUDA(cudaMalloc(&d_partial_, partial_bytes_));
+    partial_alloc_ = partial_bytes_;
+  }
+}
+
+// ----------------------------------------------------------------- colors
+void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
+  TCG_CUDA(cudaMemcpyAsync(d_seeds_, seeds, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, stream_));
+  const uint64_t limit = limit_override_ ? limit_override_
+                                         : (UINT64_MAX / static_cast<uint64_t>(plan_.k)) * plan_.k;
+  dev::mt_coloring<<<count, dev::kMtThreads, 0, stream_>>>(d_seeds_, n_, plan_.k, limit, d_out, n_);
+  ++launches_;
+  TCG_CUDA(cudaGetLastError());
+}
+
+void Engine::coloring(uint64_t seed, uint8_t* host_colors) {
+  require_ready();
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  if (colors_cap_ < n_) {
+    dfree(d_colors_);
+    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(n_, 1)));
+    colors_cap_ = n_;
+  }
+  gen_colors(&seed, 1, d_colors_);
+  TCG_CUDA(cudaMemcpyAsync(host_colors, d_colors_, n_, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// ------------------------------------------------------------------- SpMM
+void Engine::spmm(const float* X, float* Y, int cols) {
+  const int npanels = (cols + dev::Z - 1) / dev::Z;
+  const int64_t bpp = (ntasks_ + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
+  dev::spmm_panels<<<static_cast<unsigned>(bpp * npanels), dev::kSpmmWarps * 32, 0, stream_>>>(
+      d_segs_, ntasks_, bpp, d_col_, X, Y, d_partial_, n_, npanels);
+  ++launches_;
+  if (nsplit_rows_) {
+    const int64_t total = static_cast<int64_t>(nsplit_rows_) * npanels * dev::Z;
+    dev::spmm_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
+        d_split_rows_, d_split_slot_begin_, nsplit_rows_, d_partial_, Y, n_, npanels);
+    ++launches_;
+  }
+  TCG_CUDA(cudaGetLastError());
+}
+
+// -------------------------------------------------------------------- eMA
+template <typename AccT, bool AL, bool RT, bool ST>
+static void launch_ema(const NodeExec& e, cudaStream_t s, int32_t n, const float* A,
+                       const float* P, const uint8_t* colors, float* out, double* root_out,
+                       double* root_acc, double* tile_tot) {
+  auto kern = dev::ema_tile<AccT, AL, RT, ST>;
+  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(e.ema_smem)));
+  const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
+  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca,
+                                                       e.Cp, e.Cs, n, out, root_out, root_acc,
+                                                       tile_tot);
+}
+
+template <bool AL, bool RT>
+static void launch_ema2(const NodeExec& e, cudaStream_t s, int32_t n, const float* A,
+                        const float* P, const uint8_t* colors, float* out, double* root_out,
+                        double* root_acc, double* tile_tot) {
+  if (e.ema_staged)
+    launch_ema<double, AL, RT, true>(e, s, n, A, P, colors, out, root_out, root_acc, tile_tot);
+  else
+    launch_ema<double, AL, RT, false>(e, s, n, A, P, colors, out, root_out, root_acc, tile_tot);
+}
+
+// ---------------------------------------------------------------- one DP
+void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc,
+                    tcg_node_stats* stats) {
+  std::vector<cudaEvent_t> ev;
+  auto mark = [&]() {
+    cudaEvent_t e;
+    TCG_CUDA(cudaEventCreate(&e));
+    TCG_CUDA(cudaEventRecord(e, stream_));
+    ev.push_back(e);
+    return ev.size() - 1;
+  };
+  const float* hist = nullptr;
+  if (need_hist_) {
+    float* H = table_ptr(hist_off_);
+    const int64_t warps = std::min<int64_t>(n_, 148LL * 64);
+    dev::nbr_hist<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream_>>>(
+        d_row_ptr_, d_col_, d_colors, n_, plan_.k, H);
+    ++launches_;
+    TCG_CUDA(cudaGetLastError());
+    hist = H;
+  }
+  struct Marks { size_t t0, t1, t2; };
+  std::vector<Marks> marks;
+  for (auto& e : exec_) {
+    Marks m{0, 0, 0};
+    if (stats) m.t0 = mark();
+    const float* P = hist;
+    if (!e.p_leaf) {
+      spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
+      P = table_ptr(e.pp_off);
+    }
+    if (stats) m.t1 = mark();
+    const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
+    float* out = e.root ? nullptr : table_ptr(e.out_off);
+    double* rout = e.root ? reinterpret_cast<double*>(arena_ + e.out_off) : nullptr;
+    if (e.root) {
+      if (e.a_leaf) launch_ema2<true, true>(e, stream_, n_, A, P, d_colors, out, rout, d_root_acc, d_tile_tot_);
+      else launch_ema2<false, true>(e, stream_, n_, A, P, d_colors, out, rout, d_root_acc, d_tile_tot_);
+    } else {
+      if (e.a_leaf) launch_ema2<true, false>(e, stream_, n_, A, P, d_colors, out, rout, nullptr, d_tile_tot_);
+      else launch_ema2<false, false>(e, stream_, n_, A, P, d_colors, out, rout, nullptr, d_tile_tot_);
+    }
+    ++launches_;
+    TCG_CUDA(cudaGetLastError());
+    if (stats) m.t2 = mark();
+    marks.push_back(m);
+  }
+  const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
+  if (n_ > 0) {
+    dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, ntiles, d_total);
+    ++launches_;
+  } else {
+    TCG_CUDA(cudaMemsetAsync(d_total, 0, sizeof(double), stream_));
+  }
+  TCG_CUDA(cudaGetLastError());
+  if (stats) {
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    const Binom& B = binom();
+    for (int i = 0; i < plan_.num_nodes; ++i) stats[i] = tcg_node_stats{};
+    for (size_t i = 0; i < exec_.size(); ++i) {
+      const NodeExec& e = exec_[i];
+      float s1 = 0, s2 = 0;
+      TCG_CUDA(cudaEventElapsedTime(&s1, ev[marks[i].t0], ev[marks[i].t1]));
+      TCG_CUDA(cudaEventElapsedTime(&s2, ev[marks[i].t1], ev[marks[i].t2]));
+      tcg_node_stats& st = stats[e.id];
+      st.spmm_seconds = s1 * 1e-3;
+      st.ema_seconds = s2 * 1e-3;
+      st.seconds = st.spmm_seconds + st.ema_seconds;
+      st.neighbor_passes = static_cast<uint64_t>(e.Cp);
+      st.traversals = static_cast<uint64_t>(e.Cp) * static_cast<uint64_t>(n_);
+      const uint64_t pairs_total = static_cast<uint64_t>(e.Cs) * static_cast<uint64_t>(B(e.size, e.sa));
+      st.flops = static_cast<uint64_t>(e.Cp) * static_cast<uint64_t>(nnz_) + 2ull * n_ * pairs_total;
+      st.spmm_bytes = 4ull * nnz_ + 8ull * (n_ + 1) + 8ull * n_ * static_cast<uint64_t>(e.Cp);
+      st.ema_bytes = 4ull * n_ * (static_cast<uint64_t>(e.Ca) + e.Cp) +
+                     (e.root ? 8ull * n_ : 4ull * n_ * static_cast<uint64_t>(e.Cs));
+      st.ema_flops = 2ull * n_ * pairs_total;
+    }
+  }
+  for (auto e : ev) cudaEventDestroy(e);
+}
+
+double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* per_vertex,
+                            tcg_node_stats* stats) {
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  ensure_arena();
+  if (colors_cap_ < n_) {
+    dfree(d_colors_);
+    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(n_, 1)));
+    colors_cap_ = n_;
+  }
+  if (host_colors) {
+    for (int32_t i = 0; i < n_; ++i)
+      if (host_colors[i] >= plan_.k) throw invalid_argument("coloring value out of range [0, k)");
+    TCG_CUDA(cudaMemcpyAsync(d_colors_, host_colors, n_, cudaMemcpyHostToDevice, stream_));
+  } else {
+    gen_colors(&seed, 1, d_colors_);
+  }
+  run_dp(d_colors_, d_scalars_, nullptr, stats);
+  double total = 0;
+  TCG_CUDA(cudaMemcpyAsync(&total, d_scalars_, sizeof(double), cudaMemcpyDeviceToHost, stream_));
+  const NodeExec& root = exec_.empty() ? NodeExec{} : exec_.back();
+  if (per_vertex && n_ > 0) {
+    if (exec_.empty()) {
+      // single-vertex template: every vertex counts once (k = 1)
+      for (int32_t i = 0; i < n_; ++i) per_vertex[i] = 1.0;
+    } else {
+      TCG_CUDA(cudaMemcpyAsync(per_vertex, arena_ + root.out_off, sizeof(double) * n_,
+                               cudaMemcpyDeviceToHost, stream_));
+    }
+  }
+  if (cfg_.flags & TCG_KEEP_TABLES) {
+    last_colors_.resize(n_);
+    TCG_CUDA(cudaMemcpyAsync(last_colors_.data(), d_colors_, n_, cudaMemcpyDeviceToHost, stream_));
+  }
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+  if (exec_.empty()) total = static_cast<double>(n_);
+  tables_valid_ = true;
+  if (!std::isfinite(total)) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
+  return total;
+}
+
+void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est, double* se,
+                      double* per_vertex_est) {
+  if (iterations < 1) throw invalid_argument("iterations must be >= 1");
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  ensure_arena();
+  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+      {static_cast<int64_t>(iterations), 1024, std::max<int64_t>(1, (int64_t{1} << 30) / std::max(n_, 1))})));
+  if (colors_cap_ < static_cast<int64_t>(chunk) * n_) {
+    dfree(d_colors_);
+    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(static_cast<int64_t>(chunk) * n_, 1)));
+    colors_cap_ = static_cast<int64_t>(chunk) * n_;
+  }
+  double* d_totals = nullptr;
+  double* d_acc = nullptr;
+  TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * iterations));
+  try {
+    if (per_vertex_est && !exec_.empty()) {
+      TCG_CUDA(cudaMalloc(&d_acc, sizeof(double) * std::max(n_, 1)));
+      TCG_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(double) * std::max(n_, 1), stream_));
+    }
+    std::vector<uint64_t> seeds(chunk);
+    for (int i0 = 0; i0 < iterations; i0 += chunk) {
+      const int c = std::min(chunk, iterations - i0);
+      for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
+      gen_colors(seeds.data(), c, d_colors_);
+      for (int j = 0; j < c; ++j)
+        run_dp(d_colors_ + static_cast<int64_t>(j) * n_, d_totals + i0 + j, d_acc, nullptr);
+    }
+    TCG_CUDA(cudaMemcpyAsync(totals, d_totals, sizeof(double) * iterations, cudaMemcpyDeviceToHost, stream_));
+    std::vector<double> acc;
+    if (d_acc) {
+      acc.resize(n_);
+      TCG_CUDA(cudaMemcpyAsync(acc.data(), d_acc, sizeof(double) * n_, cudaMemcpyDeviceToHost, stream_));
+    }
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    if (exec_.empty())
+      for (int i = 0; i < iterations; ++i) totals[i] = static_cast<double>(n_);
+    // estimator.hpp:80-91, same arithmetic order
+    double mean = 0.0;
+    for (int i = 0; i < iterations; ++i) mean += totals[i];
+    mean /= static_cast<double>(iterations);
+    double var = 0.0;
+    for (int i = 0; i < iterations; ++i) var += (totals[i] - mean) * (totals[i] - mean);
+    const double scale = 1.0 / (static_cast<double>(aut_) * colorful_probability(plan_.k));
+    *est = mean * scale;
+    *se = iterations > 1 ? std::sqrt(var / (static_cast<double>(iterations) *
+                                            static_cast<double>(iterations - 1))) * scale
+                         : 0.0;
+    if (per_vertex_est) {
+      for (int32_t v = 0; v < n_; ++v)
+        per_vertex_est[v] = (exec_.empty() ? 1.0 : acc[v] / iterations) * scale;
+    }
+    for (int i = 0; i < iterations; ++i)
+      if (!std::isfinite(totals[i])) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
+  } catch (...) {
+    dfree(d_totals);
+    dfree(d_acc);
+    throw;
+  }
+  dfree(d_totals);
+  dfree(d_acc);
+  tables_valid_ = false;
+}
+
+// ------------------------------------------------------------ inspection
+static void unpanel(const std::vector<float>& panels, int64_t n, int64_t C, double* out) {
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t c = 0; c < C; ++c)
+      out[v * C + c] = panels[((c / dev::Z) * n + v) * dev::Z + c % dev::Z];
+}
+
+void Engine::node_table(int id, int which, double* out) {
+  if (!(cfg_.flags & TCG_KEEP_TABLES)) throw invalid_argument("context not created with TCG_KEEP_TABLES");
+  if (!tables_valid_) throw invalid_argument("no coloring has been run since the last change");
+  if (id < 0 || id >= plan_.num_nodes) throw invalid_argument("node id out of range");
+  const int64_t n = n_, k = plan_.k;
+  if (plan_.is_leaf(id)) {
+    if (which == 0) {
+      std::fill(out, out + n * k, 0.0);
+      for (int64_t v = 0; v < n; ++v) out[v * k + last_colors_[v]] = 1.0;
+      return;
+    }
+    if (hist_off_ < 0) throw invalid_argument("no neighbour histogram in this plan");
+    std::vector<float> h((k + dev::Z - 1) / dev::Z * n * dev::Z);
+    TCG_CUDA(cudaMemcpy(h.data(), arena_ + hist_off_, h.size() * 4, cudaMemcpyDeviceToHost));
+    unpanel(h, n, k, out);
+    return;
+  }
+  const int64_t C = binom()(plan_.k, plan_.size[id]);
+  if (id == plan_.full_node()) {
+    if (which != 0) throw invalid_argument("the root has no SpMM output");
+    TCG_CUDA(cudaMemcpy(out, arena_ + table_off_[id], sizeof(double) * n, cudaMemcpyDeviceToHost));
+    return;
+  }
+  const int64_t off = which == 0 ? table_off_[id] : pprime_off_[id];
+  if (off < 0) throw invalid_argument("table not available for this node");
+  std::vector<float> t((C + dev::Z - 1) / dev::Z * n * dev::Z);
+  TCG_CUDA(cudaMemcpy(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost));
+  unpanel(t, n, C, out);
+}
+
+void Engine::spmm_host(const float* x, int cols, float* y) {
+  if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
+  if (cols < 1) throw invalid_argument("cols must be >= 1");
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  const int64_t n = n_, panels = (cols + dev::Z - 1) / dev::Z;
+  std::vector<float> xp(panels * n * dev::Z, 0.f);
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t c = 0; c < cols; ++c) xp[((c / dev::Z) * n + v) * dev::Z + c % dev::Z] = x[v * cols + c];
+  float *dx = nullptr, *dy = nullptr;
+  double* saved_partial = d_partial_;
+  double* dp = nullptr;
+  try {
+    TCG_CUDA(cudaMalloc(&dx, std::max<size_t>(xp.size() * 4, 4)));
+    TCG_CUDA(cudaMalloc(&dy, std::max<size_t>(xp.size() * 4, 4)));
+    if (nsplit_slots_) TCG_CUDA(cudaMalloc(&dp, static_cast<size_t>(nsplit_slots_) * panels * dev::Z * 8));
+    TCG_CUDA(cudaMemcpy(dx, xp.data(), xp.size() * 4, cudaMemcpyHostToDevice));
+    d_partial_ = dp;
+    spmm(dx, dy, cols);
+    d_partial_ = saved_partial;
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    TCG_CUDA(cudaMemcpy(xp.data(), dy, xp.size() * 4, cudaMemcpyDeviceToHost));
+  } catch (...) {
+    d_partial_ = saved_partial;
+    dfree(dx); dfree(dy); dfree(dp);
+    throw;
+  }
+  dfree(dx); dfree(dy); dfree(dp);
+  for (int64_t v = 0; v < n; ++v)
+    for (int64_t c = 0; c < cols; ++c) y[v * cols + c] = xp[((c / dev::Z) * n + v) * dev::Z + c % dev::Z];
+}
+
+}  // namespace tcg

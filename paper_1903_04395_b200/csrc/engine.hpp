@@ -1,0 +1,115 @@
+// engine.hpp -- the per-GPU DP engine behind the C ABI (include/tcg.h).
+//
+// Drop-in for the reference's vectorized engine: IterationRun::run
+// (engines.hpp:106-132) + vectorized_node (224-268), with the count tables
+// resident in HBM as fp32 panels (kernels.cuh) and the root in fp64.
+// Device memory for one coloring is planned once per (graph, template) by
+// simulating the reference's liveness rule (engines.hpp:149-151,
+// count_table.hpp:113-133) over a single arena, so a coloring performs no
+// allocation and its launch sequence is fixed.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/tcg.h"
+#include "host.hpp"
+#include "layout.hpp"
+
+namespace tcg {
+
+struct NodeExec {
+  int id = -1, a = -1, p = -1;
+  int size = 0, sa = 0, sp = 0;
+  int32_t Cs = 0, Ca = 0, Cp = 0;
+  int pairs = 0;
+  bool a_leaf = false, p_leaf = false, root = false;
+  int2* d_split = nullptr;   // by-parent (I_a, I_p) pairs, [Cs * pairs]
+  int64_t out_off = -1;      // arena offset of M_s (root: fp64 n)
+  int64_t pp_off = -1;       // arena offset of P' (passive internal child)
+  size_t ema_smem = 0;
+  bool ema_staged = true;
+};
+
+class Engine {
+ public:
+  explicit Engine(const tcg_config& cfg);
+  ~Engine();
+
+  void set_graph(const Csr& g);
+  void set_template(int k, const int32_t* edges, int root);
+  int64_t required_bytes() const;
+  const Plan& plan() const { return plan_; }
+  uint64_t aut() const { return aut_; }
+  int32_t n() const { return n_; }
+
+  void coloring(uint64_t seed, uint8_t* host_colors);
+  double run_coloring(uint64_t seed, const uint8_t* host_colors, double* per_vertex,
+                      tcg_node_stats* stats);
+  void estimate(uint64_t seed, int iterations, double* totals, double* est, double* se,
+                double* per_vertex_est);
+  void node_table(int node_id, int which, double* out);
+  void spmm_host(const float* x, int cols, float* y);
+  void set_rejection_limit(uint64_t limit) { limit_override_ = limit; }
+  int64_t launches() const { return launches_; }
+
+ private:
+  void require_ready() const;
+  void release_graph();
+  void release_template();
+  void plan_arena();
+  void ensure_arena();
+  void gen_colors(const uint64_t* seeds, int count, uint8_t* d_out);
+  // one DP over d_colors; total written to d_total (device), optional root accumulation
+  void run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc,
+              tcg_node_stats* stats);
+  void spmm(const float* X, float* Y, int cols);
+  float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
+  int64_t table_bytes(int64_t cols) const;
+
+  tcg_config cfg_{};
+  cudaStream_t stream_ = nullptr;
+  int64_t launches_ = 0;
+  uint64_t limit_override_ = 0;
+
+  // graph
+  int32_t n_ = -1;
+  int64_t nnz_ = 0;
+  int64_t* d_row_ptr_ = nullptr;
+  int32_t* d_col_ = nullptr;
+  dev::Seg* d_segs_ = nullptr;
+  int64_t ntasks_ = 0;
+  int32_t* d_split_rows_ = nullptr;
+  int32_t* d_split_slot_begin_ = nullptr;
+  int nsplit_rows_ = 0, nsplit_slots_ = 0;
+
+  // template / plan
+  bool have_template_ = false;
+  Template tpl_;
+  Plan plan_;
+  uint64_t aut_ = 1;
+  std::vector<NodeExec> exec_;     // internal nodes in dp order
+  bool need_hist_ = false;
+
+  // arena + per-coloring buffers
+  int64_t arena_bytes_ = 0;
+  int64_t hist_off_ = -1;
+  std::vector<int64_t> table_off_;   // per node id: arena offset of its table (internal)
+  std::vector<int64_t> pprime_off_;  // per node id: offset of P' computed from it
+  char* arena_ = nullptr;
+  int64_t arena_alloc_ = 0;
+  double* d_partial_ = nullptr;
+  int64_t partial_bytes_ = 0, partial_alloc_ = 0;
+  double* d_tile_tot_ = nullptr;
+  double* d_scalars_ = nullptr;      // [0] total of run_coloring
+  uint8_t* d_colors_ = nullptr;      // color batch
+  int64_t colors_cap_ = 0;
+  uint64_t* d_seeds_ = nullptr;
+  std::vector<uint8_t> last_colors_;
+  bool tables_valid_ = false;
+};
+
+}  // namespace tcg

@@ -1,0 +1,206 @@
+"""CPU tests of the product's host side (no GPU): the C ABI library loads and
+exports every declared symbol, and the C++ host subsystems (CSR build, R-MAT
+input generator, template validation/partition, |Aut|, combinadic split
+tables, estimate_bytes) agree with the pinned oracle bit for bit."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import oracle as O
+import paper_1903_04395_b200 as T
+from paper_1903_04395_b200 import _native as N
+from conftest import CFG_TEMPLATES, parents_to_edges
+
+
+def test_library_exports_every_header_symbol():
+    syms = N.header_symbols()
+    assert len(syms) >= 30
+    missing = [s for s in syms if not hasattr(N.lib, s)]
+    assert not missing, missing
+
+
+def test_version_string_names_sm100a():
+    assert b"sm_100a" in N.lib.tcg_version()
+
+
+def _csr_eq(g, ref):
+    n, rp, col = ref
+    return g.n == n and np.array_equal(g.csc_col_ptr, rp) and np.array_equal(g.csc_rows, col)
+
+
+def test_from_edges_matches_oracle_random():
+    rng = np.random.default_rng(1)
+    for trial in range(30):
+        n = int(rng.integers(1, 500))
+        m = int(rng.integers(0, 4 * n))
+        e = rng.integers(0, n, size=(m, 2)).astype(np.int32)
+        hint = n if trial % 2 else -1
+        if m == 0 and hint < 0:
+            continue
+        assert _csr_eq(T.from_edges(e, hint), O.csr_from_edges(e, hint)), trial
+
+
+def test_from_edges_spec_examples():
+    # test_graph.cpp:48-64: K3, single edge, path; self-loops and duplicates dropped
+    g = T.from_edges([(0, 1), (1, 2), (2, 0)])
+    assert g.csc_col_ptr.tolist() == [0, 2, 4, 6] and g.csc_rows.tolist() == [1, 2, 0, 2, 0, 1]
+    g = T.from_edges([(0, 1), (1, 0), (1, 1), (0, 1)])
+    assert g.m == 1 and g.csc_rows.tolist() == [1, 0]
+    g = T.from_edges([(0, 1)], 5)
+    assert g.n == 5 and g.degree(4) == 0
+
+
+def test_from_edges_rejects_out_of_range():
+    with pytest.raises(T.ParseError):
+        T.from_edges([(0, 7)], 5)
+    with pytest.raises(T.ParseError):
+        T.from_edges([(-1, 2)])
+
+
+def test_graph_from_csr_validates():
+    g = T.Graph.from_csr(3, [0, 2, 4, 6], [1, 2, 0, 2, 0, 1])
+    assert g.m == 3
+    with pytest.raises(T.ParseError):
+        T.Graph.from_csr(2, [0, 1, 1], [1])          # not symmetric
+    with pytest.raises(T.ParseError):
+        T.Graph.from_csr(2, [0, 1, 2], [0, 1])       # self loops
+    with pytest.raises(T.ParseError):
+        T.Graph.from_csr(3, [0, 2, 3, 4], [2, 1, 0, 0])  # unsorted row
+
+
+@pytest.mark.parametrize("scale,ef,probs,seed", [
+    (10, 16, (.57, .19, .19, .05), 1), (12, 8, (.45, .15, .15, .25), 3), (7, 100, (.25, .25, .25, .25), 9)])
+def test_rmat_matches_oracle(scale, ef, probs, seed):
+    g = T.generate_rmat(T.RmatSpec(scale, ef << scale, *probs, seed))
+    assert _csr_eq(g, O.generate_rmat(scale, ef << scale, *probs, seed))
+
+
+def test_rmat_spec_validation():
+    with pytest.raises(T.ParseError):
+        T.generate_rmat(T.RmatSpec(0, 10, .25, .25, .25, .25, 1))
+    with pytest.raises(T.ParseError):
+        T.generate_rmat(T.RmatSpec(5, 10, .5, .25, .25, .25, 1))
+
+
+def test_template_validation():
+    with pytest.raises(T.ParseError):
+        T.make_template([(0, 1), (1, 2), (2, 0)])    # cycle: 3 edges for 3 vertices
+    with pytest.raises(T.ParseError):
+        T.make_template([(0, 1), (2, 3), (3, 4)])    # wrong edge count / disconnected
+    with pytest.raises(T.ParseError):
+        T.make_template([(0, 0)])
+    with pytest.raises(T.ParseError):
+        T.make_template([(0, 1)], 5)
+    # default root = max degree, smallest id (templates.hpp:67-74)
+    assert T.make_template([(0, 1), (1, 2), (1, 3)]).root == 1
+    assert T.template_from_parents(CFG_TEMPLATES["cfg2"], -1).root == 1  # SURVEY finding 9
+
+
+def test_partition_matches_oracle_and_golden(kats):
+    for name, parents in CFG_TEMPLATES.items():
+        for root in (0, -1):
+            want = kats["plans"][f"{name}_root{root}"]
+            t = T.template_from_parents(parents, root)
+            p = T.partition(t)
+            assert p.root == want["root"]
+            assert [nd.size for nd in p.nodes] == want["size"]
+            assert [nd.active_child for nd in p.nodes] == want["active"]
+            assert [nd.passive_child for nd in p.nodes] == want["passive"]
+            assert p.dp_order == want["dp_order"]
+            assert T.automorphism_count(t) == want["aut"]
+            assert T.estimate_bytes(p, 1000) == want["estimate_bytes_n1000"]
+
+
+def test_partition_and_aut_random_trees():
+    rng = np.random.default_rng(5)
+    for trial in range(200):
+        k = int(rng.integers(1, 21))
+        parents = [-1] + [int(rng.integers(0, v)) for v in range(1, k)]
+        e = parents_to_edges(parents)
+        if k == 1:
+            continue
+        root = int(rng.integers(-1, k))
+        op = O.partition(k, e, root)
+        t = T.make_template(e, root)
+        p = T.partition(t)
+        assert p.dp_order == list(op.dp_order)[:op.num_nodes]
+        assert [nd.size for nd in p.nodes] == list(op.size)[:op.num_nodes]
+        assert [nd.root for nd in p.nodes] == list(op.node_root)[:op.num_nodes]
+        assert T.automorphism_count(t) == O.automorphisms(k, e)
+
+
+def test_aut_brute_force_small():
+    from itertools import permutations
+    rng = np.random.default_rng(8)
+    for trial in range(30):
+        k = int(rng.integers(2, 8))
+        parents = [-1] + [int(rng.integers(0, v)) for v in range(1, k)]
+        e = parents_to_edges(parents)
+        es = {frozenset(x) for x in e}
+        brute = sum(all(frozenset((p[u], p[v])) in es for u, v in e) for p in permutations(range(k)))
+        assert T.automorphism_count(T.make_template(e, 0)) == brute
+
+
+def test_split_tables_match_oracle():
+    for k in range(2, 13):
+        ix = T.ColorIndexer(k)
+        for ps in range(2, k + 1):
+            for as_ in range(1, ps):
+                if ix.num_sets(ps) * ix.binom(ps, as_) > 200000:
+                    continue
+                st = T.build_split_table(ps, as_, ix)
+                o = O.split_table(k, ps, as_)
+                assert np.array_equal(st.active_index, o["active_index"])
+                assert np.array_equal(st.passive_index, o["passive_index"])
+                assert np.array_equal(st.grouped_parent, o["grouped_parent"])
+                assert np.array_equal(st.grouped_active, o["grouped_active"])
+
+
+def test_split_table_rejects_empty_child():
+    ix = T.ColorIndexer(3)
+    with pytest.raises(T.ParseError):
+        T.build_split_table(2, 2, ix)
+    with pytest.raises(T.ParseError):
+        T.build_split_table(2, 0, ix)
+
+
+def test_color_indexer():
+    ix = T.ColorIndexer(3)
+    assert ix.index_of([0, 1]) == 0 and ix.index_of([0, 2]) == 1 and ix.index_of([1, 2]) == 2
+    assert ix.set_of(2, 2) == [1, 2]
+    with pytest.raises(T.ParseError):
+        ix.index_of([1, 1])
+    with pytest.raises(T.ParseError):
+        ix.set_of(3, 2)
+    with pytest.raises(T.ParseError):
+        T.ColorIndexer(21)
+    assert T.ColorIndexer(20).binom(20, 10) == 184756
+    for k in range(1, 11):
+        ix = T.ColorIndexer(k)
+        for h in range(1, k + 1):
+            for i in range(ix.num_sets(h)):
+                assert ix.index_of(ix.set_of(i, h)) == i
+
+
+def test_colorful_probability():
+    import math
+    for k in range(1, 21):
+        assert T.colorful_probability(k) == O.colorful_probability(k)
+        assert abs(T.colorful_probability(k) - math.factorial(k) / k ** k) < 1e-12
+
+
+def test_engine_requires_gpu_or_fails_loudly():
+    """Without a usable B200 the device engine refuses with a CUDA/EINVAL
+    status -- there is no CPU fallback."""
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("GPU present")
+    with pytest.raises((T.CudaError, T.ParseError)):
+        T.Context(0)
+
+
+def test_non_b200_engine_kinds_refused():
+    g = T.from_edges([(0, 1)])
+    with pytest.raises(T.ParseError):
+        T.estimate(g, T.make_template([(0, 1)], 0), T.EngineKind.vectorized, 1, 1)
