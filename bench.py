@@ -1,0 +1,351 @@
+#!/usr/bin/env python
+"""bench.py -- per-coloring time of the pruned color-coding DP (PGBSC) on B200.
+
+Metric (BASELINE.json): "per-coloring time and SpMM+eMA HBM GB/s (k=12/17
+trees, R-MAT), 1/2/4/8 GPU".  A STEP is one coloring: on-device MT19937-64
+coloring, the neighbour histogram, every internal node's SpMM + fused eMA,
+and the fp64 root total -- one full pass of the hot path.
+
+  python bench.py [--config cfg3] [--gpus N] [--steps K] [--warmup W]
+  python bench.py --impl reference ...      (the reference CPU engine, sampled)
+
+Multi-GPU (torchrun, one rank per GPU): colorings are independent units, so
+every rank runs its own K colorings (seeds offset by rank) on a replica of the
+graph -- weak scaling, no data-path collective.  `value` is the whole-job
+per-coloring time: max-over-ranks device time / (N * K).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "per-coloring time and SpMM+eMA HBM GB/s (k=12/17 trees, R-MAT), 1/2/4/8 GPU"
+
+CONFIGS = {
+    # name: (rmat spec (scale, edges, a, b, c, d, seed), template parent array, colorings per estimate)
+    "cfg2": ((20, 16 << 20, .57, .19, .19, .05, 1), [-1, 0, 0, 1, 1, 2, 2], 10,
+             "R-MAT scale 20 ef16 (.57,.19,.19,.05), k=7 complete binary tree"),
+    "cfg3": ((20, 100 << 20, .45, .15, .15, .25, 1), [-1, 0, 1, 2, 0, 4, 4, 6, 0, 8, 9, 9], 3,
+             "R-MAT scale 20 ef100 (.45,.15,.15,.25), k=12 tree"),
+    "cfg5": ((20, 100 << 20, .45, .15, .15, .25, 1),
+             [-1, 0, 1, 2, 3, 4, 0, 6, 7, 8, 0, 10, 11, 11, 0, 14, 15], 1,
+             "R-MAT scale 20 ef100 (.45,.15,.15,.25), k=17 tree"),
+}
+DEFAULT_CONFIG = "cfg3"
+L2_GATHER_PEAK_GBS = 15400.0  # measured: 64 B row gathers from a 64 MB L2-resident panel (profiles/r01_membench.txt)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def ncu_traffic(config):
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p)).get(config)
+        if d:
+            return d
+    return None
+
+
+class Clocks:
+    """nvidia-smi sampled DURING the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, device):
+        self.proc = None
+        self.device = device
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), "--query-gpu=clocks.sm,clocks.max.sm,power.draw,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        self.rows = []
+        if self.proc is None:
+            return False
+        time.sleep(0.2)
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) >= 7:
+                self.rows.append(f)
+        return False
+
+    def summary(self):
+        if not getattr(self, "rows", None):
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        load = [x for x in sm if x > 500] or sm
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(load) if load else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_init():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        backend = "nccl" if torch.cuda.is_available() else "gloo"
+        if backend == "nccl":
+            torch.cuda.set_device(local)
+        dist.init_process_group(backend)
+        return rank, world, local, dist
+    return rank, world, local, None
+
+
+def allreduce_max(dist, x, local):
+    if dist is None:
+        return x
+    import torch
+    dev = f"cuda:{local}" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(dist, local):
+    if dist is not None:
+        dist.barrier()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.synchronize(local)
+    except Exception:
+        pass
+
+
+def build_graph(spec):
+    import paper_1903_04395_b200 as T
+    t0 = time.perf_counter()
+    g = T.generate_rmat(T.RmatSpec(*spec))
+    log(f"[bench] graph n={g.n} nnz={g.nnz()} max_deg={g.max_degree} built in {time.perf_counter() - t0:.1f}s (host C++)")
+    return g
+
+
+def cpu_reference(g, parents, seed, reps=1, pairs=32):
+    """The UNMODIFIED reference engine (oracle/_ref), sampled (ref_driver.cpp ref_time_sampled)."""
+    import numpy as np
+    import oracle as O
+    t0 = time.perf_counter()
+    rg = O.RefGraph.from_csr(g.n, g.csc_col_ptr, g.csc_rows)
+    log(f"[bench] reference Graph wrapped in {time.perf_counter() - t0:.1f}s")
+    k = len(parents)
+    e = np.array(O.parent_array_edges(parents), np.int32).reshape(-1)
+    out = np.zeros(8)
+    cores = os.cpu_count() or 1
+    rc = O.ref().ref_time_sampled(rg.h, k, e, 0, seed, cores, reps, pairs, out)
+    if rc != 0:
+        raise RuntimeError("reference sampled timing failed")
+    return dict(ms=out[0] * 1e3, spmm_ms=out[1] * 1e3, ema_ms=out[2] * 1e3, sample_wall_s=out[3],
+                t16_s=out[4], t1_s=out[5], t_pair_s=out[6], misc_s=out[7], cores=cores), rg
+
+
+def ref_sample_desc(k):
+    return ("reference vectorized engine (oracle/_ref, -O3, fp64, Z=16, WorkerPool=all host threads): "
+            "one full-graph SpMM batch of 16 and of 1 column, 32 ema() column pairs, random_coloring and "
+            f"init_leaf_table timed in full, then summed over the k={k} plan's batches/pairs "
+            "(ref_driver.cpp ref_time_sampled)")
+
+
+def run_reference(args, rank, world, local, dist):
+    spec, parents, ncol, desc = CONFIGS[args.config]
+    if rank != 0:
+        return
+    try:
+        import oracle as O
+        if not O.ref_available():
+            O.build(ref=True)
+        if not O.ref_available():
+            print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtcref.so not built"}))
+            return
+    except Exception as ex:  # noqa: BLE001
+        print(json.dumps({"impl": "reference", "unavailable": f"{type(ex).__name__}: {ex}"}))
+        return
+    g = build_graph(spec)
+    vals = []
+    rg = None
+    for i in range(args.warmup + args.steps):
+        r, rg = cpu_reference(g, parents, 1 + i) if rg is None else (cpu_reference(g, parents, 1 + i)[0], rg)
+        if i >= args.warmup:
+            vals.append(r)
+        log(f"[bench] reference step {i}: {r['ms']:.1f} ms/coloring (sample wall {r['sample_wall_s']:.1f}s)")
+    v = statistics.mean(x["ms"] for x in vals)
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/coloring",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+        "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic R-MAT from the reference generator (graph seed 1)",
+        "config": {"workload": f"{args.config}: {desc}", "n": g.n, "nnz": g.nnz(), "k": len(parents)},
+        "cpu_baseline": {"value": v, "unit": "ms/coloring", "cores": vals[0]["cores"], "kind": "reference",
+                         "sample": ref_sample_desc(len(parents)),
+                         "spmm_ms": statistics.mean(x["spmm_ms"] for x in vals),
+                         "ema_ms": statistics.mean(x["ema_ms"] for x in vals)},
+        "e2e": {"value": v, "unit": "ms/coloring", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_b200(args, rank, world, local, dist):
+    import numpy as np
+    import paper_1903_04395_b200 as T
+    spec, parents, ncol, desc = CONFIGS[args.config]
+    g = build_graph(spec)
+    t = T.template_from_parents(parents, 0)
+    ctx = T.Context(device=local)
+    ctx.set_graph(g)
+    ctx.set_template(t)
+    need = ctx.required_device_bytes()
+    log(f"[bench] rank {rank}: device bytes {need / 1e9:.2f} GB")
+    seed0 = 1 + rank * (args.warmup + args.steps)
+    ctx.time(seed0, args.warmup, per_kernel=False)               # warm-up colorings
+    barrier(dist, local)
+    l0 = ctx.kernel_launches()
+    with Clocks(local) as clk:
+        tm, totals = ctx.time(seed0 + args.warmup, args.steps, per_kernel=True)
+    barrier(dist, local)
+    launches = ctx.kernel_launches() - l0
+    ms_max = allreduce_max(dist, tm.total_ms, local)
+    value = ms_max / (args.steps * world)
+
+    # end to end through the public C ABI with HOST buffers: one estimate()
+    # call per step = H2D of the CSR + `ncol` colorings + D2H of the totals and
+    # per-vertex estimates
+    e2e = None
+    if not args.no_e2e:
+        rp = np.ascontiguousarray(g.csc_col_ptr)
+        cl = np.ascontiguousarray(g.csc_rows)
+        ectx = T.Context(device=local)
+        ectx.set_template(t)
+        ectx.set_graph_csr(g.n, rp, cl)
+        ectx.estimate(1, 1)                                       # warm (allocations)
+        barrier(dist, local)
+        e_steps = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        for i in range(e_steps):
+            ectx.set_graph_csr(g.n, rp, cl)
+            tot, est, se, pv = ectx.estimate(1 + i * ncol, ncol, per_vertex=True)
+        e_s = time.perf_counter() - t0
+        barrier(dist, local)
+        e_s = allreduce_max(dist, e_s, local)
+        e2e = {"value": e_s * 1e3 / (e_steps * ncol * world), "unit": "ms/coloring",
+               "h2d_bytes_per_step": int(rp.nbytes + cl.nbytes + 8),
+               "d2h_bytes_per_step": int(8 * ncol + 8 * g.n),
+               "colorings_per_step": ncol, "steps": e_steps,
+               "note": "one tcg_estimate per step (host CSR -> device, colorings, totals + per-vertex estimate -> host); host wall clock, max over ranks"}
+        del ectx
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            import oracle as O
+            if not O.ref_available():
+                O.build(ref=True)
+            if O.ref_available():
+                r, _ = cpu_reference(g, parents, 1)
+                cpu = {"value": r["ms"], "unit": "ms/coloring", "cores": r["cores"], "kind": "reference",
+                       "sample": ref_sample_desc(len(parents)), "spmm_ms": r["spmm_ms"], "ema_ms": r["ema_ms"]}
+            else:
+                cpu = {"value": None, "unit": "ms/coloring", "cores": 0, "kind": "reference",
+                       "sample": "oracle/_ref not built on this host"}
+        except Exception as ex:  # noqa: BLE001
+            cpu = {"value": None, "unit": "ms/coloring", "cores": 0, "kind": "reference", "sample": f"failed: {ex}"}
+
+    if rank != 0:
+        return
+    hbm_peak, peak_src = peaks()
+    spmm_gbs = tm.spmm_alg_bytes / (tm.spmm_ms * 1e-3) / 1e9 if tm.spmm_ms else None
+    per_launch_bytes = tm.spmm_alg_bytes / max(tm.spmm_launches, 1)
+    per_launch_ms = tm.spmm_ms / max(tm.spmm_launches, 1)
+    traffic = ncu_traffic(args.config)
+    gathered_gbs = tm.spmm_gathered_bytes / (tm.spmm_ms * 1e-3) / 1e9 if tm.spmm_ms else None
+    ema_gbs = tm.ema_alg_bytes / (tm.ema_ms * 1e-3) / 1e9 if tm.ema_ms else None
+    line = {
+        "metric": METRIC, "value": value, "unit": "ms/coloring", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": False,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32 tables, f64 accumulate/root",
+        "data": "synthetic R-MAT from the reference generator (graph seed 1), colorings seeds 1.. on device",
+        "config": {"workload": f"{args.config}: {desc}", "n": g.n, "nnz": g.nnz(), "k": len(parents),
+                   "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
+                   "l2": "inputs larger than L2 (CSR %.0f MB + count tables %.1f GB vs 126 MB L2)"
+                         % ((g.csc_col_ptr.nbytes + g.csc_rows.nbytes) / 1e6, need / 1e9)},
+        "roofline": {"kernel": "spmm_panels (+fixup)", "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": spmm_gbs / hbm_peak if spmm_gbs else None,
+                     "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+                     "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
+                     "launches": tm.spmm_launches, "peak_source": peak_src,
+                     "note": "achieved = SURVEY 8(d) compulsory bytes (4 nnz + 8(n+1) + 8 n C_p) / CUDA-event time; "
+                             "the panel gathers are L2->SM bound, see l2_gather",
+                     "l2_gather": {"achieved": gathered_gbs, "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
+                                   "frac": gathered_gbs / L2_GATHER_PEAK_GBS if gathered_gbs else None,
+                                   "bytes": "nnz * 64 B * panels per launch"},
+                     "ema": {"achieved_gbs": ema_gbs, "frac_hbm": ema_gbs / hbm_peak if ema_gbs else None,
+                             "tflops": tm.ema_flops / (tm.ema_ms * 1e-3) / 1e12 if tm.ema_ms else None,
+                             "ms_per_coloring": tm.ema_ms / args.steps}},
+        "phase_ms_per_coloring": {"spmm": tm.spmm_ms / args.steps, "ema": tm.ema_ms / args.steps,
+                                  "other": (tm.total_ms - tm.spmm_ms - tm.ema_ms) / args.steps},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "totals_finite": bool(np.all(np.isfinite(totals))),
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["b200", "reference"], default="b200")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        log("[bench] warmup raised to 3 (timing rules)")
+        args.warmup = 3
+    rank, world, local, dist = dist_init()
+    try:
+        if args.impl == "reference":
+            run_reference(args, rank, world, local, dist)
+        else:
+            run_b200(args, rank, world, local, dist)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -172,6 +172,25 @@ int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y);
 /* Test hook: override the rejection threshold (UINT64_MAX/k)*k of
  * Rng::below (rng.hpp:21-27); 0 restores the reference value. */
 int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit);
+/* Device-timed batch of colorings (bench.py's timed region): colorings
+ * seed..seed+count-1 generated on device and run back to back on the
+ * engine's stream, bracketed by CUDA events recorded ON THAT STREAM.  With
+ * per_kernel != 0 every SpMM / eMA launch is additionally bracketed so the
+ * phase times below are measured (otherwise they are 0).  Rooted totals
+ * land in totals[count] (nullable). */
+typedef struct {
+  double total_ms;            /* device time of the whole batch */
+  double spmm_ms, ema_ms;     /* summed over launches (per_kernel) */
+  int64_t spmm_launches, ema_launches, launches;
+  double spmm_alg_bytes;      /* 4 nnz + 8 (n+1) + 8 n C_p per internal passive */
+  double hist_alg_bytes;      /* leaf passives: 4 nnz + 8 (n+1) + n + 4 n k, once per coloring */
+  double ema_alg_bytes;       /* 4 n (C_a + C_p + C_s), root writes 8 n */
+  double ema_flops;           /* 2 n C_s C(|T_s|,|T_a|) */
+  double spmm_gathered_bytes; /* bytes moved L2 -> SM by the panel gathers: nnz * 64 B * panels */
+} tcg_timing;
+int tcg_time_colorings(tcg_ctx* ctx, uint64_t seed, int count, int per_kernel, double* totals,
+                       tcg_timing* out);
+
 /* Kernel launches issued by this context since creation (evidence for
  * bench.py's gpu_launches). */
 int64_t tcg_kernel_launches(const tcg_ctx* ctx);

@@ -203,15 +203,20 @@ int ref_estimate(const void* gp, int k, const int32_t* edges, int root, int iter
 }
 
 // Bounded-sample timing of one vectorized coloring for the CPU baseline.
-// Replays engines.hpp:224-268 through the reference's own public kernels
-// (load_batch / spmm_csc / ema) and WorkerPool: for every internal node the
-// first `max_batches` Z=16 SpMM batches over ALL rows and the first
-// `max_pairs` eMA column pairs over ALL rows are timed, then extrapolated
-// linearly to the node's full batch / pair count.  Random coloring and leaf
-// init are timed in full.  out[0] = extrapolated s/coloring, out[1] = SpMM s,
-// out[2] = eMA s, out[3] = measured wall seconds of the sample itself.
+//
+// The reference engine's per-coloring cost is a sum of identical units
+// (engines.hpp:224-268): every SpMM batch is load_batch + spmm_csc over the
+// whole graph for zc <= Z=16 columns, and every eMA column pair is one
+// pool-dispatched ema() over n rows.  So the sample times, through the
+// reference's own kernels and WorkerPool, `reps` full-graph batches of Z=16
+// and of 1 column, and `pairs` ema() dispatches, plus random_coloring and one
+// init_leaf_table in full; the coloring is then
+//   sum_nodes [ sum_batches t(zc) ] + pairs_total * t_pair + t_color + k * t_leaf
+// with t(zc) interpolated linearly between t(1) and t(16).
+// out[0] = estimated s/coloring, [1] SpMM s, [2] eMA s, [3] wall s of the
+// sample, [4] t(16), [5] t(1), [6] t_pair, [7] t_color + k*t_leaf.
 int ref_time_sampled(const void* gp, int k, const int32_t* edges, int root, uint64_t seed,
-                     int workers, int max_batches, int max_pairs, double* out) {
+                     int workers, int reps, int pairs_sample, double* out) {
   try {
     const Graph& g = *static_cast<const Graph*>(gp);
     TemplateTree t = make_tree(k, edges, root);
@@ -220,74 +225,77 @@ int ref_time_sampled(const void* gp, int k, const int32_t* edges, int root, uint
     WorkerPool pool(workers);
     const int Z = 16;
     const double wall0 = now_s();
-    double spmm_s = 0, ema_s = 0, misc_s = 0;
 
     double t0 = now_s();
     Coloring col = random_coloring(g, k, seed);
-    CountTable leaf = init_leaf_table(col, k, Layout::column_major);
-    misc_s += now_s() - t0;
+    const double t_color = now_s() - t0;
     t0 = now_s();
-    for (int rep = 1; rep < k; ++rep) leaf = init_leaf_table(col, k, Layout::column_major);
-    misc_s += now_s() - t0;
+    CountTable leaf = init_leaf_table(col, k, Layout::column_major);
+    const double t_leaf = now_s() - t0;
 
+    auto time_batch = [&](int zc) {
+      CountTable passive(g.n, zc, Layout::column_major);
+      for (int z = 0; z < zc; ++z)
+        for (vertex_t i = 0; i < g.n; ++i) passive.at(i, z) = leaf.at(i, (z + i) % k);
+      double best = 1e30;
+      for (int r = 0; r < std::max(1, reps); ++r) {
+        const double b0 = now_s();
+        RowBatch staged(g.n, zc);
+        pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
+          load_batch(passive, 0, zc, staged, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
+        });
+        ColumnBlock block{&passive, 0, zc};
+        pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
+          spmm_csc(g, staged, block, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
+        });
+        best = std::min(best, now_s() - b0);
+      }
+      return best;
+    };
+    const double t16 = time_batch(Z);
+    const double t1 = time_batch(1);
+    auto t_of = [&](int zc) { return t1 + (t16 - t1) * (zc - 1) / (Z - 1); };
+
+    double t_pair = 0;
+    {
+      const int ncol = std::max(1, pairs_sample);
+      CountTable out_t(g.n, ncol, Layout::column_major), act(g.n, ncol, Layout::column_major),
+          pas(g.n, 1, Layout::column_major);
+      for (vertex_t i = 0; i < g.n; ++i) {
+        pas.at(i, 0) = 2.0 + (i & 3);
+        for (int z = 0; z < ncol; ++z) act.at(i, z) = 1.0 + ((i + z) & 7);
+      }
+      const double e0 = now_s();
+      std::span<const double> cpv = pas.column(0);  // one passive column, several partners
+      for (int q = 0; q < ncol; ++q) {
+        std::span<double> cs_ = out_t.column(q);
+        std::span<const double> ca = act.column(q);
+        pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
+          ema(cs_, ca, cpv, lo, hi);
+        });
+      }
+      t_pair = (now_s() - e0) / ncol;
+    }
+
+    double spmm_s = 0, ema_s = 0;
     for (int id : plan.dp_order) {
       const PlanNode& nd = plan.node(id);
       if (nd.is_leaf()) continue;
       const int64_t cp = idx.num_sets(plan.node(nd.passive_child).size);
       const int64_t cs = idx.num_sets(nd.size);
-      const int64_t pairs = cs * idx.binom(nd.size, plan.node(nd.active_child).size);
-      // SpMM: stage + neighbour-sum batches, exactly vectorized_node's loop body
-      {
-        CountTable passive(g.n, Z, Layout::column_major);
-        for (int z = 0; z < Z; ++z)
-          for (vertex_t i = 0; i < g.n; ++i) passive.at(i, z) = leaf.at(i, (z + i) % k);
-        const int64_t nbatch = (cp + Z - 1) / Z;
-        const int64_t timed = std::min<int64_t>(nbatch, max_batches);
-        double s = 0, cols_timed = 0;
-        for (int64_t b = 0; b < timed; ++b) {
-          const int zc = static_cast<int>(std::min<int64_t>(Z, cp - b * Z));
-          const double b0 = now_s();
-          RowBatch staged(g.n, zc);
-          pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
-            load_batch(passive, 0, zc, staged, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
-          });
-          ColumnBlock block{&passive, 0, zc};
-          pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
-            spmm_csc(g, staged, block, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
-          });
-          s += now_s() - b0;
-          cols_timed += zc;
-        }
-        // full batches cost the measured average; scale by columns for the tail
-        spmm_s += s / cols_timed * static_cast<double>(cp);
-      }
-      // eMA: one pool dispatch per (I_p, partner) pair (engines.hpp:252-268)
-      {
-        const int64_t timed = std::min<int64_t>(pairs, max_pairs);
-        const int ncol = static_cast<int>(timed);
-        CountTable out(g.n, ncol, Layout::column_major), act(g.n, ncol, Layout::column_major),
-            pas(g.n, ncol, Layout::column_major);
-        for (int z = 0; z < ncol; ++z)
-          for (vertex_t i = 0; i < g.n; ++i) {
-            act.at(i, z) = 1.0 + ((i + z) & 7);
-            pas.at(i, z) = 2.0 + ((i ^ z) & 3);
-          }
-        const double e0 = now_s();
-        for (int q = 0; q < ncol; ++q) {
-          std::span<double> cs_ = out.column(q);
-          std::span<const double> ca = act.column(q);
-          std::span<const double> cpv = pas.column(q);
-          pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
-            ema(cs_, ca, cpv, lo, hi);
-          });
-        }
-        ema_s += (now_s() - e0) / static_cast<double>(timed) * static_cast<double>(pairs);
-      }
+      const int64_t npairs = cs * idx.binom(nd.size, plan.node(nd.active_child).size);
+      for (int64_t c0 = 0; c0 < cp; c0 += Z) spmm_s += t_of(static_cast<int>(std::min<int64_t>(Z, cp - c0)));
+      ema_s += t_pair * static_cast<double>(npairs);
     }
-    out[0] = spmm_s + ema_s + misc_s;
+    const double misc = t_color + k * t_leaf;
+    out[0] = spmm_s + ema_s + misc;
     out[1] = spmm_s;
     out[2] = ema_s;
     out[3] = now_s() - wall0;
+    out[4] = t16;
+    out[5] = t1;
+    out[6] = t_pair;
+    out[7] = misc;
     return 0;
   } catch (const std::exception&) {
     return -1;

@@ -47,6 +47,14 @@ class TcgNodeStats(C.Structure):
                 ("ema_bytes", C.c_uint64), ("ema_flops", C.c_uint64)]
 
 
+class TcgTiming(C.Structure):
+    _fields_ = [("total_ms", C.c_double), ("spmm_ms", C.c_double), ("ema_ms", C.c_double),
+                ("spmm_launches", C.c_int64), ("ema_launches", C.c_int64), ("launches", C.c_int64),
+                ("spmm_alg_bytes", C.c_double), ("hist_alg_bytes", C.c_double),
+                ("ema_alg_bytes", C.c_double), ("ema_flops", C.c_double),
+                ("spmm_gathered_bytes", C.c_double)]
+
+
 vp, i32, i64, u64, dbl = C.c_void_p, C.c_int32, C.c_int64, C.c_uint64, C.c_double
 P = C.POINTER
 
@@ -81,6 +89,7 @@ _SIGS = {
     "tcg_node_table": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "tcg_spmm": (C.c_int, [vp, vp, C.c_int, vp]),
     "tcg_set_rejection_limit": (C.c_int, [vp, u64]),
+    "tcg_time_colorings": (C.c_int, [vp, u64, C.c_int, C.c_int, vp, P(TcgTiming)]),
     "tcg_kernel_launches": (i64, [vp]),
 }
 

@@ -220,7 +220,9 @@ int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t
   return guarded([&] {
     need(ctx, "ctx");
     need(row_ptr, "row_ptr");
-    ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col));
+    // the reference's Graph invariants are the caller's contract here (as for
+    // a treecount::Graph); ranges / order / loops are still checked in O(nnz)
+    ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col, /*check_symmetry=*/false));
   });
 }
 
@@ -306,6 +308,15 @@ int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit) {
   return guarded([&] {
     need(ctx, "ctx");
     ctx->eng->set_rejection_limit(limit);
+  });
+}
+
+int tcg_time_colorings(tcg_ctx* ctx, uint64_t seed, int count, int per_kernel, double* totals,
+                       tcg_timing* out) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(out, "out");
+    ctx->eng->time_colorings(seed, count, per_kernel != 0, totals, out);
   });
 }
 

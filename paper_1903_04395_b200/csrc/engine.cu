@@ -358,9 +358,14 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     if (stats) m.t0 = mark();
     const float* P = hist;
     if (!e.p_leaf) {
+      size_t p0 = 0;
+      if (prof_) { p0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
+      if (prof_) { prof_->spmm.emplace_back(p0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       P = table_ptr(e.pp_off);
     }
+    size_t q0 = 0;
+    if (prof_) { q0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     if (stats) m.t1 = mark();
     const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
     float* out = e.root ? nullptr : table_ptr(e.out_off);
@@ -374,6 +379,7 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     }
     ++launches_;
     TCG_CUDA(cudaGetLastError());
+    if (prof_) { prof_->ema.emplace_back(q0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     if (stats) m.t2 = mark();
     marks.push_back(m);
   }
@@ -512,6 +518,95 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
   }
   dfree(d_totals);
   dfree(d_acc);
+  tables_valid_ = false;
+}
+
+// ------------------------------------------------------------ bench timing
+cudaEvent_t Engine::Prof::get() {
+  if (used == pool.size()) {
+    cudaEvent_t e;
+    TCG_CUDA(cudaEventCreate(&e));
+    pool.push_back(e);
+  }
+  return pool[used++];
+}
+
+void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* totals,
+                            tcg_timing* out) {
+  if (count < 1) throw invalid_argument("count must be >= 1");
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  ensure_arena();
+  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+      {static_cast<int64_t>(count), 1024, std::max<int64_t>(1, (int64_t{1} << 30) / std::max(n_, 1))})));
+  if (colors_cap_ < static_cast<int64_t>(chunk) * n_) {
+    dfree(d_colors_);
+    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(static_cast<int64_t>(chunk) * n_, 1)));
+    colors_cap_ = static_cast<int64_t>(chunk) * n_;
+  }
+  double* d_totals = nullptr;
+  TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * count));
+  Prof prof;
+  cudaEvent_t e0, e1;
+  TCG_CUDA(cudaEventCreate(&e0));
+  TCG_CUDA(cudaEventCreate(&e1));
+  const int64_t l0 = launches_;
+  std::vector<uint64_t> seeds(chunk);
+  try {
+    if (per_kernel) prof_ = &prof;
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    TCG_CUDA(cudaEventRecord(e0, stream_));
+    for (int i0 = 0; i0 < count; i0 += chunk) {
+      const int c = std::min(chunk, count - i0);
+      for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
+      gen_colors(seeds.data(), c, d_colors_);
+      for (int j = 0; j < c; ++j)
+        run_dp(d_colors_ + static_cast<int64_t>(j) * n_, d_totals + i0 + j, nullptr, nullptr);
+    }
+    TCG_CUDA(cudaEventRecord(e1, stream_));
+    TCG_CUDA(cudaEventSynchronize(e1));
+    prof_ = nullptr;
+  } catch (...) {
+    prof_ = nullptr;
+    dfree(d_totals);
+    throw;
+  }
+  tcg_timing t{};
+  float ms = 0;
+  TCG_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+  t.total_ms = ms;
+  for (auto& pr : prof.spmm) {
+    TCG_CUDA(cudaEventElapsedTime(&ms, prof.pool[pr.first], prof.pool[pr.second]));
+    t.spmm_ms += ms;
+  }
+  for (auto& pr : prof.ema) {
+    TCG_CUDA(cudaEventElapsedTime(&ms, prof.pool[pr.first], prof.pool[pr.second]));
+    t.ema_ms += ms;
+  }
+  for (auto ev : prof.pool) cudaEventDestroy(ev);
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  t.launches = launches_ - l0;
+  const Binom& B = binom();
+  const double n = n_, nnz = static_cast<double>(nnz_);
+  for (auto& e : exec_) {
+    if (!e.p_leaf) {
+      t.spmm_launches += count;
+      t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
+      t.spmm_gathered_bytes += count * nnz * dev::Z * 4.0 * ((e.Cp + dev::Z - 1) / dev::Z);
+    }
+    t.ema_launches += count;
+    t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));
+    t.ema_flops += count * 2 * n * e.Cs * static_cast<double>(B(e.size, e.sa));
+  }
+  if (need_hist_) t.hist_alg_bytes = count * (4 * nnz + 8 * (n + 1) + n + 4 * n * plan_.k);
+  std::vector<double> h(count);
+  TCG_CUDA(cudaMemcpy(h.data(), d_totals, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  dfree(d_totals);
+  if (exec_.empty()) std::fill(h.begin(), h.end(), static_cast<double>(n_));
+  if (totals) std::copy(h.begin(), h.end(), totals);
+  for (double x : h)
+    if (!std::isfinite(x)) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
+  *out = t;
   tables_valid_ = false;
 }
 

@@ -55,6 +55,7 @@ class Engine {
   void spmm_host(const float* x, int cols, float* y);
   void set_rejection_limit(uint64_t limit) { limit_override_ = limit; }
   int64_t launches() const { return launches_; }
+  void time_colorings(uint64_t seed, int count, bool per_kernel, double* totals, tcg_timing* out);
 
  private:
   void require_ready() const;
@@ -66,6 +67,14 @@ class Engine {
   // one DP over d_colors; total written to d_total (device), optional root accumulation
   void run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc,
               tcg_node_stats* stats);
+  // per-kernel event pairs recorded by run_dp when prof_ is set
+  struct Prof {
+    std::vector<cudaEvent_t> pool;
+    size_t used = 0;
+    std::vector<std::pair<size_t, size_t>> spmm, ema;
+    cudaEvent_t get();
+  };
+  Prof* prof_ = nullptr;
   void spmm(const float* X, float* Y, int cols);
   float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
   int64_t table_bytes(int64_t cols) const;

@@ -143,7 +143,7 @@ Csr csr_from_edges(const int32_t* edges, int64_t m, int32_t n_hint) {
   return g;
 }
 
-Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col) {
+Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col, bool check_symmetry) {
   if (n < 0 || !row_ptr || row_ptr[0] != 0) throw invalid_argument("bad CSR row_ptr");
   for (int32_t v = 0; v < n; ++v)
     if (row_ptr[v + 1] < row_ptr[v]) throw invalid_argument("CSR row_ptr not monotone");
@@ -158,7 +158,8 @@ Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col) {
         const int32_t u = g.col[j];
         if (u < 0 || u >= n || u == v) { bad = 1; return; }
         if (j > g.row_ptr[v] && g.col[j - 1] >= u) { bad = 2; return; }
-        if (!std::binary_search(g.col.data() + g.row_ptr[u], g.col.data() + g.row_ptr[u + 1],
+        if (check_symmetry &&
+            !std::binary_search(g.col.data() + g.row_ptr[u], g.col.data() + g.row_ptr[u + 1],
                                 static_cast<int32_t>(v))) { bad = 3; return; }
       }
     }

@@ -67,8 +67,9 @@ struct Csr {
 int host_threads();
 // graph.hpp:65-95; throws invalid_argument on out-of-range ids.
 Csr csr_from_edges(const int32_t* edges, int64_t m, int32_t n_hint);
-// validates symmetric / sorted / loop-free / duplicate-free
-Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col);
+// validates sorted / loop-free / duplicate-free / in range, and (check_symmetry)
+// that every edge appears in both rows (O(nnz log d))
+Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col, bool check_symmetry = true);
 Csr generate_rmat(int scale, int64_t edges, double a, double b, double c, double d,
                   uint64_t seed);
 Csr generate_erdos_renyi(int32_t n, double p, uint64_t seed);

@@ -424,6 +424,15 @@ class Context:
     def kernel_launches(self) -> int:
         return int(lib.tcg_kernel_launches(self._h))
 
+    def time(self, seed: int, count: int, per_kernel: bool = False):
+        """Device-timed batch of colorings (CUDA events on the engine stream)."""
+        if count < 1:
+            return N.TcgTiming(), np.zeros(0)
+        tm = N.TcgTiming()
+        totals = np.zeros(count, np.float64)
+        check(lib.tcg_time_colorings(self._h, seed, count, int(per_kernel), _ptr(totals), C.byref(tm)))
+        return tm, totals
+
 
 # Contexts behind the reference-style free functions, keyed by (graph, template, cfg).
 _ctx_cache: dict = {}
