@@ -4,8 +4,10 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
+#include <thread>
 
 namespace tcg {
 
@@ -32,6 +34,14 @@ void dfree(T*& p) {
   p = nullptr;
 }
 
+template <typename T>
+T* dupload(const std::vector<T>& h, cudaStream_t s) {
+  T* d = nullptr;
+  TCG_CUDA(cudaMalloc(&d, sizeof(T) * std::max<size_t>(h.size(), 1)));
+  if (!h.empty()) TCG_CUDA(cudaMemcpyAsync(d, h.data(), sizeof(T) * h.size(), cudaMemcpyHostToDevice, s));
+  return d;
+}
+
 // First-fit arena planner over the reference's liveness sequence.
 struct ArenaPlanner {
   std::map<int64_t, int64_t> used;  // offset -> bytes
@@ -49,6 +59,55 @@ struct ArenaPlanner {
   }
   void free(int64_t off) { used.erase(off); }
 };
+
+void release_schedule(PartSchedule& s) {
+  dfree(s.d_segs);
+  dfree(s.d_split_rows);
+  dfree(s.d_slot_begin);
+  s = PartSchedule{};
+}
+
+// Cut row ranges [lo[v], hi[v]) into segments of <= kSegMax, counting-sort by
+// length (descending), pad with no-op segments; rows longer than one segment
+// get fp64 partial slots (summed in order by spmm_fixup).
+PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
+                            bool keep_empty, cudaStream_t stream) {
+  const int32_t n = static_cast<int32_t>(lo.size());
+  std::vector<dev::Seg> segs;
+  segs.reserve(static_cast<size_t>(n) + 16);
+  std::vector<int32_t> split_rows, slot_begin{0};
+  int slot = 0;
+  for (int32_t v = 0; v < n; ++v) {
+    const int64_t d = hi[v] - lo[v];
+    if (d == 0 && !keep_empty) continue;
+    if (d <= dev::kSegMax) {
+      segs.push_back({lo[v], static_cast<int32_t>(d), v});
+    } else {
+      split_rows.push_back(v);
+      for (int64_t o = 0; o < d; o += dev::kSegMax)
+        segs.push_back({lo[v] + o, static_cast<int32_t>(std::min<int64_t>(dev::kSegMax, d - o)), -1 - slot++});
+      slot_begin.push_back(slot);
+    }
+  }
+  std::vector<int64_t> pos(dev::kSegMax + 2, 0);
+  for (auto& s : segs) pos[dev::kSegMax - s.len + 1]++;
+  for (size_t i = 1; i < pos.size(); ++i) pos[i] += pos[i - 1];
+  const int64_t padded = std::max<int64_t>((static_cast<int64_t>(segs.size()) + dev::kSegPad - 1) /
+                                               dev::kSegPad * dev::kSegPad, dev::kSegPad);
+  std::vector<dev::Seg> sorted(static_cast<size_t>(padded), dev::Seg{0, 0, dev::kSkip});
+  for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
+  PartSchedule ps;
+  ps.nseg_padded = padded;
+  ps.d_segs = dupload(sorted, stream);
+  ps.nsplit_rows = static_cast<int>(split_rows.size());
+  ps.nslots = slot;
+  if (ps.nsplit_rows) {
+    ps.d_split_rows = dupload(split_rows, stream);
+    ps.d_slot_begin = dupload(slot_begin, stream);
+  }
+  TCG_CUDA(cudaStreamSynchronize(stream));
+  return ps;
+}
 }  // namespace
 
 Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
@@ -63,6 +122,7 @@ Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
   if (prop.major != 10)
     throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor));
+  if (const char* e = std::getenv("TCG_PART_MB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 20;
   TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   TCG_CUDA(cudaMalloc(&d_scalars_, 64));
   TCG_CUDA(cudaMalloc(&d_seeds_, 1024 * sizeof(uint64_t)));
@@ -81,15 +141,19 @@ Engine::~Engine() {
 void Engine::release_graph() {
   dfree(d_row_ptr_);
   dfree(d_col_);
-  dfree(d_segs_);
-  dfree(d_split_rows_);
-  dfree(d_split_slot_begin_);
+  for (auto& kv : sched_)
+    for (auto& s : kv.second) release_schedule(s);
+  sched_.clear();
   dfree(d_tile_tot_);
   n_ = -1;
 }
 
 void Engine::release_template() {
-  for (auto& e : exec_) dfree(e.d_split);
+  for (auto& e : exec_) {
+    dfree(e.d_split);
+    dfree(e.d_drop);
+    dfree(e.d_packed);
+  }
   exec_.clear();
   dfree(arena_);
   arena_alloc_ = 0;
@@ -97,10 +161,6 @@ void Engine::release_template() {
   partial_bytes_ = partial_alloc_ = 0;
   have_template_ = false;
   tables_valid_ = false;
-}
-
-int64_t Engine::table_bytes(int64_t cols) const {
-  return (cols + dev::Z - 1) / dev::Z * static_cast<int64_t>(n_) * dev::Z * 4;
 }
 
 // ------------------------------------------------------------------ graph
@@ -116,47 +176,38 @@ void Engine::set_graph(const Csr& g) {
   if (nnz_)
     TCG_CUDA(cudaMemcpyAsync(d_col_, g.col.data(), sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice,
                              stream_));
-
-  // SpMM schedule: rows cut into segments of <= kSegMax neighbours, counting-
-  // sorted by length (descending) so the 8 groups of a warp are balanced and
-  // the longest work is issued first.  Split rows get fp64 partial slots.
-  std::vector<int64_t> cnt(dev::kSegMax + 2, 0);
-  std::vector<dev::Seg> segs;
-  segs.reserve(static_cast<size_t>(n_) + static_cast<size_t>(nnz_ / dev::kSegMax) + 8);
-  std::vector<int32_t> split_rows, slot_begin{0};
-  int slot = 0;
-  for (int32_t v = 0; v < n_; ++v) {
-    const int64_t b = g.row_ptr[v], d = g.row_ptr[v + 1] - b;
-    if (d <= dev::kSegMax) {
-      segs.push_back({b, static_cast<int32_t>(d), v});
-    } else {
-      split_rows.push_back(v);
-      for (int64_t o = 0; o < d; o += dev::kSegMax)
-        segs.push_back({b + o, static_cast<int32_t>(std::min<int64_t>(dev::kSegMax, d - o)), -1 - slot++});
-      slot_begin.push_back(slot);
+  // Parts: the gather source of one panel is n*ZW*4 B; split the vertex
+  // range so each part's rows (the L2-resident working set) fit in
+  // part_bytes_.  Each CSR row is sorted, so a row's neighbours in a part are
+  // one contiguous sub-range.  One schedule set per distinct part count.
+  std::vector<int> counts{1};
+  for (int zw : {8, 16, 32}) counts.push_back(parts_for_width(zw));
+  std::sort(counts.begin(), counts.end());
+  counts.erase(std::unique(counts.begin(), counts.end()), counts.end());
+  max_slots_ = 0;
+  for (int P : counts) {
+    std::vector<std::vector<int64_t>> bnd(P + 1, std::vector<int64_t>(n_));
+    const int T = std::max(1, std::min(host_threads(), 32));
+    std::vector<std::thread> th;
+    for (int w = 0; w < T; ++w)
+      th.emplace_back([&, w] {
+        for (int64_t v = static_cast<int64_t>(n_) * w / T; v < static_cast<int64_t>(n_) * (w + 1) / T; ++v) {
+          const int32_t* b = g.col.data() + g.row_ptr[v];
+          const int32_t* e = g.col.data() + g.row_ptr[v + 1];
+          bnd[0][v] = g.row_ptr[v];
+          bnd[P][v] = g.row_ptr[v + 1];
+          for (int s = 1; s < P; ++s) {
+            const int64_t cut = static_cast<int64_t>(n_) * s / P;
+            bnd[s][v] = g.row_ptr[v] + (std::lower_bound(b, e, static_cast<int32_t>(cut)) - b);
+          }
+        }
+      });
+    for (auto& t : th) t.join();
+    auto& vec = sched_[P];
+    for (int s = 0; s < P; ++s) {
+      vec.push_back(build_schedule(bnd[s], bnd[s + 1], s == 0, stream_));
+      max_slots_ = std::max(max_slots_, vec.back().nslots);
     }
-  }
-  for (auto& s : segs) cnt[dev::kSegMax - s.len]++;
-  std::vector<int64_t> pos(cnt.size(), 0);
-  for (size_t i = 1; i < cnt.size(); ++i) pos[i] = pos[i - 1] + cnt[i - 1];
-  const int64_t nseg = static_cast<int64_t>(segs.size());
-  const int64_t padded = (nseg + 7) / 8 * 8;
-  std::vector<dev::Seg> sorted(static_cast<size_t>(std::max<int64_t>(padded, 8)),
-                               dev::Seg{0, 0, dev::kSkip});
-  for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
-  ntasks_ = std::max<int64_t>(padded, 8) / 8;
-  nsplit_rows_ = static_cast<int>(split_rows.size());
-  nsplit_slots_ = slot;
-  TCG_CUDA(cudaMalloc(&d_segs_, sizeof(dev::Seg) * sorted.size()));
-  TCG_CUDA(cudaMemcpyAsync(d_segs_, sorted.data(), sizeof(dev::Seg) * sorted.size(),
-                           cudaMemcpyHostToDevice, stream_));
-  if (nsplit_rows_) {
-    TCG_CUDA(cudaMalloc(&d_split_rows_, sizeof(int32_t) * nsplit_rows_));
-    TCG_CUDA(cudaMalloc(&d_split_slot_begin_, sizeof(int32_t) * (nsplit_rows_ + 1)));
-    TCG_CUDA(cudaMemcpyAsync(d_split_rows_, split_rows.data(), sizeof(int32_t) * nsplit_rows_,
-                             cudaMemcpyHostToDevice, stream_));
-    TCG_CUDA(cudaMemcpyAsync(d_split_slot_begin_, slot_begin.data(),
-                             sizeof(int32_t) * (nsplit_rows_ + 1), cudaMemcpyHostToDevice, stream_));
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
@@ -176,6 +227,8 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   aut_ = automorphism_count(t);
   const Binom& B = binom();
   need_hist_ = false;
+  int max_smem = 0;
+  TCG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg_.device));
   for (int id : plan_.dp_order) {
     if (plan_.is_leaf(id)) continue;
     NodeExec e;
@@ -196,16 +249,28 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     e.pairs = st.pairs_per_parent;
     std::vector<int2> pr(st.active_index.size());
     for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(st.active_index[i], st.passive_index[i]);
-    TCG_CUDA(cudaMalloc(&e.d_split, sizeof(int2) * std::max<size_t>(pr.size(), 1)));
-    TCG_CUDA(cudaMemcpy(e.d_split, pr.data(), sizeof(int2) * pr.size(), cudaMemcpyHostToDevice));
-    // eMA shared memory: staged inputs + per-warp transpose buffers
-    const int64_t pitch = dev::kTileV + 1;
-    const int64_t staged = ((e.a_leaf ? 0 : e.Ca) + e.Cp) * pitch * 4 +
-                           dev::kEmaWarps * dev::kTileV * (dev::Z + 1) * 4;
-    e.ema_staged = staged <= 200 * 1024;
-    e.ema_smem = e.ema_staged ? staged : dev::kEmaWarps * dev::kTileV * (dev::Z + 1) * 4;
+    e.d_split = dupload(pr, stream_);
+    if (!e.a_leaf && !e.root && e.Ca < 65536 && e.Cp < 65536) {
+      std::vector<uint32_t> pk(pr.size());
+      for (size_t i = 0; i < pr.size(); ++i)
+        pk[i] = static_cast<uint32_t>(pr[i].x) | (static_cast<uint32_t>(pr[i].y) << 16);
+      e.d_packed = dupload(pk, stream_);
+    }
+    if (e.a_leaf && !e.root) {
+      // active leaf: the pair whose active color is c gives the column of S minus c
+      std::vector<int32_t> drop(static_cast<size_t>(e.Cs) * k, -1);
+      for (int32_t s = 0; s < e.Cs; ++s)
+        for (int p2 = 0; p2 < e.pairs; ++p2)
+          drop[static_cast<size_t>(s) * k + pr[static_cast<size_t>(s) * e.pairs + p2].x] =
+              pr[static_cast<size_t>(s) * e.pairs + p2].y;
+      e.d_drop = dupload(drop, stream_);
+    }
+    const int64_t staged = static_cast<int64_t>((e.a_leaf ? 0 : e.Ca) + e.Cp) * (dev::kTileV + 1) * 4;
+    e.ema_staged = staged <= max_smem - 4096;
+    e.ema_smem = e.ema_staged ? static_cast<size_t>(staged) : 0;
     exec_.push_back(e);
   }
+  TCG_CUDA(cudaStreamSynchronize(stream_));
   have_template_ = true;
   if (n_ >= 0) plan_arena();
   tables_valid_ = false;
@@ -217,12 +282,10 @@ void Engine::plan_arena() {
   table_off_.assign(plan_.num_nodes, -1);
   pprime_off_.assign(plan_.num_nodes, -1);
   hist_off_ = need_hist_ ? ap.alloc(table_bytes(plan_.k)) : -1;
-  int max_pp_panels = 0;
   for (auto& e : exec_) {
     if (!e.p_leaf) {
       e.pp_off = ap.alloc(table_bytes(e.Cp));
       pprime_off_[e.p] = e.pp_off;
-      max_pp_panels = std::max(max_pp_panels, (e.Cp + dev::Z - 1) / dev::Z);
       if (!keep) ap.free(table_off_[e.p]);
     }
     e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(e.Cs));
@@ -233,13 +296,16 @@ void Engine::plan_arena() {
     }
   }
   arena_bytes_ = ap.peak;
-  partial_bytes_ = static_cast<int64_t>(nsplit_slots_) * max_pp_panels * dev::Z * 8;
+  partial_bytes_ = static_cast<int64_t>(max_slots_) * dev::kZ * 8;
 }
 
 int64_t Engine::required_bytes() const {
   require_ready();
+  int64_t sched = 0;
+  for (auto& kv : sched_)
+    for (auto& s : kv.second) sched += s.nseg_padded;
   const int64_t graph = 8 * (static_cast<int64_t>(n_) + 1) + 4 * nnz_ +
-                        static_cast<int64_t>(sizeof(dev::Seg)) * ntasks_ * 8;
+                        static_cast<int64_t>(sizeof(dev::Seg)) * sched;
   return arena_bytes_ + partial_bytes_ + graph + n_ + 8 * ((n_ + 31) / 32);
 }
 
@@ -267,12 +333,22 @@ void Engine::ensure_arena() {
   }
 }
 
+void Engine::ensure_colors(int64_t bytes) {
+  if (colors_cap_ < bytes) {
+    dfree(d_colors_);
+    colors_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(bytes, 1)));
+    colors_cap_ = bytes;
+  }
+}
+
 // ----------------------------------------------------------------- colors
 void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
   TCG_CUDA(cudaMemcpyAsync(d_seeds_, seeds, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, stream_));
-  const uint64_t limit = limit_override_ ? limit_override_
-                                         : (UINT64_MAX / static_cast<uint64_t>(plan_.k)) * plan_.k;
-  dev::mt_coloring<<<count, dev::kMtThreads, 0, stream_>>>(d_seeds_, n_, plan_.k, limit, d_out, n_);
+  const uint64_t k = static_cast<uint64_t>(plan_.k);
+  const uint64_t limit = limit_override_ ? limit_override_ : (UINT64_MAX / k) * k;
+  dev::mt_coloring<<<count, dev::kMtThreads, 0, stream_>>>(d_seeds_, n_, plan_.k, limit, UINT64_MAX / k,
+                                                             d_out, n_);
   ++launches_;
   TCG_CUDA(cudaGetLastError());
 }
@@ -280,54 +356,86 @@ void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
 void Engine::coloring(uint64_t seed, uint8_t* host_colors) {
   require_ready();
   TCG_CUDA(cudaSetDevice(cfg_.device));
-  if (colors_cap_ < n_) {
-    dfree(d_colors_);
-    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(n_, 1)));
-    colors_cap_ = n_;
-  }
+  ensure_colors(n_);
   gen_colors(&seed, 1, d_colors_);
   TCG_CUDA(cudaMemcpyAsync(host_colors, d_colors_, n_, cudaMemcpyDeviceToHost, stream_));
   TCG_CUDA(cudaStreamSynchronize(stream_));
 }
 
 // ------------------------------------------------------------------- SpMM
-void Engine::spmm(const float* X, float* Y, int cols) {
-  const int npanels = (cols + dev::Z - 1) / dev::Z;
-  const int64_t bpp = (ntasks_ + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
-  dev::spmm_panels<<<static_cast<unsigned>(bpp * npanels), dev::kSpmmWarps * 32, 0, stream_>>>(
-      d_segs_, ntasks_, bpp, d_col_, X, Y, d_partial_, n_, npanels);
-  ++launches_;
-  if (nsplit_rows_) {
-    const int64_t total = static_cast<int64_t>(nsplit_rows_) * npanels * dev::Z;
-    dev::spmm_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
-        d_split_rows_, d_split_slot_begin_, nsplit_rows_, d_partial_, Y, n_, npanels);
-    ++launches_;
+template <int ZW, bool ONEHOT>
+static void launch_spmm_part(const PartSchedule& ps, cudaStream_t s, const int32_t* col,
+                             const float* X, const uint8_t* colors, int color_base, float* Y,
+                             double* partial, bool first, int64_t& launches) {
+  constexpr int spw = 128 / ZW;  // segments per warp
+  const int64_t ntasks = ps.nseg_padded / spw;
+  const int64_t blocks = (ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
+  dev::spmm_part<ZW, ONEHOT><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
+      ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
+  ++launches;
+  if (ps.nsplit_rows) {
+    const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * ZW;
+    dev::spmm_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, s>>>(
+        ps.d_split_rows, ps.d_slot_begin, ps.nsplit_rows, partial, Y, ZW, first ? 1 : 0);
+    ++launches;
+  }
+}
+
+void Engine::spmm(const float* X, float* Y, int64_t cols) {
+  const int P = dev::num_panels(cols);
+  for (int p = 0; p < P; ++p) {
+    const int zw = dev::panel_width(cols, p);
+    const float* Xp = X + static_cast<int64_t>(p) * n_ * dev::kZ;
+    float* Yp = Y + static_cast<int64_t>(p) * n_ * dev::kZ;
+    const auto& parts = sched_.at(parts_for_width(zw));
+    for (int s = 0; s < static_cast<int>(parts.size()); ++s) {
+      const PartSchedule& ps = parts[s];
+      if (zw == 32) launch_spmm_part<32, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+      else if (zw == 16) launch_spmm_part<16, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+      else launch_spmm_part<8, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+    }
   }
   TCG_CUDA(cudaGetLastError());
 }
 
-// -------------------------------------------------------------------- eMA
-template <typename AccT, bool AL, bool RT, bool ST>
-static void launch_ema(const NodeExec& e, cudaStream_t s, int32_t n, const float* A,
-                       const float* P, const uint8_t* colors, float* out, double* root_out,
-                       double* root_acc, double* tile_tot) {
-  auto kern = dev::ema_tile<AccT, AL, RT, ST>;
-  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(e.ema_smem)));
-  const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
-  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca,
-                                                       e.Cp, e.Cs, n, out, root_out, root_acc,
-                                                       tile_tot);
+// P' of a leaf passive child: SpMM against the one-hot color table, read as
+// 1-byte colors (whole rows; the colors array is L2-resident).
+int Engine::parts_for_width(int zw) const {
+  const int64_t need = (static_cast<int64_t>(n_) * zw * 4 + part_bytes_ - 1) / part_bytes_;
+  int P = 1;
+  while (P < need && P < (1 << 20)) P *= 2;
+  return std::max(1, std::min<int>(P, std::max(1, n_)));
 }
 
-template <bool AL, bool RT>
-static void launch_ema2(const NodeExec& e, cudaStream_t s, int32_t n, const float* A,
-                        const float* P, const uint8_t* colors, float* out, double* root_out,
-                        double* root_acc, double* tile_tot) {
-  if (e.ema_staged)
-    launch_ema<double, AL, RT, true>(e, s, n, A, P, colors, out, root_out, root_acc, tile_tot);
-  else
-    launch_ema<double, AL, RT, false>(e, s, n, A, P, colors, out, root_out, root_acc, tile_tot);
+void Engine::hist(const uint8_t* d_colors, float* H) {
+  const PartSchedule& full_ = sched_.at(1)[0];
+  const int zw = dev::panel_width(plan_.k, 0);
+  if (zw == 32) launch_spmm_part<32, true>(full_, stream_, d_col_, nullptr, d_colors, 0, H, d_partial_, true, launches_);
+  else if (zw == 16) launch_spmm_part<16, true>(full_, stream_, d_col_, nullptr, d_colors, 0, H, d_partial_, true, launches_);
+  else launch_spmm_part<8, true>(full_, stream_, d_col_, nullptr, d_colors, 0, H, d_partial_, true, launches_);
+  TCG_CUDA(cudaGetLastError());
+}
+
+// -------------------------------------------------------------------- eMA
+template <bool AL, bool ST>
+static void launch_node(const NodeExec& e, int k, cudaStream_t s, int32_t n, const float* A,
+                        const float* P, const uint8_t* colors, float* out) {
+  auto kern = dev::ema_node<AL, ST>;
+  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
+  const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
+  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.d_packed, e.d_drop, k,
+                                                      e.pairs, e.Ca, e.Cp, e.Cs, n, out);
+}
+
+template <bool AL, bool ST>
+static void launch_root(const NodeExec& e, cudaStream_t s, int32_t n, const float* A,
+                        const float* P, const uint8_t* colors, double* rout, double* racc,
+                        double* tile_tot) {
+  auto kern = dev::ema_root<AL, ST>;
+  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
+  const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
+  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca, e.Cp,
+                                                      n, rout, racc, tile_tot);
 }
 
 // ---------------------------------------------------------------- one DP
@@ -341,50 +449,60 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     ev.push_back(e);
     return ev.size() - 1;
   };
-  const float* hist = nullptr;
-  if (need_hist_) {
-    float* H = table_ptr(hist_off_);
-    const int64_t warps = std::min<int64_t>(n_, 148LL * 64);
-    dev::nbr_hist<<<static_cast<unsigned>((warps * 32 + 255) / 256), 256, 0, stream_>>>(
-        d_row_ptr_, d_col_, d_colors, n_, plan_.k, H);
-    ++launches_;
-    TCG_CUDA(cudaGetLastError());
-    hist = H;
+  const float* H = nullptr;
+  if (need_hist_ && n_ > 0) {
+    size_t h0 = 0;
+    if (prof_) { h0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+    hist(d_colors, table_ptr(hist_off_));
+    if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+    H = table_ptr(hist_off_);
   }
   struct Marks { size_t t0, t1, t2; };
   std::vector<Marks> marks;
   for (auto& e : exec_) {
     Marks m{0, 0, 0};
     if (stats) m.t0 = mark();
-    const float* P = hist;
-    if (!e.p_leaf) {
+    const float* P = H;
+    if (!e.p_leaf && n_ > 0) {
       size_t p0 = 0;
       if (prof_) { p0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
       if (prof_) { prof_->spmm.emplace_back(p0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       P = table_ptr(e.pp_off);
     }
+    if (stats) m.t1 = mark();
     size_t q0 = 0;
     if (prof_) { q0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-    if (stats) m.t1 = mark();
     const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
-    float* out = e.root ? nullptr : table_ptr(e.out_off);
-    double* rout = e.root ? reinterpret_cast<double*>(arena_ + e.out_off) : nullptr;
-    if (e.root) {
-      if (e.a_leaf) launch_ema2<true, true>(e, stream_, n_, A, P, d_colors, out, rout, d_root_acc, d_tile_tot_);
-      else launch_ema2<false, true>(e, stream_, n_, A, P, d_colors, out, rout, d_root_acc, d_tile_tot_);
-    } else {
-      if (e.a_leaf) launch_ema2<true, false>(e, stream_, n_, A, P, d_colors, out, rout, nullptr, d_tile_tot_);
-      else launch_ema2<false, false>(e, stream_, n_, A, P, d_colors, out, rout, nullptr, d_tile_tot_);
+    if (n_ > 0) {
+      if (e.root) {
+        double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
+        if (e.a_leaf) {
+          if (e.ema_staged) launch_root<true, true>(e, stream_, n_, A, P, d_colors, rout, d_root_acc, d_tile_tot_);
+          else launch_root<true, false>(e, stream_, n_, A, P, d_colors, rout, d_root_acc, d_tile_tot_);
+        } else {
+          if (e.ema_staged) launch_root<false, true>(e, stream_, n_, A, P, d_colors, rout, d_root_acc, d_tile_tot_);
+          else launch_root<false, false>(e, stream_, n_, A, P, d_colors, rout, d_root_acc, d_tile_tot_);
+        }
+      } else {
+        float* out = table_ptr(e.out_off);
+        if (e.a_leaf) {
+          if (e.ema_staged) launch_node<true, true>(e, plan_.k, stream_, n_, A, P, d_colors, out);
+          else launch_node<true, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);
+        } else {
+          if (e.ema_staged) launch_node<false, true>(e, plan_.k, stream_, n_, A, P, d_colors, out);
+          else launch_node<false, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);
+        }
+      }
+      ++launches_;
+      TCG_CUDA(cudaGetLastError());
     }
-    ++launches_;
-    TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->ema.emplace_back(q0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     if (stats) m.t2 = mark();
     marks.push_back(m);
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
-  if (n_ > 0) {
+  if (n_ > 0 && !exec_.empty()) {
     dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, ntiles, d_total);
     ++launches_;
   } else {
@@ -409,7 +527,7 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
       const uint64_t pairs_total = static_cast<uint64_t>(e.Cs) * static_cast<uint64_t>(B(e.size, e.sa));
       st.flops = static_cast<uint64_t>(e.Cp) * static_cast<uint64_t>(nnz_) + 2ull * n_ * pairs_total;
       st.spmm_bytes = 4ull * nnz_ + 8ull * (n_ + 1) + 8ull * n_ * static_cast<uint64_t>(e.Cp);
-      st.ema_bytes = 4ull * n_ * (static_cast<uint64_t>(e.Ca) + e.Cp) +
+      st.ema_bytes = 4ull * n_ * ((e.a_leaf ? 0ull : static_cast<uint64_t>(e.Ca)) + e.Cp) +
                      (e.root ? 8ull * n_ : 4ull * n_ * static_cast<uint64_t>(e.Cs));
       st.ema_flops = 2ull * n_ * pairs_total;
     }
@@ -421,11 +539,7 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
                             tcg_node_stats* stats) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  if (colors_cap_ < n_) {
-    dfree(d_colors_);
-    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(n_, 1)));
-    colors_cap_ = n_;
-  }
+  ensure_colors(n_);
   if (host_colors) {
     for (int32_t i = 0; i < n_; ++i)
       if (host_colors[i] >= plan_.k) throw invalid_argument("coloring value out of range [0, k)");
@@ -436,13 +550,11 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
   run_dp(d_colors_, d_scalars_, nullptr, stats);
   double total = 0;
   TCG_CUDA(cudaMemcpyAsync(&total, d_scalars_, sizeof(double), cudaMemcpyDeviceToHost, stream_));
-  const NodeExec& root = exec_.empty() ? NodeExec{} : exec_.back();
   if (per_vertex && n_ > 0) {
     if (exec_.empty()) {
-      // single-vertex template: every vertex counts once (k = 1)
-      for (int32_t i = 0; i < n_; ++i) per_vertex[i] = 1.0;
+      for (int32_t i = 0; i < n_; ++i) per_vertex[i] = 1.0;  // k = 1: every vertex once
     } else {
-      TCG_CUDA(cudaMemcpyAsync(per_vertex, arena_ + root.out_off, sizeof(double) * n_,
+      TCG_CUDA(cudaMemcpyAsync(per_vertex, arena_ + exec_.back().out_off, sizeof(double) * n_,
                                cudaMemcpyDeviceToHost, stream_));
     }
   }
@@ -457,18 +569,18 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
   return total;
 }
 
+static int color_chunk(int count, int32_t n) {
+  return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
+      {static_cast<int64_t>(count), 1024, std::max<int64_t>(1, (int64_t{1} << 30) / std::max(n, 1))})));
+}
+
 void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est, double* se,
                       double* per_vertex_est) {
   if (iterations < 1) throw invalid_argument("iterations must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
-      {static_cast<int64_t>(iterations), 1024, std::max<int64_t>(1, (int64_t{1} << 30) / std::max(n_, 1))})));
-  if (colors_cap_ < static_cast<int64_t>(chunk) * n_) {
-    dfree(d_colors_);
-    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(static_cast<int64_t>(chunk) * n_, 1)));
-    colors_cap_ = static_cast<int64_t>(chunk) * n_;
-  }
+  const int chunk = color_chunk(iterations, n_);
+  ensure_colors(static_cast<int64_t>(chunk) * n_);
   double* d_totals = nullptr;
   double* d_acc = nullptr;
   TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * iterations));
@@ -536,13 +648,8 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
   if (count < 1) throw invalid_argument("count must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  const int chunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(
-      {static_cast<int64_t>(count), 1024, std::max<int64_t>(1, (int64_t{1} << 30) / std::max(n_, 1))})));
-  if (colors_cap_ < static_cast<int64_t>(chunk) * n_) {
-    dfree(d_colors_);
-    TCG_CUDA(cudaMalloc(&d_colors_, std::max<int64_t>(static_cast<int64_t>(chunk) * n_, 1)));
-    colors_cap_ = static_cast<int64_t>(chunk) * n_;
-  }
+  const int chunk = color_chunk(count, n_);
+  ensure_colors(static_cast<int64_t>(chunk) * n_);
   double* d_totals = nullptr;
   TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * count));
   Prof prof;
@@ -592,7 +699,8 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
     if (!e.p_leaf) {
       t.spmm_launches += count;
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
-      t.spmm_gathered_bytes += count * nnz * dev::Z * 4.0 * ((e.Cp + dev::Z - 1) / dev::Z);
+      t.spmm_gathered_bytes += count * nnz * 4.0 * (static_cast<double>(dev::num_panels(e.Cp) - 1) * dev::kZ +
+                                                     dev::last_panel_width(e.Cp));
     }
     t.ema_launches += count;
     t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));
@@ -611,10 +719,9 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
 }
 
 // ------------------------------------------------------------ inspection
-static void unpanel(const std::vector<float>& panels, int64_t n, int64_t C, double* out) {
+static void unpanel(const std::vector<float>& t, int64_t n, int64_t C, double* out) {
   for (int64_t v = 0; v < n; ++v)
-    for (int64_t c = 0; c < C; ++c)
-      out[v * C + c] = panels[((c / dev::Z) * n + v) * dev::Z + c % dev::Z];
+    for (int64_t c = 0; c < C; ++c) out[v * C + c] = t[dev::panel_offset(C, n, v, c)];
 }
 
 void Engine::node_table(int id, int which, double* out) {
@@ -629,7 +736,7 @@ void Engine::node_table(int id, int which, double* out) {
       return;
     }
     if (hist_off_ < 0) throw invalid_argument("no neighbour histogram in this plan");
-    std::vector<float> h((k + dev::Z - 1) / dev::Z * n * dev::Z);
+    std::vector<float> h(dev::table_floats(k, n));
     TCG_CUDA(cudaMemcpy(h.data(), arena_ + hist_off_, h.size() * 4, cudaMemcpyDeviceToHost));
     unpanel(h, n, k, out);
     return;
@@ -642,7 +749,7 @@ void Engine::node_table(int id, int which, double* out) {
   }
   const int64_t off = which == 0 ? table_off_[id] : pprime_off_[id];
   if (off < 0) throw invalid_argument("table not available for this node");
-  std::vector<float> t((C + dev::Z - 1) / dev::Z * n * dev::Z);
+  std::vector<float> t(dev::table_floats(C, n));
   TCG_CUDA(cudaMemcpy(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost));
   unpanel(t, n, C, out);
 }
@@ -651,20 +758,20 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
   if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
   if (cols < 1) throw invalid_argument("cols must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
-  const int64_t n = n_, panels = (cols + dev::Z - 1) / dev::Z;
-  std::vector<float> xp(panels * n * dev::Z, 0.f);
+  const int64_t n = n_;
+  std::vector<float> xp(dev::table_floats(cols, n), 0.f);
   for (int64_t v = 0; v < n; ++v)
-    for (int64_t c = 0; c < cols; ++c) xp[((c / dev::Z) * n + v) * dev::Z + c % dev::Z] = x[v * cols + c];
+    for (int64_t c = 0; c < cols; ++c) xp[dev::panel_offset(cols, n, v, c)] = x[v * cols + c];
   float *dx = nullptr, *dy = nullptr;
   double* saved_partial = d_partial_;
   double* dp = nullptr;
   try {
     TCG_CUDA(cudaMalloc(&dx, std::max<size_t>(xp.size() * 4, 4)));
     TCG_CUDA(cudaMalloc(&dy, std::max<size_t>(xp.size() * 4, 4)));
-    if (nsplit_slots_) TCG_CUDA(cudaMalloc(&dp, static_cast<size_t>(nsplit_slots_) * panels * dev::Z * 8));
+    if (max_slots_) TCG_CUDA(cudaMalloc(&dp, static_cast<size_t>(max_slots_) * dev::kZ * 8));
     TCG_CUDA(cudaMemcpy(dx, xp.data(), xp.size() * 4, cudaMemcpyHostToDevice));
     d_partial_ = dp;
-    spmm(dx, dy, cols);
+    if (n > 0) spmm(dx, dy, cols);
     d_partial_ = saved_partial;
     TCG_CUDA(cudaStreamSynchronize(stream_));
     TCG_CUDA(cudaMemcpy(xp.data(), dy, xp.size() * 4, cudaMemcpyDeviceToHost));
@@ -675,7 +782,7 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
   }
   dfree(dx); dfree(dy); dfree(dp);
   for (int64_t v = 0; v < n; ++v)
-    for (int64_t c = 0; c < cols; ++c) y[v * cols + c] = xp[((c / dev::Z) * n + v) * dev::Z + c % dev::Z];
+    for (int64_t c = 0; c < cols; ++c) y[v * cols + c] = xp[dev::panel_offset(cols, n, v, c)];
 }
 
 }  // namespace tcg

@@ -2,7 +2,7 @@
 //
 // Drop-in for the reference's vectorized engine: IterationRun::run
 // (engines.hpp:106-132) + vectorized_node (224-268), with the count tables
-// resident in HBM as fp32 panels (kernels.cuh) and the root in fp64.
+// resident in HBM as fp32 panels (layout.hpp) and the root in fp64.
 // Device memory for one coloring is planned once per (graph, template) by
 // simulating the reference's liveness rule (engines.hpp:149-151,
 // count_table.hpp:113-133) over a single arena, so a coloring performs no
@@ -12,6 +12,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
 #include <string>
 #include <vector>
 
@@ -28,10 +29,21 @@ struct NodeExec {
   int pairs = 0;
   bool a_leaf = false, p_leaf = false, root = false;
   int2* d_split = nullptr;   // by-parent (I_a, I_p) pairs, [Cs * pairs]
+  int32_t* d_drop = nullptr; // active leaf: [Cs * k] column of S minus c, or -1
+  uint32_t* d_packed = nullptr;  // (I_a | I_p << 16) when both fit in 16 bits
   int64_t out_off = -1;      // arena offset of M_s (root: fp64 n)
   int64_t pp_off = -1;       // arena offset of P' (passive internal child)
   size_t ema_smem = 0;
   bool ema_staged = true;
+};
+
+// SpMM work schedule for one vertex-range part of the gather source.
+struct PartSchedule {
+  dev::Seg* d_segs = nullptr;   // padded to a multiple of kSegPad
+  int64_t nseg_padded = 0;
+  int32_t* d_split_rows = nullptr;
+  int32_t* d_slot_begin = nullptr;
+  int nsplit_rows = 0, nslots = 0;
 };
 
 class Engine {
@@ -63,10 +75,16 @@ class Engine {
   void release_template();
   void plan_arena();
   void ensure_arena();
+  void ensure_colors(int64_t bytes);
   void gen_colors(const uint64_t* seeds, int count, uint8_t* d_out);
   // one DP over d_colors; total written to d_total (device), optional root accumulation
   void run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc,
               tcg_node_stats* stats);
+  void spmm(const float* X, float* Y, int64_t cols);
+  void hist(const uint8_t* d_colors, float* H);
+  float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
+  int64_t table_bytes(int64_t cols) const { return 4 * dev::table_floats(cols, n_); }
+
   // per-kernel event pairs recorded by run_dp when prof_ is set
   struct Prof {
     std::vector<cudaEvent_t> pool;
@@ -75,25 +93,23 @@ class Engine {
     cudaEvent_t get();
   };
   Prof* prof_ = nullptr;
-  void spmm(const float* X, float* Y, int cols);
-  float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
-  int64_t table_bytes(int64_t cols) const;
 
   tcg_config cfg_{};
   cudaStream_t stream_ = nullptr;
   int64_t launches_ = 0;
   uint64_t limit_override_ = 0;
+  int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per SpMM part (measured best on cfg3)
 
   // graph
   int32_t n_ = -1;
   int64_t nnz_ = 0;
   int64_t* d_row_ptr_ = nullptr;
   int32_t* d_col_ = nullptr;
-  dev::Seg* d_segs_ = nullptr;
-  int64_t ntasks_ = 0;
-  int32_t* d_split_rows_ = nullptr;
-  int32_t* d_split_slot_begin_ = nullptr;
-  int nsplit_rows_ = 0, nsplit_slots_ = 0;
+  // part count -> that many part schedules; [1] holds whole rows (also the
+  // one-hot histogram's schedule)
+  std::map<int, std::vector<PartSchedule>> sched_;
+  int parts_for_width(int zw) const;
+  int max_slots_ = 0;
 
   // template / plan
   bool have_template_ = false;
