@@ -134,6 +134,12 @@ def allreduce_max(dist, x, local):
     return float(t.item())
 
 
+def rank_seeds(rank, warmup, steps):
+    """Colorings of one rank: warm-up then timed seeds, disjoint across ranks (replicas)."""
+    s0 = 1 + rank * (warmup + steps)
+    return list(range(s0, s0 + warmup + steps))
+
+
 def barrier(dist, local):
     if dist is not None:
         dist.barrier()
@@ -227,7 +233,7 @@ def run_b200(args, rank, world, local, dist):
     ctx.set_template(t)
     need = ctx.required_device_bytes()
     log(f"[bench] rank {rank}: device bytes {need / 1e9:.2f} GB")
-    seed0 = 1 + rank * (args.warmup + args.steps)
+    seed0 = rank_seeds(rank, args.warmup, args.steps)[0]
     ctx.time(seed0, args.warmup, per_kernel=False)               # warm-up colorings
     barrier(dist, local)
     l0 = ctx.kernel_launches()
