@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -59,6 +60,65 @@ struct ArenaPlanner {
   }
   void free(int64_t off) { used.erase(off); }
 };
+
+// g(X2, i): combinadic contribution of the H2 colors of a set whose H1 part has
+// i colors (they take positions 1..i) -- kernels.cuh ema_blocked.
+int64_t h2_offset(uint32_t x2, int i) {
+  int64_t off = 0;
+  int pos = i;
+  for (int c = 0; c < 32; ++c)
+    if (x2 >> c & 1u) off += binom()(c, ++pos);
+  return off;
+}
+
+// Output groups and blocks of the color-split eMA for a node (s, a) with k colors.
+void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
+                   std::vector<dev::BlockDesc>& blocks) {
+  const int h1 = dev::kH1, p = s - a;
+  struct G { dev::GroupDesc d; int64_t work; std::vector<dev::BlockDesc> b; };
+  std::vector<G> gs;
+  const uint32_t h2mask = (k >= 32 ? ~0u : ((1u << k) - 1)) & ~((1u << h1) - 1);
+  int64_t total = 0;
+  // all subsets S2 of H2
+  for (uint32_t s2 = 0;; s2 = (s2 - h2mask) & h2mask) {
+    const int t = __builtin_popcount(s2), s1 = s - t;
+    if (s1 >= 0 && s1 <= h1) {
+      G g;
+      g.d = dev::GroupDesc{static_cast<int32_t>(h2_offset(s2, s1)), s1, 0, 0};
+      g.work = 0;
+      for (int i = std::max(0, s1 - p); i <= std::min(a, s1); ++i) {
+        const int j = s1 - i, ac = a - i;
+        if (ac < 0 || ac > t || p - j < 0) continue;
+        // subsets a2 of s2 with |a2| = ac
+        for (uint32_t a2 = 0;; a2 = (a2 - s2) & s2) {
+          if (__builtin_popcount(a2) == ac) {
+            const uint32_t p2 = s2 & ~a2;
+            g.b.push_back(dev::BlockDesc{static_cast<int32_t>(h2_offset(a2, i)),
+                                         static_cast<int32_t>(h2_offset(p2, j)), i * 8 + j, 0});
+            g.work += dev::cbin(h1, i) * dev::cbin(h1 - i, j);
+          }
+          if (a2 == s2) break;
+        }
+      }
+      std::sort(g.b.begin(), g.b.end(), [](const dev::BlockDesc& x, const dev::BlockDesc& y) {
+        return x.ij < y.ij || (x.ij == y.ij && x.a_off < y.a_off);
+      });
+      total += g.work;
+      gs.push_back(std::move(g));
+    }
+    if (s2 == h2mask) break;
+  }
+  if (total != binom()(k, s) * binom()(s, a)) throw logic_error("blocked eMA does not cover every split pair");
+  std::stable_sort(gs.begin(), gs.end(), [](const G& x, const G& y) { return x.work > y.work; });
+  groups.clear();
+  blocks.clear();
+  for (auto& g : gs) {
+    g.d.b0 = static_cast<int32_t>(blocks.size());
+    blocks.insert(blocks.end(), g.b.begin(), g.b.end());
+    g.d.b1 = static_cast<int32_t>(blocks.size());
+    groups.push_back(g.d);
+  }
+}
 
 void release_schedule(PartSchedule& s) {
   dfree(s.d_segs);
@@ -123,6 +183,16 @@ Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
     throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor));
   if (const char* e = std::getenv("TCG_PART_MB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 20;
+  if (const char* e = std::getenv("TCG_L2_PERSIST"); e && std::atoi(e) > 0) {
+    int win = 0;
+    TCG_CUDA(cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, cfg.device));
+    const size_t want = std::min<size_t>(static_cast<size_t>(prop.persistingL2CacheMaxSize),
+                                         static_cast<size_t>(std::atoi(e)) << 20);
+    TCG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
+    persist_max_ = std::min<int64_t>(win, static_cast<int64_t>(want));
+    std::fprintf(stderr, "[tcg] L2 persisting: max window %d B, set-aside %zu B (device max %d)\n", win,
+                 want, prop.persistingL2CacheMaxSize);
+  }
   TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   TCG_CUDA(cudaMalloc(&d_scalars_, 64));
   TCG_CUDA(cudaMalloc(&d_seeds_, 1024 * sizeof(uint64_t)));
@@ -153,6 +223,8 @@ void Engine::release_template() {
     dfree(e.d_split);
     dfree(e.d_drop);
     dfree(e.d_packed);
+    dfree(e.d_groups);
+    dfree(e.d_blocks);
   }
   exec_.clear();
   dfree(arena_);
@@ -180,6 +252,11 @@ void Engine::set_graph(const Csr& g) {
   // range so each part's rows (the L2-resident working set) fit in
   // part_bytes_.  Each CSR row is sorted, so a row's neighbours in a part are
   // one contiguous sub-range.  One schedule set per distinct part count.
+  // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
+  // sparse skewed graphs (cfg2, avg ~30) the hub rows stay L2-resident anyway
+  // and extra parts only add output passes (measured: profiles/ DESIGN.md 3).
+  if (!std::getenv("TCG_PART_MB"))
+    part_bytes_ = (n_ > 0 && nnz_ / std::max(n_, 1) >= 64) ? (64ll << 20) : (128ll << 20);
   std::vector<int> counts{1};
   for (int zw : {8, 16, 32}) counts.push_back(parts_for_width(zw));
   std::sort(counts.begin(), counts.end());
@@ -268,6 +345,22 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     const int64_t staged = static_cast<int64_t>((e.a_leaf ? 0 : e.Ca) + e.Cp) * (dev::kTileV + 1) * 4;
     e.ema_staged = staged <= max_smem - 4096;
     e.ema_smem = e.ema_staged ? static_cast<size_t>(staged) : 0;
+    static const int blocked_mode = [] {
+      const char* s = std::getenv("TCG_EMA_BLOCKED");
+      return s ? std::atoi(s) : 1;
+    }();
+    // FMA-heavy nodes only: narrow nodes are bound by their output writes,
+    // which the 8-column chunks of ema_node coalesce better
+    if (blocked_mode && !e.a_leaf && !e.root && e.ema_staged && k >= dev::kH1 &&
+        (e.pairs >= 16 || blocked_mode == 2)) {
+      std::vector<dev::GroupDesc> gr;
+      std::vector<dev::BlockDesc> bl;
+      build_blocked(k, e.size, e.sa, gr, bl);
+      e.blocked = true;
+      e.ngroups = static_cast<int>(gr.size());
+      e.d_groups = dupload(gr, stream_);
+      e.d_blocks = dupload(bl, stream_);
+    }
     exec_.push_back(e);
   }
   TCG_CUDA(cudaStreamSynchronize(stream_));
@@ -366,12 +459,40 @@ void Engine::coloring(uint64_t seed, uint8_t* host_colors) {
 template <int ZW, bool ONEHOT>
 static void launch_spmm_part(const PartSchedule& ps, cudaStream_t s, const int32_t* col,
                              const float* X, const uint8_t* colors, int color_base, float* Y,
-                             double* partial, bool first, int64_t& launches) {
+                             double* partial, bool first, int64_t& launches,
+                             const char* win_base = nullptr, int64_t win_bytes = 0) {
   constexpr int spw = 128 / ZW;  // segments per warp
   const int64_t ntasks = ps.nseg_padded / spw;
   const int64_t blocks = (ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
-  dev::spmm_part<ZW, ONEHOT><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
-      ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
+  static const int rounds = [] {
+    const char* e = std::getenv("TCG_SPMM_R");
+    return e ? std::atoi(e) : 8;
+  }();
+  if (rounds == 16) {
+    dev::spmm_part<ZW, ONEHOT, 16><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
+        ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
+  } else if (win_bytes > 0) {
+    // pin the part's gather window in L2 (persisting) against the index and
+    // output streams that pass through L2 during the launch
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3(static_cast<unsigned>(blocks));
+    lc.blockDim = dim3(dev::kSpmmWarps * 32);
+    lc.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = const_cast<char*>(win_base);
+    at[0].val.accessPolicyWindow.num_bytes = static_cast<size_t>(win_bytes);
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    lc.attrs = at;
+    lc.numAttrs = 1;
+    TCG_CUDA(cudaLaunchKernelEx(&lc, dev::spmm_part<ZW, ONEHOT, 8>, ps.d_segs, ntasks, col, X, colors,
+                                color_base, Y, partial, first ? 1 : 0));
+  } else {
+    dev::spmm_part<ZW, ONEHOT, 8><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
+        ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
+  }
   ++launches;
   if (ps.nsplit_rows) {
     const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * ZW;
@@ -388,11 +509,15 @@ void Engine::spmm(const float* X, float* Y, int64_t cols) {
     const float* Xp = X + static_cast<int64_t>(p) * n_ * dev::kZ;
     float* Yp = Y + static_cast<int64_t>(p) * n_ * dev::kZ;
     const auto& parts = sched_.at(parts_for_width(zw));
-    for (int s = 0; s < static_cast<int>(parts.size()); ++s) {
+    const int P = static_cast<int>(parts.size());
+    for (int s = 0; s < P; ++s) {
       const PartSchedule& ps = parts[s];
-      if (zw == 32) launch_spmm_part<32, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
-      else if (zw == 16) launch_spmm_part<16, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
-      else launch_spmm_part<8, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+      const int64_t r0 = static_cast<int64_t>(n_) * s / P, r1 = static_cast<int64_t>(n_) * (s + 1) / P;
+      const char* wb = persist_max_ > 0 ? reinterpret_cast<const char*>(Xp + r0 * zw) : nullptr;
+      const int64_t wn = persist_max_ > 0 ? std::min<int64_t>((r1 - r0) * zw * 4, persist_max_) : 0;
+      if (zw == 32) launch_spmm_part<32, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
+      else if (zw == 16) launch_spmm_part<16, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
+      else launch_spmm_part<8, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
     }
   }
   TCG_CUDA(cudaGetLastError());
@@ -489,6 +614,13 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
         if (e.a_leaf) {
           if (e.ema_staged) launch_node<true, true>(e, plan_.k, stream_, n_, A, P, d_colors, out);
           else launch_node<true, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);
+        } else if (e.blocked) {
+          auto kern = dev::ema_blocked<true>;
+          TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(e.ema_smem)));
+          kern<<<static_cast<unsigned>((n_ + dev::kTileV - 1) / dev::kTileV), 256, e.ema_smem, stream_>>>(
+              A, P, static_cast<const dev::GroupDesc*>(e.d_groups), e.ngroups,
+              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, out);
         } else {
           if (e.ema_staged) launch_node<false, true>(e, plan_.k, stream_, n_, A, P, d_colors, out);
           else launch_node<false, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);

@@ -31,6 +31,11 @@ struct NodeExec {
   int2* d_split = nullptr;   // by-parent (I_a, I_p) pairs, [Cs * pairs]
   int32_t* d_drop = nullptr; // active leaf: [Cs * k] column of S minus c, or -1
   uint32_t* d_packed = nullptr;  // (I_a | I_p << 16) when both fit in 16 bits
+  // register-blocked eMA (kernels.cuh ema_blocked): output groups + blocks
+  bool blocked = false;
+  void* d_groups = nullptr;      // dev::GroupDesc[ngroups], sorted by work
+  void* d_blocks = nullptr;      // dev::BlockDesc[]
+  int ngroups = 0;
   int64_t out_off = -1;      // arena offset of M_s (root: fp64 n)
   int64_t pp_off = -1;       // arena offset of P' (passive internal child)
   size_t ema_smem = 0;
@@ -99,6 +104,7 @@ class Engine {
   int64_t launches_ = 0;
   uint64_t limit_override_ = 0;
   int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per SpMM part (measured best on cfg3)
+  int64_t persist_max_ = 0;          // > 0: pin each part's gather window in L2 (TCG_L2_PERSIST=MB)
 
   // graph
   int32_t n_ = -1;
