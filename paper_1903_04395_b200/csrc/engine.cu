@@ -124,6 +124,7 @@ void release_schedule(PartSchedule& s) {
   dfree(s.d_segs);
   dfree(s.d_split_rows);
   dfree(s.d_slot_begin);
+  dfree(s.d_slot_row);
   s = PartSchedule{};
 }
 
@@ -164,6 +165,10 @@ PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<in
   if (ps.nsplit_rows) {
     ps.d_split_rows = dupload(split_rows, stream);
     ps.d_slot_begin = dupload(slot_begin, stream);
+    std::vector<int32_t> slot_row(static_cast<size_t>(slot));
+    for (int r = 0; r < ps.nsplit_rows; ++r)
+      for (int q = slot_begin[r]; q < slot_begin[r + 1]; ++q) slot_row[q] = split_rows[r];
+    ps.d_slot_row = dupload(slot_row, stream);
   }
   TCG_CUDA(cudaStreamSynchronize(stream));
   return ps;
@@ -215,6 +220,8 @@ void Engine::release_graph() {
     for (auto& s : kv.second) release_schedule(s);
   sched_.clear();
   dfree(d_tile_tot_);
+  dfree(d_row_order_);
+  dfree(d_counter_);
   n_ = -1;
 }
 
@@ -225,6 +232,7 @@ void Engine::release_template() {
     dfree(e.d_packed);
     dfree(e.d_groups);
     dfree(e.d_blocks);
+    dfree(e.d_ins);
   }
   exec_.clear();
   dfree(arena_);
@@ -285,6 +293,15 @@ void Engine::set_graph(const Csr& g) {
       vec.push_back(build_schedule(bnd[s], bnd[s + 1], s == 0, stream_));
       max_slots_ = std::max(max_slots_, vec.back().nslots);
     }
+  }
+  {  // rows by degree, descending, for the per-coloring color bucketing
+    std::vector<int32_t> order(static_cast<size_t>(n_));
+    for (int32_t v = 0; v < n_; ++v) order[v] = v;
+    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
+      return g.row_ptr[x + 1] - g.row_ptr[x] > g.row_ptr[y + 1] - g.row_ptr[y];
+    });
+    d_row_order_ = dupload(order, stream_);
+    TCG_CUDA(cudaMalloc(&d_counter_, 64));
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
@@ -363,6 +380,51 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     }
     exec_.push_back(e);
   }
+  // Leaf-pushed SpMM: a node whose passive child p is (h, 1, h-1) gathers
+  // p's own P' (C(k,h-1) columns) per neighbour color instead of M_p
+  // (C(k,h) columns); p's eMA is then skipped.  Opt-in (TCG_LSPMM=1): on B200
+  // the per-(vertex, color) buckets (~deg/k neighbours) and the Q round trip
+  // cost more than the gathered columns save (measured cfg3: node 2 SpMM
+  // 26.6 -> 70 ms), so the direct panel SpMM is the default.
+  need_bucket_ = false;
+  static const int lmode = [] {
+    const char* s = std::getenv("TCG_LSPMM");
+    return s ? std::atoi(s) : 0;
+  }();
+  static const int64_t q_budget = [] {
+    const char* s = std::getenv("TCG_Q_GB");
+    return (s ? std::atoll(s) : 12ll) << 30;
+  }();
+  std::vector<int> pos(plan_.num_nodes, -1);
+  for (size_t i = 0; i < exec_.size(); ++i) pos[exec_[i].id] = static_cast<int>(i);
+  for (auto& e : exec_) {
+    if (!lmode || e.p_leaf) continue;
+    NodeExec& c = exec_[pos[e.p]];
+    if (!c.a_leaf || c.root) continue;
+    const int32_t Cx = static_cast<int32_t>(B(k, c.size - 1));
+    const int64_t comb = static_cast<int64_t>(Cx + e.Cp) * (dev::kTileV + 1) * 4;
+    if (Cx >= e.Cp || comb > max_smem - 4096) continue;
+    e.lspmm = true;
+    e.Cx = Cx;
+    e.comb_smem = static_cast<size_t>(comb);
+    c.skip_ema = !(cfg_.flags & TCG_KEEP_TABLES);
+    need_bucket_ = true;
+    std::vector<int32_t> ins(static_cast<size_t>(k) * Cx, -1);
+    int cs[kMaxK], us[kMaxK];
+    for (int32_t x = 0; x < Cx; ++x) {
+      set_of(k, x, c.size - 1, cs);
+      for (int col = 0; col < k; ++col) {
+        if (std::find(cs, cs + c.size - 1, col) != cs + c.size - 1) continue;
+        int m = 0;
+        for (int q = 0; q < c.size - 1 && cs[q] < col; ++q) us[m++] = cs[q];
+        us[m++] = col;
+        for (int q = 0; q < c.size - 1; ++q)
+          if (cs[q] > col) us[m++] = cs[q];
+        ins[static_cast<size_t>(col) * Cx + x] = static_cast<int32_t>(index_of(us, c.size));
+      }
+    }
+    e.d_ins = dupload(ins, stream_);
+  }
   TCG_CUDA(cudaStreamSynchronize(stream_));
   have_template_ = true;
   if (n_ >= 0) plan_arena();
@@ -375,11 +437,35 @@ void Engine::plan_arena() {
   table_off_.assign(plan_.num_nodes, -1);
   pprime_off_.assign(plan_.num_nodes, -1);
   hist_off_ = need_hist_ ? ap.alloc(table_bytes(plan_.k)) : -1;
+  colb_off_ = need_bucket_ ? ap.alloc(4 * std::max<int64_t>(nnz_, 1)) : -1;
+  boff_off_ = need_bucket_ ? ap.alloc(8 * static_cast<int64_t>(n_) * (plan_.k + 1)) : -1;
+  const int64_t q_budget = (std::getenv("TCG_Q_GB") ? std::atoll(std::getenv("TCG_Q_GB")) : 12ll) << 30;
+  std::vector<int64_t> child_pp(plan_.num_nodes, -1);  // P' kept alive for an LSpMM parent
+  int64_t lslots = 0;
+  const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
   for (auto& e : exec_) {
     if (!e.p_leaf) {
       e.pp_off = ap.alloc(table_bytes(e.Cp));
       pprime_off_[e.p] = e.pp_off;
-      if (!keep) ap.free(table_off_[e.p]);
+      if (e.lspmm) {
+        e.qchunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(plan_.k, q_budget / std::max<int64_t>(table_bytes(e.Cx), 1))));
+        e.q_off = ap.alloc(static_cast<int64_t>(e.qchunk) * table_bytes(e.Cx));
+        lslots = std::max<int64_t>(lslots, static_cast<int64_t>(e.qchunk) * full_slots);
+        if (!keep) {
+          ap.free(e.q_off);
+          if (child_pp[e.p] >= 0) ap.free(child_pp[e.p]);
+          if (table_off_[e.p] >= 0) ap.free(table_off_[e.p]);
+        }
+      } else if (!keep) {
+        ap.free(table_off_[e.p]);
+      }
+    }
+    if (e.skip_ema) {                 // M of this node is never needed
+      table_off_[e.id] = -1;
+      e.out_off = -1;
+      if (!e.p_leaf) child_pp[e.id] = e.pp_off;  // X of the parent's LSpMM
+      if (!keep && !e.a_leaf) ap.free(table_off_[e.a]);
+      continue;
     }
     e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(e.Cs));
     table_off_[e.id] = e.out_off;
@@ -389,7 +475,7 @@ void Engine::plan_arena() {
     }
   }
   arena_bytes_ = ap.peak;
-  partial_bytes_ = static_cast<int64_t>(max_slots_) * dev::kZ * 8;
+  partial_bytes_ = std::max<int64_t>(static_cast<int64_t>(max_slots_), lslots) * dev::kZ * 8;
 }
 
 int64_t Engine::required_bytes() const {
@@ -523,6 +609,52 @@ void Engine::spmm(const float* X, float* Y, int64_t cols) {
   TCG_CUDA(cudaGetLastError());
 }
 
+// Leaf-pushed SpMM: P'_s = sum_c (A D_c X) inserted at S = x u {c}, in color
+// chunks of e.qchunk (Q chunk buffer at e.q_off).
+void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
+  const PartSchedule& full = sched_.at(1)[0];
+  float* Q = table_ptr(e.q_off);
+  const int64_t q_stride = dev::table_floats(e.Cx, n_);
+  const int k = plan_.k;
+  for (int c0 = 0; c0 < k; c0 += e.qchunk) {
+    const int nc = std::min(e.qchunk, k - c0);
+    const int P = dev::num_panels(e.Cx);
+    for (int p = 0; p < P; ++p) {
+      const int zw = dev::panel_width(e.Cx, p);
+      const float* Xp = X + static_cast<int64_t>(p) * n_ * dev::kZ;
+      float* Qp = Q + static_cast<int64_t>(p) * n_ * dev::kZ;
+      const int spw = 128 / zw;
+      const int64_t ntasks = full.nseg_padded / spw;
+      const int64_t bpc = (ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
+      const unsigned grid = static_cast<unsigned>(bpc * nc);
+      const int64_t* boff = reinterpret_cast<const int64_t*>(arena_ + boff_off_);
+      const int32_t* colb = reinterpret_cast<const int32_t*>(arena_ + colb_off_);
+      if (zw == 32)
+        dev::spmm_bucket<32><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
+      else if (zw == 16)
+        dev::spmm_bucket<16><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
+      else
+        dev::spmm_bucket<8><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
+      ++launches_;
+      if (full.nsplit_rows) {
+        const int64_t total = static_cast<int64_t>(full.nsplit_rows) * zw;
+        for (int cl = 0; cl < nc; ++cl) {
+          dev::spmm_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
+              full.d_split_rows, full.d_slot_begin, full.nsplit_rows,
+              d_partial_ + static_cast<int64_t>(cl) * full.nslots * zw, Qp + cl * q_stride, zw, 1);
+          ++launches_;
+        }
+      }
+    }
+    auto kern = dev::lspmm_combine;
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.comb_smem)));
+    kern<<<static_cast<unsigned>((n_ + dev::kTileV - 1) / dev::kTileV), 512, e.comb_smem, stream_>>>(
+        Q, q_stride, c0, nc, e.d_ins, e.Cx, e.Cp, n_, Pp, c0 == 0 ? 1 : 0);
+    ++launches_;
+  }
+  TCG_CUDA(cudaGetLastError());
+}
+
 // P' of a leaf passive child: SpMM against the one-hot color table, read as
 // 1-byte colors (whole rows; the colors array is L2-resident).
 int Engine::parts_for_width(int zw) const {
@@ -575,12 +707,23 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     return ev.size() - 1;
   };
   const float* H = nullptr;
-  if (need_hist_ && n_ > 0) {
+  if ((need_hist_ || need_bucket_) && n_ > 0) {
     size_t h0 = 0;
     if (prof_) { h0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-    hist(d_colors, table_ptr(hist_off_));
+    if (need_bucket_) {
+      // color-bucketed CSR for the leaf-pushed SpMMs; yields the histogram too
+      TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
+      dev::color_bucket<<<148 * 8, 256, 0, stream_>>>(
+          d_row_ptr_, d_col_, d_colors, d_row_order_, n_, plan_.k,
+          reinterpret_cast<int32_t*>(arena_ + colb_off_), reinterpret_cast<int64_t*>(arena_ + boff_off_),
+          need_hist_ ? table_ptr(hist_off_) : nullptr, dev::panel_width(plan_.k, 0), d_counter_);
+      ++launches_;
+      TCG_CUDA(cudaGetLastError());
+    } else {
+      hist(d_colors, table_ptr(hist_off_));
+    }
     if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-    H = table_ptr(hist_off_);
+    if (need_hist_) H = table_ptr(hist_off_);
   }
   struct Marks { size_t t0, t1, t2; };
   std::vector<Marks> marks;
@@ -591,9 +734,21 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     if (!e.p_leaf && n_ > 0) {
       size_t p0 = 0;
       if (prof_) { p0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-      spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
+      if (e.lspmm) {
+        const NodeExec* c = nullptr;
+        for (auto& x : exec_)
+          if (x.id == e.p) c = &x;
+        lspmm(e, c->p_leaf ? H : table_ptr(c->pp_off), table_ptr(e.pp_off));
+      } else {
+        spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
+      }
       if (prof_) { prof_->spmm.emplace_back(p0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       P = table_ptr(e.pp_off);
+    }
+    if (e.skip_ema) {
+      if (stats) { m.t1 = mark(); m.t2 = mark(); }
+      marks.push_back(m);
+      continue;
     }
     if (stats) m.t1 = mark();
     size_t q0 = 0;
@@ -831,8 +986,9 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
     if (!e.p_leaf) {
       t.spmm_launches += count;
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
-      t.spmm_gathered_bytes += count * nnz * 4.0 * (static_cast<double>(dev::num_panels(e.Cp) - 1) * dev::kZ +
-                                                     dev::last_panel_width(e.Cp));
+      const int32_t gc = e.lspmm ? e.Cx : e.Cp;  // columns actually gathered per neighbour
+      t.spmm_gathered_bytes += count * nnz * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
+                                                     dev::last_panel_width(gc));
     }
     t.ema_launches += count;
     t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));

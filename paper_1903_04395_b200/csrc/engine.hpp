@@ -36,6 +36,13 @@ struct NodeExec {
   void* d_groups = nullptr;      // dev::GroupDesc[ngroups], sorted by work
   void* d_blocks = nullptr;      // dev::BlockDesc[]
   int ngroups = 0;
+  // leaf-pushed SpMM (kernels.cuh spmm_bucket + lspmm_combine): P' of this node
+  // from the P' (X) of its active-leaf passive child, whose eMA is skipped
+  bool lspmm = false, skip_ema = false;
+  int Cx = 0, qchunk = 0;
+  int32_t* d_ins = nullptr;      // [k * Cx] column of (x u {c}) in P', or -1
+  int64_t q_off = -1;
+  size_t comb_smem = 0;
   int64_t out_off = -1;      // arena offset of M_s (root: fp64 n)
   int64_t pp_off = -1;       // arena offset of P' (passive internal child)
   size_t ema_smem = 0;
@@ -48,6 +55,7 @@ struct PartSchedule {
   int64_t nseg_padded = 0;
   int32_t* d_split_rows = nullptr;
   int32_t* d_slot_begin = nullptr;
+  int32_t* d_slot_row = nullptr;  // partial slot -> row
   int nsplit_rows = 0, nslots = 0;
 };
 
@@ -87,6 +95,7 @@ class Engine {
               tcg_node_stats* stats);
   void spmm(const float* X, float* Y, int64_t cols);
   void hist(const uint8_t* d_colors, float* H);
+  void lspmm(const NodeExec& e, const float* X, float* Pp);
   float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
   int64_t table_bytes(int64_t cols) const { return 4 * dev::table_floats(cols, n_); }
 
@@ -116,6 +125,8 @@ class Engine {
   std::map<int, std::vector<PartSchedule>> sched_;
   int parts_for_width(int zw) const;
   int max_slots_ = 0;
+  int32_t* d_row_order_ = nullptr;   // rows by degree, descending (color_bucket)
+  int* d_counter_ = nullptr;
 
   // template / plan
   bool have_template_ = false;
@@ -128,6 +139,8 @@ class Engine {
   // arena + per-coloring buffers
   int64_t arena_bytes_ = 0;
   int64_t hist_off_ = -1;
+  bool need_bucket_ = false;         // some node uses the leaf-pushed SpMM
+  int64_t colb_off_ = -1, boff_off_ = -1;
   std::vector<int64_t> table_off_;   // per node id: arena offset of its table (internal)
   std::vector<int64_t> pprime_off_;  // per node id: offset of P' computed from it
   char* arena_ = nullptr;

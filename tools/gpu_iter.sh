@@ -1,4 +1,5 @@
 # build-verify-measure loop: tests, smoke, benches, launch list
+TCG_LSPMM=1 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 900 -k "node_tables or small_instances or full_size" 2>&1 | tail -2
 TCG_EMA_BLOCKED=2 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 900 -k "node_tables or small_instances or large_k or cfg1" 2>&1 | tail -2
 python -m pytest tests/test_gpu_parity.py -x -q -m gpu --timeout 900 2>&1 | tail -4
 python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
