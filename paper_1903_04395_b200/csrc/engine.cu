@@ -680,8 +680,11 @@ static void launch_node(const NodeExec& e, int k, cudaStream_t s, int32_t n, con
   auto kern = dev::ema_node<AL, ST>;
   TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
   const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
-  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.d_packed, e.d_drop, k,
-                                                      e.pairs, e.Ca, e.Cp, e.Cs, n, out);
+  // one warp per 8-column output chunk (up to 16): light nodes get small CTAs,
+  // so many tiles co-reside per SM and staging overlaps compute across CTAs
+  const int warps = std::max(2, std::min(dev::kEmaWarps, (e.Cs + 7) / 8));
+  kern<<<tiles, warps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.d_packed, e.d_drop, k,
+                                             e.pairs, e.Ca, e.Cp, e.Cs, n, out);
 }
 
 template <bool AL, bool ST>

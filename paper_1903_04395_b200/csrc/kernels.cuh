@@ -495,7 +495,7 @@ ema_node(const float* __restrict__ Am, const float* __restrict__ Pm,
     return valid ? Am[panel_offset(Ca, n, v, ia)] : 0.f;
   };
   const int nchunks = (Cs + 7) / 8;
-  for (int q = warp; q < nchunks; q += kEmaWarps) {
+  for (int q = warp; q < nchunks; q += blockDim.x >> 5) {
     float r[8];
     if (ALEAF) {
 #pragma unroll
