@@ -368,8 +368,15 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     }();
     // FMA-heavy nodes only: narrow nodes are bound by their output writes,
     // which the 8-column chunks of ema_node coalesce better
-    if (blocked_mode && !e.a_leaf && !e.root && e.ema_staged && k >= dev::kH1 &&
-        (e.pairs >= 16 || blocked_mode == 2)) {
+    // vertex-per-CTA when a 32-vertex tile does not fit: one vertex's rows
+    auto row_floats = [](int64_t C) { return C <= 0 ? 0 : dev::table_floats(C, 1); };
+    const int64_t vsm = 4 * (((e.a_leaf ? 0 : row_floats(e.Ca)) + 3) / 4 * 4 + row_floats(e.Cp));
+    if (!e.ema_staged && vsm <= max_smem - 4096 && (e.a_leaf || e.root || k >= dev::kH1)) {
+      e.vtx = true;
+      e.vtx_smem = static_cast<size_t>(vsm);
+    }
+    if (!e.a_leaf && !e.root && k >= dev::kH1 &&
+        ((blocked_mode && e.ema_staged && (e.pairs >= 16 || blocked_mode == 2)) || e.vtx)) {
       std::vector<dev::GroupDesc> gr;
       std::vector<dev::BlockDesc> bl;
       build_blocked(k, e.size, e.sa, gr, bl);
@@ -758,7 +765,27 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
     if (prof_) { q0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
     if (n_ > 0) {
-      if (e.root) {
+      const unsigned vgrid = static_cast<unsigned>(std::min<int64_t>(n_, 148 * 16));
+      if (e.vtx) {
+        auto smem_attr = [&](const void* f) {
+          TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.vtx_smem)));
+        };
+        if (e.root) {
+          double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
+          smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_root));
+          dev::ema_vtx_root<<<vgrid, 256, e.vtx_smem, stream_>>>(A, P, d_colors, e.d_split, e.pairs, e.Ca, e.Cp,
+                                                                   e.a_leaf ? 1 : 0, n_, rout, d_root_acc);
+        } else if (e.a_leaf) {
+          smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_aleaf));
+          dev::ema_vtx_aleaf<<<vgrid, 256, e.vtx_smem, stream_>>>(P, d_colors, e.d_drop, plan_.k, e.Cp, e.Cs, n_,
+                                                                    table_ptr(e.out_off));
+        } else {
+          smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_blocked));
+          dev::ema_vtx_blocked<<<vgrid, 256, e.vtx_smem, stream_>>>(
+              A, P, static_cast<const dev::GroupDesc*>(e.d_groups), e.ngroups,
+              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, table_ptr(e.out_off));
+        }
+      } else if (e.root) {
         double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
         if (e.a_leaf) {
           if (e.ema_staged) launch_root<true, true>(e, stream_, n_, A, P, d_colors, rout, d_root_acc, d_tile_tot_);
@@ -793,7 +820,11 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   if (n_ > 0 && !exec_.empty()) {
-    dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, ntiles, d_total);
+    if (exec_.back().vtx)  // vertex-per-CTA root wrote per-vertex values only
+      dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
+                                                n_, d_total);
+    else
+      dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, ntiles, d_total);
     ++launches_;
   } else {
     TCG_CUDA(cudaMemsetAsync(d_total, 0, sizeof(double), stream_));

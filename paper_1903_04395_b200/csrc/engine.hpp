@@ -47,6 +47,8 @@ struct NodeExec {
   int64_t pp_off = -1;       // arena offset of P' (passive internal child)
   size_t ema_smem = 0;
   bool ema_staged = true;
+  bool vtx = false;              // vertex-per-CTA eMA (32-vertex tile does not fit smem)
+  size_t vtx_smem = 0;
 };
 
 // SpMM work schedule for one vertex-range part of the gather source.

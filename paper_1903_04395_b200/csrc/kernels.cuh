@@ -679,6 +679,156 @@ ema_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
 }
 #undef TCG_IJ
 
+// ------------------------------------------ vertex-per-CTA eMA (huge nodes)
+// When a 32-vertex tile of a node's inputs does not fit in shared memory
+// (k = 15/17: a single A row can be 97 KB), a CTA owns ONE vertex at a time:
+// its A and P rows are staged contiguously in smem (128 B panel rows, fully
+// coalesced loads) and the threads split the node's work -- output groups
+// (blocked micro-patterns), parent columns (active leaf) or split pairs (root).
+// Persistent grid-stride over vertices; several CTAs per SM overlap staging
+// with compute.
+// floats of one vertex's panel-padded row (a multiple of 4)
+__device__ __forceinline__ int row_floats(int C) { return (num_panels(C) - 1) * kZ + last_panel_width(C); }
+
+__device__ __forceinline__ void stage_row(const float* __restrict__ T, int C, int32_t n, int64_t v,
+                                          float* dst) {
+  const int panels = num_panels(C);
+  const int zl = last_panel_width(C);
+  const int total4 = ((panels - 1) * kZ + zl) / 4;
+  for (int f = threadIdx.x; f < total4; f += blockDim.x) {
+    const int p = (f * 4) / kZ, z4 = (f * 4) % kZ;
+    const int zw = p == panels - 1 ? zl : kZ;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
+    *reinterpret_cast<float4*>(dst + p * kZ + z4) = x;
+  }
+}
+
+#define TCG_IJV(I, J) \
+  case I * 8 + J: micro_block_v<I, J>(sA + bd.x, sP + bd.y, acc); break;
+
+template <int I, int J>
+__device__ __forceinline__ void micro_block_v(const float* __restrict__ sa, const float* __restrict__ sp,
+                                              float (&acc)[kMaxAcc]) {
+  constexpr int NA = cbin(kH1, I), NP = cbin(kH1, J), NT = cbin(kH1, I) * cbin(kH1 - I, J);
+  float a[kMaxAcc], p[kMaxAcc];
+#pragma unroll
+  for (int x = 0; x < NA; ++x) a[x] = sa[x];
+#pragma unroll
+  for (int x = 0; x < NP; ++x) p[x] = sp[x];
+  micro_fma<I, J>(a, p, acc, std::make_integer_sequence<int, NT>{});
+}
+
+// groups: GroupDesc list (sorted by work); blocks: BlockDesc list.  Thread t
+// takes groups in a snake order over the threads (balanced, deterministic).
+__global__ void __launch_bounds__(256)
+ema_vtx_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
+                const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks,
+                int Ca, int Cp, int Cs, int32_t n, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  float* sA = smem;
+  float* sP = smem + row_floats(Ca);  // stage_row writes the panel-padded row
+  const int T = blockDim.x;
+  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    __syncthreads();
+    stage_row(Am, Ca, n, v, sA);
+    stage_row(Pm, Cp, n, v, sP);
+    __syncthreads();
+    for (int r = 0;; ++r) {
+      const int gi = (r & 1) ? (r + 1) * T - 1 - static_cast<int>(threadIdx.x) : r * T + static_cast<int>(threadIdx.x);
+      if (r * T >= ngroups) break;
+      if (gi >= ngroups) continue;
+      const GroupDesc gd = groups[gi];
+      float acc[kMaxAcc];
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
+      for (int b = gd.b0; b < gd.b1; ++b) {
+        const BlockDesc b4 = blocks[b];
+        const int2 bd = make_int2(b4.a_off, b4.p_off);
+        switch (b4.ij) {
+          TCG_IJV(0, 1) TCG_IJV(0, 2) TCG_IJV(0, 3) TCG_IJV(0, 4) TCG_IJV(0, 5) TCG_IJV(0, 6)
+          TCG_IJV(1, 0) TCG_IJV(1, 1) TCG_IJV(1, 2) TCG_IJV(1, 3) TCG_IJV(1, 4) TCG_IJV(1, 5)
+          TCG_IJV(2, 0) TCG_IJV(2, 1) TCG_IJV(2, 2) TCG_IJV(2, 3) TCG_IJV(2, 4)
+          TCG_IJV(3, 0) TCG_IJV(3, 1) TCG_IJV(3, 2) TCG_IJV(3, 3)
+          TCG_IJV(4, 0) TCG_IJV(4, 1) TCG_IJV(4, 2)
+          TCG_IJV(5, 0) TCG_IJV(5, 1)
+          TCG_IJV(6, 0) TCG_IJV(0, 0)
+          default: break;
+        }
+      }
+      const int cnt = cbin(kH1, gd.s1);
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x)
+        if (x < cnt) out[panel_offset(Cs, n, v, gd.out_off + x)] = acc[x];
+    }
+  }
+}
+#undef TCG_IJV
+
+// Active leaf, one vertex per CTA: M_s[v,S] = P'[v, S minus color(v)] or 0.
+__global__ void __launch_bounds__(256)
+ema_vtx_aleaf(const float* __restrict__ Pm, const uint8_t* __restrict__ colors,
+              const int32_t* __restrict__ drop, int k, int Cp, int Cs, int32_t n, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    __syncthreads();
+    stage_row(Pm, Cp, n, v, smem);
+    __syncthreads();
+    const int c = colors[v];
+    const int panels = num_panels(Cs);
+    // write the row panel by panel, float4 per thread (coalesced 128 B rows)
+    const int zl = last_panel_width(Cs);
+    const int total4 = ((panels - 1) * kZ + zl) / 4;
+    for (int f = threadIdx.x; f < total4; f += blockDim.x) {
+      const int p = (f * 4) / kZ, z4 = (f * 4) % kZ;
+      const int zw = p == panels - 1 ? zl : kZ;
+      float r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int S = p * kZ + z4 + j;
+        const int d = S < Cs ? __ldg(drop + static_cast<int64_t>(S) * k + c) : -1;
+        r[j] = d >= 0 ? smem[d] : 0.f;
+      }
+      *reinterpret_cast<float4*>(out + static_cast<int64_t>(p) * n * kZ + v * zw + z4) = make_float4(r[0], r[1], r[2], r[3]);
+    }
+  }
+}
+
+// Root, one vertex per CTA: fp64 dot product over the split pairs, fixed-order
+// block reduction; root_out[v] (the tile totals are then reduced by root_reduce
+// over root_out itself).
+__global__ void __launch_bounds__(256)
+ema_vtx_root(const float* __restrict__ Am, const float* __restrict__ Pm, const uint8_t* __restrict__ colors,
+             const int2* __restrict__ split, int pairs, int Ca, int Cp, int aleaf, int32_t n,
+             double* __restrict__ root_out, double* __restrict__ root_acc) {
+  extern __shared__ float smem[];
+  __shared__ double red[256];
+  float* sA = smem;
+  float* sP = smem + (aleaf ? 0 : row_floats(Ca));
+  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    __syncthreads();
+    if (!aleaf) stage_row(Am, Ca, n, v, sA);
+    stage_row(Pm, Cp, n, v, sP);
+    __syncthreads();
+    const int c = colors[v];
+    double acc = 0;
+    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+      const int2 s = __ldg(split + p);
+      const float a = aleaf ? (s.x == c ? 1.f : 0.f) : sA[s.x];
+      acc = fma(static_cast<double>(a), static_cast<double>(sP[s.y]), acc);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      root_out[v] = red[0];
+      if (root_acc) root_acc[v] += red[0];
+    }
+  }
+}
+
 // Root node: one parent column; warps split the pair list, fp64 throughout,
 // fixed-order reduction; per-vertex counts (fp64) and per-tile totals.
 template <bool ALEAF, bool STAGED>

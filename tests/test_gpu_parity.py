@@ -251,6 +251,22 @@ def test_large_k_unstaged_ema(k):
     assert rel_err([total], [ototal]) <= REL
 
 
+@pytest.mark.parametrize("name", ["cfg4", "cfg5"])
+def test_k15_k17_templates_small_graph(name):
+    """The cfg4/cfg5 templates (k=15/17): wide nodes take the vertex-per-CTA
+    eMA kernels (blocked, active-leaf, root) -- parity with the oracle."""
+    g = T.generate_rmat(T.RmatSpec(9, 48 << 9, .45, .15, .15, .25, 7))
+    parents = CFG_TEMPLATES[name]
+    k = len(parents)
+    c = ctx_for(g, T.template_from_parents(parents, 0))
+    total, pv, _ = c.run_coloring(2, per_vertex=True)
+    plan = O.partition(k, parents_to_edges(parents), 0)
+    ototal, opv, _ = O.run_iteration(g.n, g.csc_col_ptr, g.csc_rows, plan, O.random_coloring(g.n, k, 2))
+    assert ototal > 0
+    assert_close(pv, opv)
+    assert rel_err([total], [ototal]) <= REL
+
+
 def test_given_coloring_matches_seeded(cfg1_golden):
     gold = cfg1_golden
     g = T.Graph.from_csr(16384, gold["row_ptr"], gold["col"])
