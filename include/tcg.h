@@ -191,6 +191,27 @@ typedef struct {
 int tcg_time_colorings(tcg_ctx* ctx, uint64_t seed, int count, int per_kernel, double* totals,
                        tcg_timing* out);
 
+/* ------------------------------------------------------------------------
+ * Vertex sharding: the context owns a contiguous range of
+ * vertex rows (balanced by degree + average degree); every count table holds
+ * only those rows (padded to the largest shard), and before each SpMM panel
+ * the passive table's panel is all-gathered from every rank.  eMA is local;
+ * rooted totals are summed in rank order on the host (deterministic).
+ * Call before tcg_set_graph.  All ranks call the same entry points with the
+ * same arguments (graph, template, seeds).
+ * ---------------------------------------------------------------------- */
+/* Row bounds of each shard: bounds[world+1] (host-only, no GPU needed). */
+int tcg_shard_bounds(int32_t n, const int64_t* row_ptr, int world, int64_t* bounds);
+/* All-gather callback: `send` holds this rank's `bytes`, `recv` receives
+ * world*bytes in rank order.  Returns 0 on success. */
+typedef int (*tcg_allgather_fn)(void* user, const void* send, size_t bytes, void* recv);
+/* Device transport (production): send/recv are DEVICE pointers, the engine
+ * stream is synchronized before the call and recv must be complete on return
+ * (e.g. torch.distributed.all_gather_into_tensor, NCCL over NVLink/NVSwitch). */
+int tcg_set_shard_device(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user);
+/* Host transport (tests, any backend): send/recv are HOST buffers. */
+int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user);
+
 /* Kernel launches issued by this context since creation (evidence for
  * bench.py's gpu_launches). */
 int64_t tcg_kernel_launches(const tcg_ctx* ctx);

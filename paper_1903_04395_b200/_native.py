@@ -91,7 +91,13 @@ _SIGS = {
     "tcg_set_rejection_limit": (C.c_int, [vp, u64]),
     "tcg_time_colorings": (C.c_int, [vp, u64, C.c_int, C.c_int, vp, P(TcgTiming)]),
     "tcg_kernel_launches": (i64, [vp]),
+    "tcg_shard_bounds": (C.c_int, [i32, vp, C.c_int, vp]),
+    "tcg_set_shard_device": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+    "tcg_set_shard_host": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
 }
+
+# int (*)(void* user, const void* send, size_t bytes, void* recv)
+ALLGATHER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
 
 for _name, (_res, _args) in _SIGS.items():
     _f = getattr(lib, _name)

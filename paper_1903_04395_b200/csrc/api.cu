@@ -320,6 +320,33 @@ int tcg_time_colorings(tcg_ctx* ctx, uint64_t seed, int count, int per_kernel, d
   });
 }
 
+int tcg_shard_bounds(int32_t n, const int64_t* row_ptr, int world, int64_t* bounds) {
+  return guarded([&] {
+    need(row_ptr, "row_ptr");
+    need(bounds, "bounds");
+    const auto b = tcg::shard_bounds(n, row_ptr, world);
+    std::copy(b.begin(), b.end(), bounds);
+  });
+}
+
+int tcg_set_shard_device(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (!fn) throw tcg::invalid_argument("allgather callback is NULL");
+    ctx->eng->set_shard(rank, world, tcg::make_device_transport(fn, user));
+  });
+}
+
+int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (!fn) throw tcg::invalid_argument("allgather callback is NULL");
+    auto t = tcg::make_host_transport(fn, user);
+    tcg::set_host_transport_world(t.get(), world);
+    ctx->eng->set_shard(rank, world, std::move(t));
+  });
+}
+
 int64_t tcg_kernel_launches(const tcg_ctx* ctx) { return ctx ? ctx->eng->launches() : -1; }
 
 }  // extern "C"

@@ -222,6 +222,10 @@ void Engine::release_graph() {
   dfree(d_tile_tot_);
   dfree(d_row_order_);
   dfree(d_counter_);
+  dfree(d_xfull_);
+  dfree(d_colors_pad_);
+  dfree(d_gather_);
+  dfree(d_rows_);
   n_ = -1;
 }
 
@@ -244,11 +248,58 @@ void Engine::release_template() {
 }
 
 // ------------------------------------------------------------------ graph
-void Engine::set_graph(const Csr& g) {
+void Engine::set_shard(int rank, int world, std::unique_ptr<Transport> t) {
+  if (world < 1 || rank < 0 || rank >= world) throw invalid_argument("bad shard rank/world");
+  if (n_ >= 0) throw invalid_argument("tcg_set_shard_* must be called before tcg_set_graph");
+  rank_ = rank;
+  world_ = world;
+  tr_ = std::move(t);
+}
+
+void Engine::set_graph(const Csr& gin) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   release_graph();
+  Csr local;
+  const Csr* gp = &gin;
+  nglob_ = gin.n;
+  if (sharded()) {
+    // this rank's rows, padded to the largest shard; neighbour ids remapped
+    // to padded-global (rank * nmax + local row) so the all-gathered panel is
+    // indexed directly
+    rows_ = shard_bounds(gin.n, gin.row_ptr.data(), world_);
+    int64_t nmax = 1;
+    for (int r = 0; r < world_; ++r) nmax = std::max(nmax, rows_[r + 1] - rows_[r]);
+    nloc_ = static_cast<int32_t>(rows_[rank_ + 1] - rows_[rank_]);
+    local.n = static_cast<int32_t>(nmax);
+    local.row_ptr.assign(static_cast<size_t>(nmax) + 1, 0);
+    const int64_t r0 = rows_[rank_];
+    for (int32_t i = 0; i < nmax; ++i)
+      local.row_ptr[i + 1] = local.row_ptr[i] + (i < nloc_ ? gin.row_ptr[r0 + i + 1] - gin.row_ptr[r0 + i] : 0);
+    local.col.resize(static_cast<size_t>(local.row_ptr[nmax]));
+    const int64_t e0 = gin.row_ptr[r0];
+    for (int64_t e = 0; e < local.row_ptr[nmax]; ++e) {
+      const int32_t u = gin.col[e0 + e];
+      const int r = static_cast<int>(std::upper_bound(rows_.begin(), rows_.end(), static_cast<int64_t>(u)) - rows_.begin()) - 1;
+      local.col[e] = static_cast<int32_t>(r * nmax + (u - rows_[r]));
+    }
+    gp = &local;
+    nsrc_ = static_cast<int32_t>(world_ * nmax);
+    if (static_cast<int64_t>(world_) * nmax > INT32_MAX) throw invalid_argument("sharded graph too large");
+  } else {
+    rows_ = {0, static_cast<int64_t>(gin.n)};
+    nloc_ = gin.n;
+    nsrc_ = gin.n;
+  }
+  const Csr& g = *gp;
   n_ = g.n;
   nnz_ = g.nnz();
+  if (sharded()) {
+    TCG_CUDA(cudaMalloc(&d_xfull_, sizeof(float) * dev::kZ * std::max<int64_t>(nsrc_, 1)));
+    TCG_CUDA(cudaMalloc(&d_colors_pad_, std::max<int64_t>(nsrc_, 1)));
+    // [0, 2048): this rank's totals chunk; [2048, 2048 * (world + 1)): gathered
+    TCG_CUDA(cudaMalloc(&d_gather_, sizeof(double) * 2048 * (world_ + 1)));
+    d_rows_ = dupload(rows_, stream_);
+  }
   TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (n_ + 1)));
   TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
   TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, g.row_ptr.data(), sizeof(int64_t) * (n_ + 1),
@@ -282,7 +333,7 @@ void Engine::set_graph(const Csr& g) {
           bnd[0][v] = g.row_ptr[v];
           bnd[P][v] = g.row_ptr[v + 1];
           for (int s = 1; s < P; ++s) {
-            const int64_t cut = static_cast<int64_t>(n_) * s / P;
+            const int64_t cut = static_cast<int64_t>(nsrc_) * s / P;
             bnd[s][v] = g.row_ptr[v] + (std::lower_bound(b, e, static_cast<int32_t>(cut)) - b);
           }
         }
@@ -405,7 +456,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   std::vector<int> pos(plan_.num_nodes, -1);
   for (size_t i = 0; i < exec_.size(); ++i) pos[exec_[i].id] = static_cast<int>(i);
   for (auto& e : exec_) {
-    if (!lmode || e.p_leaf) continue;
+    if (!lmode || e.p_leaf || sharded()) continue;
     NodeExec& c = exec_[pos[e.p]];
     if (!c.a_leaf || c.root) continue;
     const int32_t Cx = static_cast<int32_t>(B(k, c.size - 1));
@@ -533,8 +584,9 @@ void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
   TCG_CUDA(cudaMemcpyAsync(d_seeds_, seeds, sizeof(uint64_t) * count, cudaMemcpyHostToDevice, stream_));
   const uint64_t k = static_cast<uint64_t>(plan_.k);
   const uint64_t limit = limit_override_ ? limit_override_ : (UINT64_MAX / k) * k;
-  dev::mt_coloring<<<count, dev::kMtThreads, 0, stream_>>>(d_seeds_, n_, plan_.k, limit, UINT64_MAX / k,
-                                                             d_out, n_);
+  // every rank generates the full (global) coloring: the MT stream is serial
+  dev::mt_coloring<<<count, dev::kMtThreads, 0, stream_>>>(d_seeds_, nglob_, plan_.k, limit, UINT64_MAX / k,
+                                                             d_out, nglob_);
   ++launches_;
   TCG_CUDA(cudaGetLastError());
 }
@@ -542,10 +594,71 @@ void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
 void Engine::coloring(uint64_t seed, uint8_t* host_colors) {
   require_ready();
   TCG_CUDA(cudaSetDevice(cfg_.device));
-  ensure_colors(n_);
+  ensure_colors(nglob_);
   gen_colors(&seed, 1, d_colors_);
-  TCG_CUDA(cudaMemcpyAsync(host_colors, d_colors_, n_, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaMemcpyAsync(host_colors, d_colors_, nglob_, cudaMemcpyDeviceToHost, stream_));
   TCG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// colors in padded-global order (the gather ids of a sharded graph)
+void Engine::gather_colors(const uint8_t* d_colors) {
+  const int64_t nmax = n_;
+  dev::pad_colors<<<static_cast<unsigned>((nsrc_ + 255) / 256), 256, 0, stream_>>>(d_colors, d_rows_, nmax, nsrc_,
+                                                                                   d_colors_pad_);
+  ++launches_;
+  TCG_CUDA(cudaGetLastError());
+}
+
+// rooted totals of `count` colorings: all-gather the per-rank fp64 partials
+// and sum them in rank order (deterministic)
+void Engine::finish_shard_totals(double* totals, int count) {
+  if (!sharded()) return;
+  static const bool dbg = std::getenv("TCG_DEBUG_SHARD") != nullptr;
+  if (dbg)
+    std::fprintf(stderr, "[tcg shard %d/%d] rows [%lld,%lld) nmax %d nsrc %d local total[0] %.6e\n", rank_,
+                 world_, static_cast<long long>(rows_[rank_]), static_cast<long long>(rows_[rank_ + 1]), n_,
+                 nsrc_, totals[0]);
+  std::vector<double> all(static_cast<size_t>(count) * world_);
+  for (int i0 = 0; i0 < count; i0 += 2048) {
+    const int c = std::min(2048, count - i0);
+    TCG_CUDA(cudaMemcpyAsync(d_gather_, totals + i0, sizeof(double) * c, cudaMemcpyHostToDevice, stream_));
+    tr_->allgather(d_gather_, sizeof(double) * c, d_gather_ + 2048, stream_);
+    std::vector<double> part(static_cast<size_t>(c) * world_);
+    TCG_CUDA(cudaMemcpyAsync(part.data(), d_gather_ + 2048, sizeof(double) * c * world_, cudaMemcpyDeviceToHost, stream_));
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    if (dbg && i0 == 0)
+      for (int r = 0; r < world_; ++r)
+        std::fprintf(stderr, "[tcg shard %d/%d] gathered[%d] %.6e\n", rank_, world_, r, part[static_cast<size_t>(r) * c]);
+    for (int j = 0; j < c; ++j) {
+      double s = 0.0;
+      for (int r = 0; r < world_; ++r) s += part[static_cast<size_t>(r) * c + j];
+      totals[i0 + j] = s;
+    }
+  }
+}
+
+void Engine::copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind) {
+  TCG_CUDA(cudaMemcpyAsync(dst, src, bytes, kind, stream_));
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+}
+
+// per-vertex fp64 values of the local rows -> global vector on the host
+void Engine::gather_per_vertex(const double* d_local, double* host_global) {
+  double* d_all = nullptr;
+  TCG_CUDA(cudaMalloc(&d_all, sizeof(double) * static_cast<size_t>(n_) * world_));
+  std::vector<double> all(static_cast<size_t>(n_) * world_);
+  try {
+    tr_->allgather(d_local, sizeof(double) * n_, d_all, stream_);
+    TCG_CUDA(cudaMemcpyAsync(all.data(), d_all, all.size() * sizeof(double), cudaMemcpyDeviceToHost, stream_));
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+  } catch (...) {
+    cudaFree(d_all);
+    throw;
+  }
+  cudaFree(d_all);
+  for (int r = 0; r < world_; ++r)
+    for (int64_t j = 0; j < rows_[r + 1] - rows_[r]; ++j)
+      host_global[rows_[r] + j] = all[static_cast<size_t>(r) * n_ + j];
 }
 
 // ------------------------------------------------------------------- SpMM
@@ -601,6 +714,12 @@ void Engine::spmm(const float* X, float* Y, int64_t cols) {
     const int zw = dev::panel_width(cols, p);
     const float* Xp = X + static_cast<int64_t>(p) * n_ * dev::kZ;
     float* Yp = Y + static_cast<int64_t>(p) * n_ * dev::kZ;
+    if (sharded()) {
+      // the gather source is every rank's panel: all-gather it (rank blocks
+      // of nmax rows = the padded-global ids of the local CSR)
+      tr_->allgather(Xp, sizeof(float) * static_cast<size_t>(n_) * zw, d_xfull_, stream_);
+      Xp = d_xfull_;
+    }
     const auto& parts = sched_.at(parts_for_width(zw));
     const int P = static_cast<int>(parts.size());
     for (int s = 0; s < P; ++s) {
@@ -665,10 +784,10 @@ void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
 // P' of a leaf passive child: SpMM against the one-hot color table, read as
 // 1-byte colors (whole rows; the colors array is L2-resident).
 int Engine::parts_for_width(int zw) const {
-  const int64_t need = (static_cast<int64_t>(n_) * zw * 4 + part_bytes_ - 1) / part_bytes_;
+  const int64_t need = (static_cast<int64_t>(nsrc_) * zw * 4 + part_bytes_ - 1) / part_bytes_;
   int P = 1;
   while (P < need && P < (1 << 20)) P *= 2;
-  return std::max(1, std::min<int>(P, std::max(1, n_)));
+  return std::max(1, std::min<int>(P, std::max(1, nsrc_)));
 }
 
 void Engine::hist(const uint8_t* d_colors, float* H) {
@@ -706,8 +825,16 @@ static void launch_root(const NodeExec& e, cudaStream_t s, int32_t n, const floa
 }
 
 // ---------------------------------------------------------------- one DP
-void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc,
+void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_acc,
                     tcg_node_stats* stats) {
+  // d_colors: colors of this context's rows (eMA); d_gcolors: by gather id
+  const uint8_t* d_colors = d_colors_in;
+  const uint8_t* d_gcolors = d_colors_in;
+  if (sharded()) {
+    gather_colors(d_colors_in);
+    d_gcolors = d_colors_pad_;
+    d_colors = d_colors_pad_ + static_cast<int64_t>(rank_) * n_;
+  }
   std::vector<cudaEvent_t> ev;
   auto mark = [&]() {
     cudaEvent_t e;
@@ -724,13 +851,13 @@ void Engine::run_dp(const uint8_t* d_colors, double* d_total, double* d_root_acc
       // color-bucketed CSR for the leaf-pushed SpMMs; yields the histogram too
       TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
       dev::color_bucket<<<148 * 8, 256, 0, stream_>>>(
-          d_row_ptr_, d_col_, d_colors, d_row_order_, n_, plan_.k,
+          d_row_ptr_, d_col_, d_gcolors, d_row_order_, n_, plan_.k,
           reinterpret_cast<int32_t*>(arena_ + colb_off_), reinterpret_cast<int64_t*>(arena_ + boff_off_),
           need_hist_ ? table_ptr(hist_off_) : nullptr, dev::panel_width(plan_.k, 0), d_counter_);
       ++launches_;
       TCG_CUDA(cudaGetLastError());
     } else {
-      hist(d_colors, table_ptr(hist_off_));
+      hist(d_gcolors, table_ptr(hist_off_));
     }
     if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     if (need_hist_) H = table_ptr(hist_off_);
@@ -860,31 +987,34 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
                             tcg_node_stats* stats) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  ensure_colors(n_);
+  ensure_colors(nglob_);
   if (host_colors) {
-    for (int32_t i = 0; i < n_; ++i)
+    for (int32_t i = 0; i < nglob_; ++i)
       if (host_colors[i] >= plan_.k) throw invalid_argument("coloring value out of range [0, k)");
-    TCG_CUDA(cudaMemcpyAsync(d_colors_, host_colors, n_, cudaMemcpyHostToDevice, stream_));
+    TCG_CUDA(cudaMemcpyAsync(d_colors_, host_colors, nglob_, cudaMemcpyHostToDevice, stream_));
   } else {
     gen_colors(&seed, 1, d_colors_);
   }
   run_dp(d_colors_, d_scalars_, nullptr, stats);
   double total = 0;
   TCG_CUDA(cudaMemcpyAsync(&total, d_scalars_, sizeof(double), cudaMemcpyDeviceToHost, stream_));
-  if (per_vertex && n_ > 0) {
+  if (per_vertex && nglob_ > 0) {
     if (exec_.empty()) {
-      for (int32_t i = 0; i < n_; ++i) per_vertex[i] = 1.0;  // k = 1: every vertex once
+      for (int32_t i = 0; i < nglob_; ++i) per_vertex[i] = 1.0;  // k = 1: every vertex once
+    } else if (sharded()) {
+      gather_per_vertex(reinterpret_cast<const double*>(arena_ + exec_.back().out_off), per_vertex);
     } else {
       TCG_CUDA(cudaMemcpyAsync(per_vertex, arena_ + exec_.back().out_off, sizeof(double) * n_,
                                cudaMemcpyDeviceToHost, stream_));
     }
   }
   if (cfg_.flags & TCG_KEEP_TABLES) {
-    last_colors_.resize(n_);
-    TCG_CUDA(cudaMemcpyAsync(last_colors_.data(), d_colors_, n_, cudaMemcpyDeviceToHost, stream_));
+    last_colors_.resize(nglob_);
+    TCG_CUDA(cudaMemcpyAsync(last_colors_.data(), d_colors_, nglob_, cudaMemcpyDeviceToHost, stream_));
   }
   TCG_CUDA(cudaStreamSynchronize(stream_));
-  if (exec_.empty()) total = static_cast<double>(n_);
+  if (exec_.empty()) total = static_cast<double>(nloc_);
+  finish_shard_totals(&total, 1);
   tables_valid_ = true;
   if (!std::isfinite(total)) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
   return total;
@@ -900,8 +1030,8 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
   if (iterations < 1) throw invalid_argument("iterations must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  const int chunk = color_chunk(iterations, n_);
-  ensure_colors(static_cast<int64_t>(chunk) * n_);
+  const int chunk = color_chunk(iterations, nglob_);
+  ensure_colors(static_cast<int64_t>(chunk) * nglob_);
   double* d_totals = nullptr;
   double* d_acc = nullptr;
   TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * iterations));
@@ -916,17 +1046,22 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
       for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
       gen_colors(seeds.data(), c, d_colors_);
       for (int j = 0; j < c; ++j)
-        run_dp(d_colors_ + static_cast<int64_t>(j) * n_, d_totals + i0 + j, d_acc, nullptr);
+        run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, d_acc, nullptr);
     }
     TCG_CUDA(cudaMemcpyAsync(totals, d_totals, sizeof(double) * iterations, cudaMemcpyDeviceToHost, stream_));
     std::vector<double> acc;
     if (d_acc) {
-      acc.resize(n_);
-      TCG_CUDA(cudaMemcpyAsync(acc.data(), d_acc, sizeof(double) * n_, cudaMemcpyDeviceToHost, stream_));
+      acc.resize(nglob_);
+      if (sharded()) {
+        gather_per_vertex(d_acc, acc.data());
+      } else {
+        TCG_CUDA(cudaMemcpyAsync(acc.data(), d_acc, sizeof(double) * n_, cudaMemcpyDeviceToHost, stream_));
+      }
     }
     TCG_CUDA(cudaStreamSynchronize(stream_));
     if (exec_.empty())
-      for (int i = 0; i < iterations; ++i) totals[i] = static_cast<double>(n_);
+      for (int i = 0; i < iterations; ++i) totals[i] = static_cast<double>(nloc_);
+    finish_shard_totals(totals, iterations);
     // estimator.hpp:80-91, same arithmetic order
     double mean = 0.0;
     for (int i = 0; i < iterations; ++i) mean += totals[i];
@@ -939,7 +1074,7 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
                                             static_cast<double>(iterations - 1))) * scale
                          : 0.0;
     if (per_vertex_est) {
-      for (int32_t v = 0; v < n_; ++v)
+      for (int32_t v = 0; v < nglob_; ++v)
         per_vertex_est[v] = (exec_.empty() ? 1.0 : acc[v] / iterations) * scale;
     }
     for (int i = 0; i < iterations; ++i)
@@ -969,8 +1104,8 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
   if (count < 1) throw invalid_argument("count must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
-  const int chunk = color_chunk(count, n_);
-  ensure_colors(static_cast<int64_t>(chunk) * n_);
+  const int chunk = color_chunk(count, nglob_);
+  ensure_colors(static_cast<int64_t>(chunk) * nglob_);
   double* d_totals = nullptr;
   TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * count));
   Prof prof;
@@ -988,7 +1123,7 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
       for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
       gen_colors(seeds.data(), c, d_colors_);
       for (int j = 0; j < c; ++j)
-        run_dp(d_colors_ + static_cast<int64_t>(j) * n_, d_totals + i0 + j, nullptr, nullptr);
+        run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, nullptr, nullptr);
     }
     TCG_CUDA(cudaEventRecord(e1, stream_));
     TCG_CUDA(cudaEventSynchronize(e1));
@@ -1030,9 +1165,10 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
   }
   if (need_hist_) t.hist_alg_bytes = count * (4 * nnz + 8 * (n + 1) + n + 4 * n * plan_.k);
   std::vector<double> h(count);
-  TCG_CUDA(cudaMemcpy(h.data(), d_totals, sizeof(double) * count, cudaMemcpyDeviceToHost));
+  copy_sync(h.data(), d_totals, sizeof(double) * count, cudaMemcpyDeviceToHost);
   dfree(d_totals);
-  if (exec_.empty()) std::fill(h.begin(), h.end(), static_cast<double>(n_));
+  if (exec_.empty()) std::fill(h.begin(), h.end(), static_cast<double>(nloc_));
+  finish_shard_totals(h.data(), count);
   if (totals) std::copy(h.begin(), h.end(), totals);
   for (double x : h)
     if (!std::isfinite(x)) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
@@ -1047,6 +1183,7 @@ static void unpanel(const std::vector<float>& t, int64_t n, int64_t C, double* o
 }
 
 void Engine::node_table(int id, int which, double* out) {
+  if (sharded()) throw invalid_argument("node tables are not inspectable on a sharded context");
   if (!(cfg_.flags & TCG_KEEP_TABLES)) throw invalid_argument("context not created with TCG_KEEP_TABLES");
   if (!tables_valid_) throw invalid_argument("no coloring has been run since the last change");
   if (id < 0 || id >= plan_.num_nodes) throw invalid_argument("node id out of range");
@@ -1059,25 +1196,26 @@ void Engine::node_table(int id, int which, double* out) {
     }
     if (hist_off_ < 0) throw invalid_argument("no neighbour histogram in this plan");
     std::vector<float> h(dev::table_floats(k, n));
-    TCG_CUDA(cudaMemcpy(h.data(), arena_ + hist_off_, h.size() * 4, cudaMemcpyDeviceToHost));
+    copy_sync(h.data(), arena_ + hist_off_, h.size() * 4, cudaMemcpyDeviceToHost);
     unpanel(h, n, k, out);
     return;
   }
   const int64_t C = binom()(plan_.k, plan_.size[id]);
   if (id == plan_.full_node()) {
     if (which != 0) throw invalid_argument("the root has no SpMM output");
-    TCG_CUDA(cudaMemcpy(out, arena_ + table_off_[id], sizeof(double) * n, cudaMemcpyDeviceToHost));
+    copy_sync(out, arena_ + table_off_[id], sizeof(double) * n, cudaMemcpyDeviceToHost);
     return;
   }
   const int64_t off = which == 0 ? table_off_[id] : pprime_off_[id];
   if (off < 0) throw invalid_argument("table not available for this node");
   std::vector<float> t(dev::table_floats(C, n));
-  TCG_CUDA(cudaMemcpy(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost));
+  copy_sync(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost);
   unpanel(t, n, C, out);
 }
 
 void Engine::spmm_host(const float* x, int cols, float* y) {
   if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
+  if (sharded()) throw invalid_argument("tcg_spmm is not available on a sharded context");
   if (cols < 1) throw invalid_argument("cols must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   const int64_t n = n_;
@@ -1091,12 +1229,12 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
     TCG_CUDA(cudaMalloc(&dx, std::max<size_t>(xp.size() * 4, 4)));
     TCG_CUDA(cudaMalloc(&dy, std::max<size_t>(xp.size() * 4, 4)));
     if (max_slots_) TCG_CUDA(cudaMalloc(&dp, static_cast<size_t>(max_slots_) * dev::kZ * 8));
-    TCG_CUDA(cudaMemcpy(dx, xp.data(), xp.size() * 4, cudaMemcpyHostToDevice));
+    copy_sync(dx, xp.data(), xp.size() * 4, cudaMemcpyHostToDevice);
     d_partial_ = dp;
     if (n > 0) spmm(dx, dy, cols);
     d_partial_ = saved_partial;
     TCG_CUDA(cudaStreamSynchronize(stream_));
-    TCG_CUDA(cudaMemcpy(xp.data(), dy, xp.size() * 4, cudaMemcpyDeviceToHost));
+    copy_sync(xp.data(), dy, xp.size() * 4, cudaMemcpyDeviceToHost);
   } catch (...) {
     d_partial_ = saved_partial;
     dfree(dx); dfree(dy); dfree(dp);

@@ -13,6 +13,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -61,8 +62,22 @@ struct PartSchedule {
   int nsplit_rows = 0, nslots = 0;
 };
 
+// All-gather of equal-size per-rank device buffers (SpMM panels, totals).
+struct Transport {
+  virtual ~Transport() = default;
+  virtual void allgather(const void* d_send, size_t bytes, void* d_recv, cudaStream_t s) = 0;
+};
+std::unique_ptr<Transport> make_device_transport(tcg_allgather_fn fn, void* user);
+std::unique_ptr<Transport> make_host_transport(tcg_allgather_fn fn, void* user);
+void set_host_transport_world(Transport* t, int world);
+// contiguous row ranges balanced by deg(v) + avg degree
+std::vector<int64_t> shard_bounds(int32_t n, const int64_t* row_ptr, int world);
+
 class Engine {
  public:
+  void set_shard(int rank, int world, std::unique_ptr<Transport> t);
+  bool sharded() const { return world_ > 1 || static_cast<bool>(tr_); }
+  int32_t n_global() const { return nglob_; }
   explicit Engine(const tcg_config& cfg);
   ~Engine();
 
@@ -116,6 +131,25 @@ class Engine {
   uint64_t limit_override_ = 0;
   int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per SpMM part (measured best on cfg3)
   int64_t persist_max_ = 0;          // > 0: pin each part's gather window in L2 (TCG_L2_PERSIST=MB)
+
+  // sharding: this rank owns global rows [rows_[rank], rows_[rank+1]); tables
+  // have n_ = nmax rows (the largest shard; pad rows have no neighbours);
+  // gather ids are padded-global: rank * nmax + local row
+  int rank_ = 0, world_ = 1;
+  std::unique_ptr<Transport> tr_;
+  std::vector<int64_t> rows_;
+  int32_t nglob_ = -1, nloc_ = -1;
+  int32_t nsrc_ = -1;                // rows of a gather source (world * nmax, or n)
+  int64_t* d_rows_ = nullptr;        // rows_ on device
+  float* d_xfull_ = nullptr;         // all-gathered panel (world * nmax * 32 floats)
+  uint8_t* d_colors_pad_ = nullptr;  // colors in padded-global order
+  double* d_gather_ = nullptr;       // small all-gather scratch (totals)
+  void gather_colors(const uint8_t* d_colors);
+  void finish_shard_totals(double* totals, int count);  // host: sum over ranks in order
+  void gather_per_vertex(const double* d_local, double* host_global);
+  // blocking copy ordered on stream_ (stream_ is non-blocking: a plain
+  // cudaMemcpy on the legacy stream would not wait for it)
+  void copy_sync(void* dst, const void* src, size_t bytes, cudaMemcpyKind kind);
 
   // graph
   int32_t n_ = -1;

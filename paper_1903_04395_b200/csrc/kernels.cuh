@@ -141,6 +141,16 @@ mt_coloring(const uint64_t* __restrict__ seeds, int32_t n, int k, uint64_t limit
   }
 }
 
+// Sharded graphs: colors in padded-global order, pad[r*nmax + j] = color of
+// global vertex rows[r] + j (0 for pad rows, which have no neighbours).
+__global__ void pad_colors(const uint8_t* __restrict__ colors, const int64_t* __restrict__ rows, int64_t nmax,
+                           int64_t nsrc, uint8_t* __restrict__ pad) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= nsrc) return;
+  const int64_t r = i / nmax, j = i % nmax;
+  pad[i] = j < rows[r + 1] - rows[r] ? colors[rows[r] + j] : 0;
+}
+
 // ----------------------------------------------------------------- SpMM
 // One launch = one (panel, part).  A warp owns 32/G segments, one per lane
 // group of G = ZW/4 lanes; each lane carries a float4 of the ZW-wide row.

@@ -353,6 +353,49 @@ class Context:
         self.k = None
         self.graph = None
 
+    # -- vertex sharding; call before set_graph -------------
+    def set_shard_torch(self, rank: int, world: int, group=None) -> None:
+        """Device transport through torch.distributed (NCCL over NVLink/NVSwitch
+        when the process group is NCCL): the engine hands device pointers, the
+        panel is all-gathered with all_gather_into_tensor on zero-copy views."""
+        import torch
+        import torch.distributed as dist
+        dev = torch.device("cuda", torch.cuda.current_device())
+
+        class _Dev:  # __cuda_array_interface__ view of a raw device buffer
+            def __init__(self, ptr, nbytes):
+                self.__cuda_array_interface__ = {"shape": (nbytes,), "typestr": "|u1", "descr": [("", "|u1")],
+                                                 "data": (ptr, False), "strides": None, "version": 2}
+
+        def fn(user, send, nbytes, recv):
+            try:
+                src = torch.as_tensor(_Dev(send, nbytes), device=dev)
+                dst = torch.as_tensor(_Dev(recv, nbytes * world), device=dev)
+                dist.all_gather_into_tensor(dst, src, group=group)
+                torch.cuda.current_stream().synchronize()
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as a status code
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._allgather_cb = N.ALLGATHER_FN(fn)  # keep alive
+        check(lib.tcg_set_shard_device(self._h, rank, world, C.cast(self._allgather_cb, C.c_void_p), None))
+
+    def set_shard_host(self, rank: int, world: int, allgather) -> None:
+        """Host transport: allgather(send: bytes-like np.uint8 array) -> np.uint8
+        array of world*len(send) bytes in rank order (e.g. gloo)."""
+        def fn(user, send, nbytes, recv):
+            try:
+                src = np.ctypeslib.as_array((C.c_uint8 * nbytes).from_address(send)).copy()
+                out = np.asarray(allgather(src), dtype=np.uint8).reshape(-1)
+                dst = np.ctypeslib.as_array((C.c_uint8 * out.size).from_address(recv))
+                dst[:] = out
+                return 0
+            except Exception:  # noqa: BLE001 -- reported as a status code
+                return 1
+        self._allgather_cb = N.ALLGATHER_FN(fn)  # keep alive
+        check(lib.tcg_set_shard_host(self._h, rank, world, C.cast(self._allgather_cb, C.c_void_p), None))
+
     def set_graph(self, g: Graph) -> None:
         check(lib.tcg_set_graph_handle(self._h, g._h))
         self.n, self.graph = g.n, g
@@ -432,6 +475,13 @@ class Context:
         totals = np.zeros(count, np.float64)
         check(lib.tcg_time_colorings(self._h, seed, count, int(per_kernel), _ptr(totals), C.byref(tm)))
         return tm, totals
+
+
+def shard_bounds(g: Graph, world: int) -> np.ndarray:
+    """Row bounds of `world` vertex shards (balanced by degree + average degree)."""
+    out = np.zeros(world + 1, np.int64)
+    check(lib.tcg_shard_bounds(g.n, _ptr(np.ascontiguousarray(g.csc_col_ptr)), world, _ptr(out)))
+    return out
 
 
 # Contexts behind the reference-style free functions, keyed by (graph, template, cfg).
