@@ -102,6 +102,11 @@ int tcg_color_set_of(int k, int64_t index, int h, int32_t* colors);
 int64_t tcg_estimate_bytes(const tcg_plan* plan, int64_t n);
 /* estimator.hpp:29-33 */
 double tcg_colorful_probability(int k);
+/* Rooted-color compression layout of a size-s sub-template table (B200
+ * design, no reference counterpart): info[4] = {zw, groups,
+ * full_cols, store_cols}; optional perm[full_cols] (full column -> P' storage
+ * column) and slot_col[k * groups * zw] (compressed slot -> full column or -1). */
+int tcg_rooted_layout(int k, int s, int32_t* info, int32_t* perm, int32_t* slot_col);
 
 /* ------------------------------------------------------------------------
  * Device engine (one GPU).  == the vectorized engine of engines.hpp:224-268.

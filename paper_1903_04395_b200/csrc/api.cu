@@ -202,6 +202,19 @@ int64_t tcg_estimate_bytes(const tcg_plan* plan, int64_t n) {
 
 double tcg_colorful_probability(int k) { return tcg::colorful_probability(k); }
 
+int tcg_rooted_layout(int k, int s, int32_t* info, int32_t* perm, int32_t* slot_col) {
+  return guarded([&] {
+    need(info, "info");
+    const tcg::RootedLayout L = tcg::build_rooted_layout(k, s);
+    info[0] = L.zw;
+    info[1] = L.groups;
+    info[2] = L.full_cols;
+    info[3] = L.store_cols;
+    if (perm) std::copy(L.perm.begin(), L.perm.end(), perm);
+    if (slot_col) std::copy(L.slot_col.begin(), L.slot_col.end(), slot_col);
+  });
+}
+
 // ----------------------------------------------------------------- engine
 int tcg_create(const tcg_config* cfg, tcg_ctx** out) {
   return guarded([&] {

@@ -226,6 +226,7 @@ void Engine::release_graph() {
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
+  dfree(d_cuts_);
   n_ = -1;
 }
 
@@ -237,6 +238,9 @@ void Engine::release_template() {
     dfree(e.d_groups);
     dfree(e.d_blocks);
     dfree(e.d_ins);
+    dfree(e.d_slot_acc);
+    dfree(e.d_slot_col);
+    dfree(e.d_pinv);
   }
   exec_.clear();
   dfree(arena_);
@@ -352,6 +356,8 @@ void Engine::set_graph(const Csr& gin) {
       return g.row_ptr[x + 1] - g.row_ptr[x] > g.row_ptr[y + 1] - g.row_ptr[y];
     });
     d_row_order_ = dupload(order, stream_);
+    nlong_ = 0;
+    while (nlong_ < n_ && g.row_ptr[order[nlong_] + 1] - g.row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
     TCG_CUDA(cudaMalloc(&d_counter_, 64));
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
@@ -374,6 +380,14 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   need_hist_ = false;
   int max_smem = 0;
   TCG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg_.device));
+  static const int lmode = [] {
+    const char* s = std::getenv("TCG_LSPMM");
+    return s ? std::atoi(s) : 0;
+  }();
+  static const int rooted_mode = [] {
+    const char* s = std::getenv("TCG_ROOTED");
+    return s ? std::atoi(s) : 1;
+  }() && !lmode;
   for (int id : plan_.dp_order) {
     if (plan_.is_leaf(id)) continue;
     NodeExec e;
@@ -394,8 +408,34 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     e.pairs = st.pairs_per_parent;
     std::vector<int2> pr(st.active_index.size());
     for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(st.active_index[i], st.passive_index[i]);
+    // Rooted-color compressed SpMM for every internal passive child (default;
+    // TCG_ROOTED=0 restores the full-table panel SpMM): P' is then stored
+    // group-major, so the eMA's passive indices are remapped to storage columns.
+    e.Cps = e.Cp;
+    if (rooted_mode && !e.p_leaf) {
+      const RootedLayout rl = build_rooted_layout(k, e.sp);
+      int fpad_max = 0;
+      for (int g = 0; g < rl.groups; ++g)
+        fpad_max = std::max(fpad_max, (g + 1 < rl.groups ? rl.fbase[g + 1] : rl.store_cols) - rl.fbase[g]);
+      const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * fpad_max * 4;
+      // (rooted_compress stages at least one full row of M_p in smem)
+      if (smem <= static_cast<size_t>(max_smem) - 4096 && 4 * dev::table_floats(e.Cp, 1) <= max_smem - 4096) {
+        e.rooted = true;
+        e.Cps = rl.store_cols;
+        e.rl_zw = rl.zw;
+        e.rl_groups = rl.groups;
+        e.rl_fbase = rl.fbase;
+        e.rl_fsize = rl.fsize;
+        e.rl_perm = rl.perm;
+        e.rooted_smem = smem;
+        e.d_slot_acc = dupload(rl.slot_acc, stream_);
+        e.d_slot_col = dupload(rl.slot_col, stream_);
+        e.d_pinv = dupload(rl.inv, stream_);
+        for (auto& q : pr) q.y = rl.perm[q.y];
+      }
+    }
     e.d_split = dupload(pr, stream_);
-    if (!e.a_leaf && !e.root && e.Ca < 65536 && e.Cp < 65536) {
+    if (!e.a_leaf && !e.root && e.Ca < 65536 && e.Cps < 65536) {
       std::vector<uint32_t> pk(pr.size());
       for (size_t i = 0; i < pr.size(); ++i)
         pk[i] = static_cast<uint32_t>(pr[i].x) | (static_cast<uint32_t>(pr[i].y) << 16);
@@ -410,7 +450,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
               pr[static_cast<size_t>(s) * e.pairs + p2].y;
       e.d_drop = dupload(drop, stream_);
     }
-    const int64_t staged = static_cast<int64_t>((e.a_leaf ? 0 : e.Ca) + e.Cp) * (dev::kTileV + 1) * 4;
+    const int64_t staged = static_cast<int64_t>((e.a_leaf ? 0 : e.Ca) + e.Cps) * (dev::kTileV + 1) * 4;
     e.ema_staged = staged <= max_smem - 4096;
     e.ema_smem = e.ema_staged ? static_cast<size_t>(staged) : 0;
     static const int blocked_mode = [] {
@@ -421,7 +461,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     // which the 8-column chunks of ema_node coalesce better
     // vertex-per-CTA when a 32-vertex tile does not fit: one vertex's rows
     auto row_floats = [](int64_t C) { return C <= 0 ? 0 : dev::table_floats(C, 1); };
-    const int64_t vsm = 4 * (((e.a_leaf ? 0 : row_floats(e.Ca)) + 3) / 4 * 4 + row_floats(e.Cp));
+    const int64_t vsm = 4 * (((e.a_leaf ? 0 : row_floats(e.Ca)) + 3) / 4 * 4 + row_floats(e.Cps));
     if (!e.ema_staged && vsm <= max_smem - 4096 && (e.a_leaf || e.root || k >= dev::kH1)) {
       e.vtx = true;
       e.vtx_smem = static_cast<size_t>(vsm);
@@ -445,10 +485,6 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   // cost more than the gathered columns save (measured cfg3: node 2 SpMM
   // 26.6 -> 70 ms), so the direct panel SpMM is the default.
   need_bucket_ = false;
-  static const int lmode = [] {
-    const char* s = std::getenv("TCG_LSPMM");
-    return s ? std::atoi(s) : 0;
-  }();
   static const int64_t q_budget = [] {
     const char* s = std::getenv("TCG_Q_GB");
     return (s ? std::atoll(s) : 12ll) << 30;
@@ -501,8 +537,40 @@ void Engine::plan_arena() {
   std::vector<int64_t> child_pp(plan_.num_nodes, -1);  // P' kept alive for an LSpMM parent
   int64_t lslots = 0;
   const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
+  // rooted SpMMs: one part count for all of them (the widest compressed
+  // panel's), so the per-coloring row bucketing matches every schedule
+  need_rooted_ = false;
+  rooted_parts_ = 1;
+  for (auto& e : exec_)
+    if (e.rooted) {
+      need_rooted_ = true;
+      rooted_parts_ = std::max(rooted_parts_, parts_for_width(e.rl_zw));
+    }
+  dfree(d_cuts_);
+  rcol_off_ = -1;
+  int64_t rooted_partial = 0;
+  if (need_rooted_) {
+    if (nsrc_ >= (1 << dev::kPackShift))
+      throw invalid_argument("graph too large for the rooted-compressed SpMM (ids >= 2^27); set TCG_ROOTED=0");
+    rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
+    std::vector<int32_t> cuts(static_cast<size_t>(rooted_parts_) + 1);
+    for (int q = 0; q <= rooted_parts_; ++q) cuts[q] = static_cast<int32_t>(static_cast<int64_t>(nsrc_) * q / rooted_parts_);
+    d_cuts_ = dupload(cuts, stream_);
+    int slots = 0;
+    for (auto& ps : sched_.at(rooted_parts_)) slots = std::max(slots, ps.nslots);
+    for (auto& e : exec_)
+      if (e.rooted) rooted_partial = std::max<int64_t>(rooted_partial, static_cast<int64_t>(slots) * static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / e.rl_zw))));
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+  }
   for (auto& e : exec_) {
-    if (!e.p_leaf) {
+    if (!e.p_leaf && e.rooted) {
+      // compress M_p (alive), drop it, then P' while the compressed table lives
+      e.ct_off = ap.alloc(table_bytes(static_cast<int64_t>(e.rl_groups) * e.rl_zw));
+      if (!keep) ap.free(table_off_[e.p]);
+      e.pp_off = ap.alloc(table_bytes(e.Cps));
+      pprime_off_[e.p] = e.pp_off;
+      if (!keep) ap.free(e.ct_off);
+    } else if (!e.p_leaf) {
       e.pp_off = ap.alloc(table_bytes(e.Cp));
       pprime_off_[e.p] = e.pp_off;
       if (e.lspmm) {
@@ -533,7 +601,8 @@ void Engine::plan_arena() {
     }
   }
   arena_bytes_ = ap.peak;
-  partial_bytes_ = std::max<int64_t>(static_cast<int64_t>(max_slots_), lslots) * dev::kZ * 8;
+  partial_bytes_ = std::max<int64_t>(std::max<int64_t>(static_cast<int64_t>(max_slots_), lslots) * dev::kZ * 8,
+                                     rooted_partial * 8);
 }
 
 int64_t Engine::required_bytes() const {
@@ -781,6 +850,61 @@ void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
   TCG_CUDA(cudaGetLastError());
 }
 
+// Rooted-color compressed SpMM (host.hpp RootedLayout, kernels.cuh): compress
+// M_p to its color-rooted slots, then one pass per (group, part) over the
+// (part, color)-sorted rows, each producing the group's P' columns.
+void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors) {
+  const int zw = e.rl_zw, G = e.rl_groups;
+  float* X = table_ptr(e.ct_off);
+  {
+    const int rf = static_cast<int>(dev::table_floats(e.Cp, 1));
+    const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (96 << 10) / (4 * rf))));
+    const size_t smem = static_cast<size_t>(vpb) * rf * 4;
+    TCG_CUDA(cudaFuncSetAttribute(dev::rooted_compress, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dev::rooted_compress<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
+        M, e.Cp, d_colors, e.d_slot_col, G, zw, n_, vpb, X);
+    ++launches_;
+  }
+  const auto& parts = sched_.at(rooted_parts_);
+  const uint32_t* colb = reinterpret_cast<const uint32_t*>(arena_ + rcol_off_);
+  const void* kern = zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32>)
+                   : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16>)
+                              : reinterpret_cast<const void*>(dev::spmm_rooted<8>);
+  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rooted_smem)));
+  const int spw = 128 / zw;
+  for (int g = 0; g < G; ++g) {
+    const float* Xg = X + static_cast<int64_t>(g) * n_ * dev::kZ;
+    if (sharded()) {
+      tr_->allgather(Xg, sizeof(float) * static_cast<size_t>(n_) * zw, d_xfull_, stream_);
+      Xg = d_xfull_;
+    }
+    const int fbase = e.rl_fbase[g];
+    const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - fbase;
+    const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * fpad * 4;
+    const int16_t* sl = e.d_slot_acc + static_cast<int64_t>(g) * zw;
+    for (size_t q = 0; q < parts.size(); ++q) {
+      const PartSchedule& ps = parts[q];
+      const int64_t ntasks = ps.nseg_padded / spw;
+      const unsigned blocks = static_cast<unsigned>((ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps);
+      const int first = q == 0 ? 1 : 0;
+      if (zw == 32)
+        dev::spmm_rooted<32><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
+      else if (zw == 16)
+        dev::spmm_rooted<16><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
+      else
+        dev::spmm_rooted<8><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
+      ++launches_;
+      if (ps.nsplit_rows) {
+        const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * fpad;
+        dev::rooted_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
+            ps.d_split_rows, ps.d_slot_begin, ps.nsplit_rows, d_partial_, fbase, fpad, e.Cps, n_, Pp, first);
+        ++launches_;
+      }
+    }
+  }
+  TCG_CUDA(cudaGetLastError());
+}
+
 // P' of a leaf passive child: SpMM against the one-hot color table, read as
 // 1-byte colors (whole rows; the colors array is L2-resident).
 int Engine::parts_for_width(int zw) const {
@@ -810,7 +934,7 @@ static void launch_node(const NodeExec& e, int k, cudaStream_t s, int32_t n, con
   // so many tiles co-reside per SM and staging overlaps compute across CTAs
   const int warps = std::max(2, std::min(dev::kEmaWarps, (e.Cs + 7) / 8));
   kern<<<tiles, warps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.d_packed, e.d_drop, k,
-                                             e.pairs, e.Ca, e.Cp, e.Cs, n, out);
+                                             e.pairs, e.Ca, e.Cps, e.Cs, n, out);
 }
 
 template <bool AL, bool ST>
@@ -820,7 +944,7 @@ static void launch_root(const NodeExec& e, cudaStream_t s, int32_t n, const floa
   auto kern = dev::ema_root<AL, ST>;
   TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
   const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
-  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca, e.Cp,
+  kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca, e.Cps,
                                                       n, rout, racc, tile_tot);
 }
 
@@ -862,6 +986,29 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     if (need_hist_) H = table_ptr(hist_off_);
   }
+  if (need_rooted_ && n_ > 0) {
+    // (part, color)-sorted packed rows for the rooted SpMMs of this coloring
+    size_t b0 = 0;
+    if (prof_) { b0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+    TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
+    const size_t nkeys = static_cast<size_t>(rooted_parts_) * plan_.k;
+    const size_t smem = sizeof(int) * 8 * nkeys, lsmem = sizeof(int) * 9 * nkeys;
+    if (smem > 48 * 1024)
+      TCG_CUDA(cudaFuncSetAttribute(dev::bucket_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    if (lsmem > 48 * 1024)
+      TCG_CUDA(cudaFuncSetAttribute(dev::bucket_long, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+    uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
+    if (nlong_ > 0) {
+      dev::bucket_long<<<static_cast<unsigned>(nlong_), 256, lsmem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_,
+                                                                                plan_.k, d_cuts_, rooted_parts_, rc);
+      ++launches_;
+    }
+    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, n_, plan_.k,
+                                                     d_cuts_, rooted_parts_, rc, d_counter_);
+    ++launches_;
+    TCG_CUDA(cudaGetLastError());
+    if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+  }
   struct Marks { size_t t0, t1, t2; };
   std::vector<Marks> marks;
   for (auto& e : exec_) {
@@ -876,6 +1023,8 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
         for (auto& x : exec_)
           if (x.id == e.p) c = &x;
         lspmm(e, c->p_leaf ? H : table_ptr(c->pp_off), table_ptr(e.pp_off));
+      } else if (e.rooted) {
+        rooted_spmm(e, table_ptr(table_off_[e.p]), table_ptr(e.pp_off), d_colors);
       } else {
         spmm(table_ptr(table_off_[e.p]), table_ptr(e.pp_off), e.Cp);
       }
@@ -900,17 +1049,18 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
         if (e.root) {
           double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
           smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_root));
-          dev::ema_vtx_root<<<vgrid, 256, e.vtx_smem, stream_>>>(A, P, d_colors, e.d_split, e.pairs, e.Ca, e.Cp,
+          dev::ema_vtx_root<<<vgrid, 256, e.vtx_smem, stream_>>>(A, P, d_colors, e.d_split, e.pairs, e.Ca, e.Cps,
                                                                    e.a_leaf ? 1 : 0, n_, rout, d_root_acc);
         } else if (e.a_leaf) {
           smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_aleaf));
-          dev::ema_vtx_aleaf<<<vgrid, 256, e.vtx_smem, stream_>>>(P, d_colors, e.d_drop, plan_.k, e.Cp, e.Cs, n_,
+          dev::ema_vtx_aleaf<<<vgrid, 256, e.vtx_smem, stream_>>>(P, d_colors, e.d_drop, plan_.k, e.Cps, e.Cs, n_,
                                                                     table_ptr(e.out_off));
         } else {
           smem_attr(reinterpret_cast<const void*>(dev::ema_vtx_blocked));
           dev::ema_vtx_blocked<<<vgrid, 256, e.vtx_smem, stream_>>>(
               A, P, static_cast<const dev::GroupDesc*>(e.d_groups), e.ngroups,
-              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, table_ptr(e.out_off));
+              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, table_ptr(e.out_off),
+              e.Cps, e.rooted ? e.d_pinv : nullptr);
         }
       } else if (e.root) {
         double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
@@ -932,7 +1082,8 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
                                         static_cast<int>(e.ema_smem)));
           kern<<<static_cast<unsigned>((n_ + dev::kTileV - 1) / dev::kTileV), 256, e.ema_smem, stream_>>>(
               A, P, static_cast<const dev::GroupDesc*>(e.d_groups), e.ngroups,
-              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, out);
+              static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, out, e.Cps,
+              e.rooted ? e.d_pinv : nullptr);
         } else {
           if (e.ema_staged) launch_node<false, true>(e, plan_.k, stream_, n_, A, P, d_colors, out);
           else launch_node<false, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);
@@ -1155,7 +1306,8 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
     if (!e.p_leaf) {
       t.spmm_launches += count;
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
-      const int32_t gc = e.lspmm ? e.Cx : e.Cp;  // columns actually gathered per neighbour
+      // columns actually gathered per neighbour
+      const int32_t gc = e.lspmm ? e.Cx : e.rooted ? e.rl_groups * e.rl_zw : e.Cp;
       t.spmm_gathered_bytes += count * nnz * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
                                                      dev::last_panel_width(gc));
     }
@@ -1208,6 +1360,16 @@ void Engine::node_table(int id, int which, double* out) {
   }
   const int64_t off = which == 0 ? table_off_[id] : pprime_off_[id];
   if (off < 0) throw invalid_argument("table not available for this node");
+  if (which == 1) {
+    for (const auto& e : exec_)
+      if (e.p == id && e.rooted) {  // group-major P': storage column perm[S]
+        std::vector<float> t(dev::table_floats(e.Cps, n));
+        copy_sync(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost);
+        for (int64_t v = 0; v < n; ++v)
+          for (int64_t c = 0; c < C; ++c) out[v * C + c] = t[dev::panel_offset(e.Cps, n, v, e.rl_perm[c])];
+        return;
+      }
+  }
   std::vector<float> t(dev::table_floats(C, n));
   copy_sync(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost);
   unpanel(t, n, C, out);

@@ -50,6 +50,18 @@ struct NodeExec {
   bool ema_staged = true;
   bool vtx = false;              // vertex-per-CTA eMA (32-vertex tile does not fit smem)
   size_t vtx_smem = 0;
+  // rooted-color compressed SpMM (host.hpp RootedLayout): the passive child's
+  // table is compressed to `rl_groups` panels of rl_zw slots, P' is stored
+  // group-major with Cps columns (== Cp when not rooted)
+  bool rooted = false;
+  int32_t Cps = 0;
+  int rl_zw = 0, rl_groups = 0;
+  std::vector<int32_t> rl_fbase, rl_fsize, rl_perm;
+  int16_t* d_slot_acc = nullptr;  // [k][groups * zw]
+  int32_t* d_slot_col = nullptr;  // [k][groups * zw]
+  int32_t* d_pinv = nullptr;      // [Cps] storage column -> combinadic column (blocked eMA staging)
+  int64_t ct_off = -1;            // arena offset of the compressed passive table
+  size_t rooted_smem = 0;         // spmm_rooted dynamic smem
 };
 
 // SpMM work schedule for one vertex-range part of the gather source.
@@ -162,6 +174,7 @@ class Engine {
   int parts_for_width(int zw) const;
   int max_slots_ = 0;
   int32_t* d_row_order_ = nullptr;   // rows by degree, descending (color_bucket)
+  int32_t nlong_ = 0;                // rows of degree > dev::kBucketLong (a prefix of row order)
   int* d_counter_ = nullptr;
 
   // template / plan
@@ -177,6 +190,11 @@ class Engine {
   int64_t hist_off_ = -1;
   bool need_bucket_ = false;         // some node uses the leaf-pushed SpMM
   int64_t colb_off_ = -1, boff_off_ = -1;
+  bool need_rooted_ = false;         // some node uses the rooted-compressed SpMM
+  int rooted_parts_ = 1;             // part count of every rooted SpMM (and of the row bucketing)
+  int64_t rcol_off_ = -1;            // per-coloring (part, color)-sorted packed CSR
+  int32_t* d_cuts_ = nullptr;        // rooted_parts_ + 1 gather-id part boundaries
+  void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors);
   std::vector<int64_t> table_off_;   // per node id: arena offset of its table (internal)
   std::vector<int64_t> pprime_off_;  // per node id: offset of P' computed from it
   char* arena_ = nullptr;

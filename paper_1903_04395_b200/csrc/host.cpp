@@ -307,6 +307,165 @@ uint32_t set_mask(int k, int64_t index, int h) {
   return m;
 }
 
+// ------------------------------------------------- rooted-color compression
+// Group assignment: start from g(S) = (sum of the colors of S) mod m, which is
+// already balanced for most (k, s) (every color's sets spread evenly over the
+// residues), then repair overfull (group, color) pairs by min-conflict moves.
+// m starts at the lower bound ceil(C(k-1,s-1) / zw); a first-fit pass is the
+// always-feasible fallback.  Deterministic (fixed-seed generator).
+RootedLayout build_rooted_layout(int k, int s) {
+  if (k < 1 || k > kMaxK || s < 1 || s > k) throw invalid_argument("rooted layout: bad (k, s)");
+  const Binom& B = binom();
+  RootedLayout L;
+  L.k = k;
+  L.s = s;
+  const int64_t C = B(k, s), W = B(k - 1, s - 1);
+  L.full_cols = static_cast<int32_t>(C);
+  L.zw = W <= 8 ? 8 : (W <= 16 ? 16 : 32);
+  const int zw = L.zw;
+  std::vector<uint32_t> mask(static_cast<size_t>(C));
+  std::vector<int> csum(static_cast<size_t>(C));
+  int cs[kMaxK];
+  for (int64_t x = 0; x < C; ++x) {
+    set_of(k, x, s, cs);
+    uint32_t m = 0;
+    int sum = 0;
+    for (int j = 0; j < s; ++j) { m |= 1u << cs[j]; sum += cs[j]; }
+    mask[x] = m;
+    csum[x] = sum;
+  }
+  std::vector<int> g(static_cast<size_t>(C));
+  uint64_t rs = 0x9E3779B97F4A7C15ull;
+  auto rnd = [&rs](uint64_t bound) {
+    rs += 0x9E3779B97F4A7C15ull;
+    uint64_t z = rs;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return (z ^ (z >> 31)) % bound;
+  };
+  auto try_groups = [&](int m) -> bool {
+    std::vector<int> cnt(static_cast<size_t>(m) * k, 0);
+    std::vector<std::vector<int64_t>> members(static_cast<size_t>(m));
+    std::vector<int64_t> where(static_cast<size_t>(C));
+    for (int64_t x = 0; x < C; ++x) {
+      const int gi = csum[x] % m;
+      g[x] = gi;
+      where[x] = static_cast<int64_t>(members[gi].size());
+      members[gi].push_back(x);
+      for (uint32_t b = mask[x]; b; b &= b - 1) ++cnt[static_cast<size_t>(gi) * k + __builtin_ctz(b)];
+    }
+    // overfull (group, color) pairs, kept as an indexable set
+    std::vector<int> over, opos(static_cast<size_t>(m) * k, -1);
+    auto sync = [&](int gi, int c) {
+      const size_t id = static_cast<size_t>(gi) * k + c;
+      const bool bad = cnt[id] > zw;
+      if (bad && opos[id] < 0) { opos[id] = static_cast<int>(over.size()); over.push_back(static_cast<int>(id)); }
+      if (!bad && opos[id] >= 0) {
+        const int last = over.back();
+        over[opos[id]] = last;
+        opos[last] = opos[id];
+        over.pop_back();
+        opos[id] = -1;
+      }
+    };
+    for (int gi = 0; gi < m; ++gi)
+      for (int c = 0; c < k; ++c) sync(gi, c);
+    const int64_t maxit = 4 * C + 20000;
+    for (int64_t it = 0; it < maxit && !over.empty(); ++it) {
+      const int id = over[rnd(over.size())];
+      const int gi = id / k, c = id % k;
+      auto& mem = members[gi];
+      int64_t x = -1;
+      for (int tries = 0; tries < 64 * k && x < 0; ++tries) {
+        const int64_t y = mem[rnd(mem.size())];
+        if (mask[y] >> c & 1u) x = y;
+      }
+      if (x < 0) continue;
+      // best of (at most) 48 candidate groups
+      int best = -1, bd = 1 << 30;
+      const int ncand = std::min(m - 1, 48);
+      for (int q = 0; q < ncand; ++q) {
+        const int b = m - 1 <= 48 ? (q < gi ? q : q + 1) : static_cast<int>(rnd(m));
+        if (b == gi) continue;
+        int d = 0;
+        for (uint32_t bb = mask[x]; bb; bb &= bb - 1) d += cnt[static_cast<size_t>(b) * k + __builtin_ctz(bb)] >= zw;
+        if (d < bd || (d == bd && (rnd(4) == 0))) { bd = d; best = b; }
+      }
+      if (best < 0) return false;
+      // move x: gi -> best
+      const int64_t last = mem.back();
+      mem[where[x]] = last;
+      where[last] = where[x];
+      mem.pop_back();
+      where[x] = static_cast<int64_t>(members[best].size());
+      members[best].push_back(x);
+      g[x] = best;
+      for (uint32_t bb = mask[x]; bb; bb &= bb - 1) {
+        const int cc = __builtin_ctz(bb);
+        --cnt[static_cast<size_t>(gi) * k + cc];
+        ++cnt[static_cast<size_t>(best) * k + cc];
+        sync(gi, cc);
+        sync(best, cc);
+      }
+    }
+    return over.empty();
+  };
+  const int lb = static_cast<int>((W + zw - 1) / zw);
+  int m = -1;
+  for (int step = 0; step < 6 && m < 0; ++step) {
+    const int t = lb + (step == 0 ? 0 : (lb >> (6 - step)) + step);  // lb, +1/32, +1/16, ... +1/2
+    if (try_groups(t)) m = t;
+  }
+  if (m < 0) {  // first fit in column order: always feasible
+    std::vector<std::vector<int>> cnt;
+    for (int64_t x = 0; x < C; ++x) {
+      int gi = 0;
+      for (;; ++gi) {
+        if (gi == static_cast<int>(cnt.size())) cnt.emplace_back(k, 0);
+        bool ok = true;
+        for (uint32_t b = mask[x]; b && ok; b &= b - 1) ok = cnt[gi][__builtin_ctz(b)] < zw;
+        if (ok) break;
+      }
+      g[x] = gi;
+      for (uint32_t b = mask[x]; b; b &= b - 1) ++cnt[gi][__builtin_ctz(b)];
+    }
+    m = static_cast<int>(cnt.size());
+  }
+  // drop empty groups; members in ascending full-column order
+  std::vector<std::vector<int64_t>> mem(static_cast<size_t>(m));
+  for (int64_t x = 0; x < C; ++x) mem[g[x]].push_back(x);
+  mem.erase(std::remove_if(mem.begin(), mem.end(), [](const std::vector<int64_t>& v) { return v.empty(); }),
+            mem.end());
+  L.groups = static_cast<int>(mem.size());
+  L.perm.assign(static_cast<size_t>(C), -1);
+  int32_t base = 0;
+  for (int gi = 0; gi < L.groups; ++gi) {
+    L.fbase.push_back(base);
+    L.fsize.push_back(static_cast<int32_t>(mem[gi].size()));
+    for (size_t a = 0; a < mem[gi].size(); ++a) L.perm[mem[gi][a]] = base + static_cast<int32_t>(a);
+    base += (static_cast<int32_t>(mem[gi].size()) + 7) / 8 * 8;
+  }
+  L.store_cols = base;
+  L.inv.assign(static_cast<size_t>(base), -1);
+  for (int64_t x = 0; x < C; ++x) L.inv[L.perm[x]] = static_cast<int32_t>(x);
+  const size_t slots = static_cast<size_t>(L.groups) * zw;
+  L.slot_acc.assign(slots * k, -1);
+  L.slot_col.assign(slots * k, -1);
+  for (int c = 0; c < k; ++c)
+    for (int gi = 0; gi < L.groups; ++gi) {
+      int t = 0;
+      for (size_t a = 0; a < mem[gi].size(); ++a) {
+        const int64_t x = mem[gi][a];
+        if (!(mask[x] >> c & 1u)) continue;
+        if (t >= zw) throw logic_error("rooted layout: group over capacity");
+        const size_t i = static_cast<size_t>(c) * slots + static_cast<size_t>(gi) * zw + t++;
+        L.slot_acc[i] = static_cast<int16_t>(a);
+        L.slot_col[i] = static_cast<int32_t>(x);
+      }
+    }
+  return L;
+}
+
 SplitTable build_split_table(int k, int parent_size, int active_size) {
   const int passive_size = parent_size - active_size;
   if (active_size < 1 || passive_size < 1)

@@ -95,6 +95,34 @@ struct SplitTable {  // color_index.hpp:91-101
 };
 SplitTable build_split_table(int k, int parent_size, int active_size);  // :103-180
 
+// ------------------------------------------------- rooted-color compression
+// A sub-template table M_p[u,S] is zero unless S contains u's own color (the
+// root of T_p is mapped to u), so only C(k-1,s-1) of its C(k,s) columns can
+// be nonzero: a fraction s/k.  The compressed table keeps, for every vertex,
+// just those columns, arranged so the SpMM over it can still accumulate into
+// whole output columns:
+//   * the C(k,s) sets are partitioned into `groups` groups F_g such that, for
+//     every color c, at most `zw` sets of F_g contain c;
+//   * compressed panel g of vertex u (zw floats) holds M_p[u,S] for the sets
+//     S in F_g that contain color(u), in slot order;
+//   * the SpMM output P' is stored GROUP-MAJOR: group g owns the storage
+//     columns [fbase[g], fbase[g] + fsize[g]), fbase 8-aligned (32 B sectors),
+//     so one pass over compressed panel g produces P' columns F_g complete.
+// (B200 design, no reference counterpart: the reference gathers every column.)
+struct RootedLayout {
+  int k = 0, s = 0;
+  int zw = 0;                      // compressed panel width: 8, 16 or 32 floats
+  int groups = 0;
+  int32_t full_cols = 0;           // C(k,s)
+  int32_t store_cols = 0;          // P' storage columns (sum of 8-aligned groups)
+  std::vector<int32_t> fsize, fbase;
+  std::vector<int32_t> perm;       // full (combinadic) column -> storage column
+  std::vector<int32_t> inv;        // storage column -> full column, or -1 (padding)
+  std::vector<int16_t> slot_acc;   // [c * groups * zw + g * zw + t] -> index in F_g, or -1
+  std::vector<int32_t> slot_col;   // same slots -> full column, or -1
+};
+RootedLayout build_rooted_layout(int k, int s);
+
 // ----------------------------------------------------------------- template
 struct Plan {  // templates.hpp:143-170
   int k = 0, root = 0, num_nodes = 0;

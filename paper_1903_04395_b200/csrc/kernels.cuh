@@ -415,6 +415,332 @@ lspmm_combine(const float* __restrict__ Q, int64_t q_stride, int c0, int nc,
   }
 }
 
+// ------------------------------------------ rooted-color compressed SpMM
+// (host.hpp RootedLayout).  Per coloring, every CSR row is re-ordered by
+// (part, neighbour color) and each entry packed as u | color << 27, so the
+// SpMM walks a row's neighbours in runs of one color: within a run the
+// compressed panel slots mean the same parent columns, so the run is summed
+// in registers and scattered into the task's F_g accumulators (smem, fp64)
+// once per run.
+constexpr uint32_t kPackSentinel = 0xFFFFFFFFu;  // color 31: never a real color (k <= 20)
+constexpr int kPackShift = 27;
+constexpr uint32_t kPackMask = (1u << kPackShift) - 1u;
+
+// Key of a neighbour: part(u) * k + color(u); `cuts` holds the nparts + 1
+// gather-id boundaries of the parts (engine.cu parts_for_width).
+__device__ __forceinline__ int bucket_key(int u, const uint8_t* __restrict__ colors,
+                                          const int32_t* __restrict__ cuts, int nparts, int k) {
+  int p = 0;
+  while (p + 1 < nparts && u >= __ldg(cuts + p + 1)) ++p;
+  return p * k + colors[u];
+}
+
+// exclusive scan of cnt[0, nkeys) by one warp, in place
+__device__ __forceinline__ void warp_exclusive_scan(int* cnt, int nkeys, int lane) {
+  int run = 0;
+  for (int i0 = 0; i0 < nkeys; i0 += 32) {
+    const int x = i0 + lane < nkeys ? cnt[i0 + lane] : 0;
+    int incl = x;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    if (i0 + lane < nkeys) cnt[i0 + lane] = run + incl - x;
+    run += __shfl_sync(0xffffffffu, incl, 31);
+  }
+  __syncwarp();
+}
+
+// Per coloring: every CSR row stably counting-sorted by key, entries packed
+// as u | color << 27.  Warp per row over row_order[row0, n) (degree order,
+// dynamic); rows of up to kBucketCache * 32 neighbours are held in registers
+// so both passes cost one round of loads.  Longer rows: bucket_long.
+constexpr int kBucketCache = 8;
+constexpr int kBucketLong = 1024;  // rows above this go to bucket_long (CTA per row)
+__global__ void __launch_bounds__(256)
+bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t row0,
+            int32_t n, int k, const int32_t* __restrict__ cuts, int nparts, uint32_t* __restrict__ out,
+            int* __restrict__ next_row) {
+  extern __shared__ int bsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int nkeys = nparts * k;
+  int* cnt = bsm + warp * nkeys;
+  const unsigned lt = (1u << lane) - 1u;
+  for (;;) {
+    int ri = 0;
+    if (lane == 0) ri = row0 + atomicAdd(next_row, 1);
+    ri = __shfl_sync(0xffffffffu, ri, 0);
+    if (ri >= n) return;
+    const int32_t v = row_order[ri];
+    const int64_t b = row_ptr[v], e = row_ptr[v + 1];
+    const int d = static_cast<int>(e - b);
+    for (int i = lane; i < nkeys; i += 32) cnt[i] = 0;
+    __syncwarp();
+    if (d <= kBucketCache * 32) {
+      int u[kBucketCache], key[kBucketCache];
+#pragma unroll
+      for (int q = 0; q < kBucketCache; ++q) u[q] = q * 32 + lane < d ? __ldg(col + b + q * 32 + lane) : -1;
+#pragma unroll
+      for (int q = 0; q < kBucketCache; ++q) key[q] = u[q] >= 0 ? bucket_key(u[q], colors, cuts, nparts, k) : -1;
+#pragma unroll
+      for (int q = 0; q < kBucketCache; ++q) {
+        if (q * 32 >= d) break;
+        const unsigned same = __match_any_sync(0xffffffffu, key[q]);
+        if (key[q] >= 0 && (same & lt) == 0) cnt[key[q]] += __popc(same);
+        __syncwarp();
+      }
+      warp_exclusive_scan(cnt, nkeys, lane);
+#pragma unroll
+      for (int q = 0; q < kBucketCache; ++q) {
+        if (q * 32 >= d) break;
+        const unsigned same = __match_any_sync(0xffffffffu, key[q]);
+        const int slot = key[q] >= 0 ? cnt[key[q]] + __popc(same & lt) : 0;
+        __syncwarp();
+        if (key[q] >= 0) {
+          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(key[q] % k) << kPackShift);
+          if ((same & lt) == 0) cnt[key[q]] += __popc(same);
+        }
+        __syncwarp();
+      }
+    } else {
+      for (int64_t j = b; j < e; j += 32) {
+        const bool ok = j + lane < e;
+        const int key = ok ? bucket_key(col[j + lane], colors, cuts, nparts, k) : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, key);
+        if (ok && (same & lt) == 0) cnt[key] += __popc(same);
+        __syncwarp();
+      }
+      warp_exclusive_scan(cnt, nkeys, lane);
+      for (int64_t j = b; j < e; j += 32) {
+        const bool ok = j + lane < e;
+        const int u = ok ? col[j + lane] : 0;
+        const int key = ok ? bucket_key(u, colors, cuts, nparts, k) : -1;
+        const unsigned same = __match_any_sync(0xffffffffu, key);
+        const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
+        __syncwarp();
+        if (ok) {
+          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key % k) << kPackShift);
+          if ((same & lt) == 0) cnt[key] += __popc(same);
+        }
+        __syncwarp();
+      }
+    }
+  }
+}
+
+// Rows longer than kBucketLong (row_order[0, nlong)): one CTA per row; warp w
+// owns the w-th contiguous slice, so offsets ordered (key, warp) keep the sort
+// stable.  smem: cnt[8][nkeys] + tot[nkeys].
+__global__ void __launch_bounds__(256)
+bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int k,
+            const int32_t* __restrict__ cuts, int nparts, uint32_t* __restrict__ out) {
+  extern __shared__ int bsm[];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int nkeys = nparts * k;
+  int* cnt = bsm + warp * nkeys;
+  int* tot = bsm + nw * nkeys;
+  const unsigned lt = (1u << lane) - 1u;
+  const int32_t v = row_order[blockIdx.x];
+  const int64_t b = row_ptr[v], e = row_ptr[v + 1];
+  const int64_t slice = ((e - b + nw - 1) / nw + 31) / 32 * 32;
+  const int64_t sb = b + warp * slice, se = min(e, sb + slice);
+  for (int i = threadIdx.x; i < (nw + 1) * nkeys; i += blockDim.x) bsm[i] = 0;
+  __syncthreads();
+  for (int64_t j = sb; j < se; j += 32) {
+    const bool ok = j + lane < se;
+    const int key = ok ? bucket_key(col[j + lane], colors, cuts, nparts, k) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    if (ok && (same & lt) == 0) cnt[key] += __popc(same);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int key = threadIdx.x; key < nkeys; key += blockDim.x) {
+    int t = 0;
+    for (int w = 0; w < nw; ++w) t += bsm[w * nkeys + key];
+    tot[key] = t;
+  }
+  __syncthreads();
+  if (warp == 0) warp_exclusive_scan(tot, nkeys, lane);
+  __syncthreads();
+  for (int key = threadIdx.x; key < nkeys; key += blockDim.x) {
+    int run = tot[key];
+    for (int w = 0; w < nw; ++w) {
+      const int c = bsm[w * nkeys + key];
+      bsm[w * nkeys + key] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  for (int64_t j = sb; j < se; j += 32) {
+    const bool ok = j + lane < se;
+    const int u = ok ? col[j + lane] : 0;
+    const int key = ok ? bucket_key(u, colors, cuts, nparts, k) : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, key);
+    const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
+    __syncwarp();
+    if (ok) {
+      out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key % k) << kPackShift);
+      if ((same & lt) == 0) cnt[key] += __popc(same);
+    }
+    __syncwarp();
+  }
+}
+
+// Full table M (C columns) -> compressed table (groups * zw columns): slot t
+// of group g of vertex u holds M[u, slot_col[color(u)][g][t]] (0 if unused).
+// A CTA stages the full rows of `vpb` vertices in smem (coalesced 128 B panel
+// rows), then writes the compressed rows group-major (coalesced as well).
+__global__ void __launch_bounds__(256)
+rooted_compress(const float* __restrict__ M, int C, const uint8_t* __restrict__ colors,
+                const int32_t* __restrict__ slot_col, int groups, int zw, int32_t n, int vpb,
+                float* __restrict__ out) {
+  extern __shared__ float crow[];
+  const int panels = num_panels(C);
+  const int zl = last_panel_width(C);
+  const int rf = (panels - 1) * kZ + zl;  // floats of one panel-padded row
+  const int per = rf / 4;
+  const int64_t u0 = static_cast<int64_t>(blockIdx.x) * vpb;
+  for (int f = threadIdx.x; f < vpb * per; f += blockDim.x) {
+    const int r = f / per, c4 = (f % per) * 4;
+    const int64_t u = u0 + r;
+    if (u >= n) continue;
+    const int p = c4 / kZ, z = c4 % kZ;
+    const int zp = p == panels - 1 ? zl : kZ;
+    *reinterpret_cast<float4*>(crow + r * rf + c4) =
+        __ldg(reinterpret_cast<const float4*>(M + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+  }
+  __syncthreads();
+  const int total = vpb * groups * zw;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int t = i % zw, it = i / zw;
+    const int g = it / vpb, r = it % vpb;
+    const int64_t u = u0 + r;
+    if (u >= n) continue;
+    const int col = __ldg(slot_col + (static_cast<int64_t>(colors[u]) * groups + g) * zw + t);
+    out[static_cast<int64_t>(g) * n * kZ + u * zw + t] = col >= 0 ? crow[r * rf + col] : 0.f;
+  }
+}
+
+// One launch = one (group, part).  Task = one segment (lane group of G = ZW/4
+// lanes, float4 per lane), as spmm_part.  A ROUND takes the next (up to) R
+// entries of the segment that share the first one's color -- rows are color
+// sorted, so that is a prefix -- gathers them, and adds their fp32 tree sum
+// to the fp64 run accumulator; a color change scatters the run into the
+// task's F_g accumulators (smem, fp32: each F_g column receives at most one
+// run per color of its set).  The next round's entries are fetched while the
+// current round's gathers are in flight (its start only depends on the
+// entries' colors).  slot_acc: [k][stride], this group's zw slots at offset 0.
+template <int ZW>
+__global__ void __launch_bounds__(kSpmmWarps * 32, 4)
+spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __restrict__ colb,
+            const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
+            int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
+            double* __restrict__ partial, int first) {
+  constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
+  extern __shared__ float racc_sm[];
+  const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
+  const int64_t task = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp;
+  if (task >= ntasks) return;
+  const Seg s = segs[task * SPW + g];
+  float* acc = racc_sm + static_cast<int64_t>(warp * SPW + g) * fpad;
+  for (int i = l; i < fpad; i += G) acc[i] = 0.f;
+  const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
+  const uint32_t* cp = colb + s.e_begin;
+  const int len = s.len;
+  double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
+  int cur = -1;
+  int pos = 0;  // first unconsumed entry of the segment
+  auto fetch = [&](int at, uint32_t (&w)[NI]) {
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const int e = at + i * G + l;
+      w[i] = e < len ? static_cast<uint32_t>(ld_stream_i32(reinterpret_cast<const int32_t*>(cp + e), pstream))
+                     : kPackSentinel;
+    }
+  };
+  uint32_t w[NI];
+  fetch(0, w);
+  __syncwarp();
+  for (;;) {
+    uint32_t pk[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) pk[j] = __shfl_sync(0xffffffffu, w[j / G], g * G + (j % G));
+    const uint32_t c_round = pk[0] >> kPackShift;
+    int count = 0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) count += (pk[j] >> kPackShift) == c_round && pk[j] != kPackSentinel;
+    if (!__any_sync(0xffffffffu, count > 0)) break;
+    pos += count;
+    fetch(pos, w);  // next round's entries, overlapping this round's gathers
+    float4 v[R];
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      v[j] = make_float4(0, 0, 0, 0);
+      if (j < count) v[j] = ld_keep_f4(X + static_cast<int64_t>(pk[j] & kPackMask) * ZW + l * 4, pkeep);
+    }
+    if (count > 0 && static_cast<int>(c_round) != cur) {
+      if (cur >= 0) {
+        const short4 sl = __ldg(reinterpret_cast<const short4*>(slot_acc + static_cast<int64_t>(cur) * slot_stride + l * 4));
+        if (sl.x >= 0) acc[sl.x] += static_cast<float>(r0);
+        if (sl.y >= 0) acc[sl.y] += static_cast<float>(r1);
+        if (sl.z >= 0) acc[sl.z] += static_cast<float>(r2);
+        if (sl.w >= 0) acc[sl.w] += static_cast<float>(r3);
+        r0 = r1 = r2 = r3 = 0;
+      }
+      cur = static_cast<int>(c_round);
+    }
+#pragma unroll
+    for (int wd = R / 2; wd; wd >>= 1)
+#pragma unroll
+      for (int j = 0; j < wd; ++j) {
+        v[j].x += v[j + wd].x; v[j].y += v[j + wd].y; v[j].z += v[j + wd].z; v[j].w += v[j + wd].w;
+      }
+    r0 += v[0].x; r1 += v[0].y; r2 += v[0].z; r3 += v[0].w;
+  }
+  if (cur >= 0) {
+    const short4 sl = __ldg(reinterpret_cast<const short4*>(slot_acc + static_cast<int64_t>(cur) * slot_stride + l * 4));
+    if (sl.x >= 0) acc[sl.x] += static_cast<float>(r0);
+    if (sl.y >= 0) acc[sl.y] += static_cast<float>(r1);
+    if (sl.z >= 0) acc[sl.z] += static_cast<float>(r2);
+    if (sl.w >= 0) acc[sl.w] += static_cast<float>(r3);
+  }
+  __syncwarp();
+  if (s.dst == kSkip) return;
+  if (s.dst >= 0) {
+    for (int i = l * 4; i < fpad; i += G * 4) {
+      const int colc = fbase + i;
+      const int p = colc / kZ, z = colc % kZ;
+      float* yp = Y + static_cast<int64_t>(p) * n * kZ + static_cast<int64_t>(s.dst) * panel_width(Cstore, p) + z;
+      float4 a = *reinterpret_cast<const float4*>(acc + i);
+      if (!first) {
+        const float4 o = ld_stream_f4(yp, pstream);
+        a.x += o.x; a.y += o.y; a.z += o.z; a.w += o.w;
+      }
+      st_stream_f4(yp, a, pstream);
+    }
+  } else {
+    double* pp = partial + static_cast<int64_t>(-1 - s.dst) * fpad;
+    for (int i = l; i < fpad; i += G) pp[i] = acc[i];
+  }
+}
+
+// Split rows of the rooted SpMM: storage columns [fbase, fbase + fpad) of row
+// rows[r] (+)= the sum of the row's fp64 partial slots, in slot order.
+__global__ void rooted_fixup(const int32_t* __restrict__ rows, const int32_t* __restrict__ slot_begin,
+                             int nrows, const double* __restrict__ partial, int fbase, int fpad, int Cstore,
+                             int32_t n, float* __restrict__ Y, int first) {
+  const int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x;
+  if (i >= static_cast<int64_t>(nrows) * fpad) return;
+  const int a = static_cast<int>(i % fpad);
+  const int r = static_cast<int>(i / fpad);
+  double acc = 0;
+  for (int s = slot_begin[r]; s < slot_begin[r + 1]; ++s) acc += partial[static_cast<int64_t>(s) * fpad + a];
+  float* y = Y + panel_offset(Cstore, n, rows[r], fbase + a);
+  *y = static_cast<float>(first ? acc : acc + static_cast<double>(*y));
+}
+
 // Split rows: Y[row] (+)= sum of the row's fp64 partial slots, in slot order.
 __global__ void spmm_fixup(const int32_t* __restrict__ rows, const int32_t* __restrict__ slot_begin,
                            int nrows, const double* __restrict__ partial, float* __restrict__ Y,
@@ -467,6 +793,45 @@ __device__ __forceinline__ void stage_tile(const float* __restrict__ T, int C, i
       if (c + 1 < C) dst[(c + 1) * kSpitch + vv[u]] = x[u].y;
       if (c + 2 < C) dst[(c + 2) * kSpitch + vv[u]] = x[u].z;
       if (c + 3 < C) dst[(c + 3) * kSpitch + vv[u]] = x[u].w;
+    }
+  }
+}
+
+// stage_tile for a P' stored group-major (rooted layout): storage column c
+// goes to smem row inv[c] (the combinadic column), padding (-1) is dropped.
+// Cstore is a multiple of 8, so a float4 never straddles its end.
+template <int kStageU>
+__device__ __forceinline__ void stage_tile_map(const float* __restrict__ T, int Cstore, int32_t n, int64_t v0,
+                                               float* dst, const int32_t* __restrict__ inv) {
+  const int panels = num_panels(Cstore);
+  const int zl = last_panel_width(Cstore);
+  const int full4 = (panels - 1) * kTileV * (kZ / 4);
+  const int total4 = full4 + kTileV * (zl / 4);
+  for (int base = threadIdx.x; base < total4; base += blockDim.x * kStageU) {
+    float4 x[kStageU];
+    int c0[kStageU], vv[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int f = base + u * blockDim.x;
+      int p, r, zw;
+      if (f < full4) { p = f / (kTileV * 8); r = f % (kTileV * 8); zw = kZ; }
+      else { p = panels - 1; r = f - full4; zw = zl; }
+      const int q4 = zw / 4;
+      vv[u] = r / q4;
+      c0[u] = p * kZ + (r % q4) * 4;
+      x[u] = make_float4(0, 0, 0, 0);
+      if (f < total4 && v0 + vv[u] < n && c0[u] < Cstore)
+        x[u] = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + (v0 + vv[u]) * zw + (r % q4) * 4));
+      if (f >= total4) c0[u] = Cstore;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      if (c0[u] >= Cstore) continue;
+      const int4 m = __ldg(reinterpret_cast<const int4*>(inv + c0[u]));
+      if (m.x >= 0) dst[m.x * kSpitch + vv[u]] = x[u].x;
+      if (m.y >= 0) dst[m.y * kSpitch + vv[u]] = x[u].y;
+      if (m.z >= 0) dst[m.z * kSpitch + vv[u]] = x[u].z;
+      if (m.w >= 0) dst[m.w * kSpitch + vv[u]] = x[u].w;
     }
   }
 }
@@ -646,7 +1011,8 @@ template <bool STAGED>
 __global__ void __launch_bounds__(256)
 ema_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
             const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks,
-            int Ca, int Cp, int Cs, int32_t n, float* __restrict__ out) {
+            int Ca, int Cp, int Cs, int32_t n, float* __restrict__ out, int Cps,
+            const int32_t* __restrict__ pinv) {
   extern __shared__ float smem[];
   __shared__ int next_group;
   const int lane = threadIdx.x & 31;
@@ -656,7 +1022,8 @@ ema_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
   float* sP = smem + Ca * kSpitch;
   if (threadIdx.x == 0) next_group = blockDim.x / 32;
   stage_tile<8>(Am, Ca, n, v0, sA);
-  stage_tile<8>(Pm, Cp, n, v0, sP);
+  if (pinv) stage_tile_map<8>(Pm, Cps, n, v0, sP, pinv);
+  else stage_tile<8>(Pm, Cp, n, v0, sP);
   __syncthreads();
   // groups are sorted by work (descending); warps take them dynamically
   for (int gi = threadIdx.x >> 5; gi < ngroups;) {
@@ -713,6 +1080,24 @@ __device__ __forceinline__ void stage_row(const float* __restrict__ T, int C, in
   }
 }
 
+// stage_row of a group-major P' (see stage_tile_map): dst[inv[c]] = row[c]
+__device__ __forceinline__ void stage_row_map(const float* __restrict__ T, int Cstore, int32_t n, int64_t v,
+                                              float* dst, const int32_t* __restrict__ inv) {
+  const int panels = num_panels(Cstore);
+  const int zl = last_panel_width(Cstore);
+  const int total4 = Cstore / 4;
+  for (int f = threadIdx.x; f < total4; f += blockDim.x) {
+    const int p = (f * 4) / kZ, z4 = (f * 4) % kZ;
+    const int zw = p == panels - 1 ? zl : kZ;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
+    const int4 m = __ldg(reinterpret_cast<const int4*>(inv + f * 4));
+    if (m.x >= 0) dst[m.x] = x.x;
+    if (m.y >= 0) dst[m.y] = x.y;
+    if (m.z >= 0) dst[m.z] = x.z;
+    if (m.w >= 0) dst[m.w] = x.w;
+  }
+}
+
 #define TCG_IJV(I, J) \
   case I * 8 + J: micro_block_v<I, J>(sA + bd.x, sP + bd.y, acc); break;
 
@@ -733,7 +1118,8 @@ __device__ __forceinline__ void micro_block_v(const float* __restrict__ sa, cons
 __global__ void __launch_bounds__(256)
 ema_vtx_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
                 const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks,
-                int Ca, int Cp, int Cs, int32_t n, float* __restrict__ out) {
+                int Ca, int Cp, int Cs, int32_t n, float* __restrict__ out, int Cps,
+                const int32_t* __restrict__ pinv) {
   extern __shared__ float smem[];
   float* sA = smem;
   float* sP = smem + row_floats(Ca);  // stage_row writes the panel-padded row
@@ -741,7 +1127,8 @@ ema_vtx_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
   for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
     __syncthreads();
     stage_row(Am, Ca, n, v, sA);
-    stage_row(Pm, Cp, n, v, sP);
+    if (pinv) stage_row_map(Pm, Cps, n, v, sP, pinv);
+    else stage_row(Pm, Cp, n, v, sP);
     __syncthreads();
     for (int r = 0;; ++r) {
       const int gi = (r & 1) ? (r + 1) * T - 1 - static_cast<int>(threadIdx.x) : r * T + static_cast<int>(threadIdx.x);
