@@ -226,7 +226,6 @@ void Engine::release_graph() {
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
-  dfree(d_cuts_);
   n_ = -1;
 }
 
@@ -537,30 +536,25 @@ void Engine::plan_arena() {
   std::vector<int64_t> child_pp(plan_.num_nodes, -1);  // P' kept alive for an LSpMM parent
   int64_t lslots = 0;
   const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
-  // rooted SpMMs: one part count for all of them (the widest compressed
-  // panel's), so the per-coloring row bucketing matches every schedule
+  // rooted SpMMs: parts are contiguous COLOR classes (one count for all
+  // rooted nodes: the widest compressed panel's), over whole-row schedules
   need_rooted_ = false;
   rooted_parts_ = 1;
   for (auto& e : exec_)
     if (e.rooted) {
       need_rooted_ = true;
-      rooted_parts_ = std::max(rooted_parts_, parts_for_width(e.rl_zw));
+      rooted_parts_ = std::max(rooted_parts_, std::min(plan_.k, parts_for_width(e.rl_zw)));
     }
-  dfree(d_cuts_);
-  rcol_off_ = -1;
+  rcol_off_ = rcut_off_ = -1;
   int64_t rooted_partial = 0;
   if (need_rooted_) {
     if (nsrc_ >= (1 << dev::kPackShift))
       throw invalid_argument("graph too large for the rooted-compressed SpMM (ids >= 2^27); set TCG_ROOTED=0");
     rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
-    std::vector<int32_t> cuts(static_cast<size_t>(rooted_parts_) + 1);
-    for (int q = 0; q <= rooted_parts_; ++q) cuts[q] = static_cast<int32_t>(static_cast<int64_t>(nsrc_) * q / rooted_parts_);
-    d_cuts_ = dupload(cuts, stream_);
-    int slots = 0;
-    for (auto& ps : sched_.at(rooted_parts_)) slots = std::max(slots, ps.nslots);
+    rcut_off_ = ap.alloc(8 * static_cast<int64_t>(n_) * (rooted_parts_ + 1));
+    const int slots = sched_.at(1)[0].nslots;
     for (auto& e : exec_)
       if (e.rooted) rooted_partial = std::max<int64_t>(rooted_partial, static_cast<int64_t>(slots) * static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / e.rl_zw))));
-    TCG_CUDA(cudaStreamSynchronize(stream_));
   }
   for (auto& e : exec_) {
     if (!e.p_leaf && e.rooted) {
@@ -865,11 +859,19 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
         M, e.Cp, d_colors, e.d_slot_col, G, zw, n_, vpb, X);
     ++launches_;
   }
-  const auto& parts = sched_.at(rooted_parts_);
+  const PartSchedule& ps = sched_.at(1)[0];  // whole rows; parts = color classes
   const uint32_t* colb = reinterpret_cast<const uint32_t*>(arena_ + rcol_off_);
-  const void* kern = zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32>)
-                   : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16>)
-                              : reinterpret_cast<const void*>(dev::spmm_rooted<8>);
+  const int64_t* cuts = reinterpret_cast<const int64_t*>(arena_ + rcut_off_);
+  static const int minb = [] {
+    const char* s = std::getenv("TCG_ROOTED_MINB");
+    return s ? std::atoi(s) : 4;
+  }();
+  const void* kern = minb == 4 ? (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 4>)
+                                  : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 4>)
+                                             : reinterpret_cast<const void*>(dev::spmm_rooted<8, 4>))
+                               : (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 1>)
+                                  : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 1>)
+                                             : reinterpret_cast<const void*>(dev::spmm_rooted<8, 1>));
   TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rooted_smem)));
   const int spw = 128 / zw;
   for (int g = 0; g < G; ++g) {
@@ -882,17 +884,18 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - fbase;
     const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * fpad * 4;
     const int16_t* sl = e.d_slot_acc + static_cast<int64_t>(g) * zw;
-    for (size_t q = 0; q < parts.size(); ++q) {
-      const PartSchedule& ps = parts[q];
+    int slot_stride = G * zw;
+    for (int q = 0; q < rooted_parts_; ++q) {
       const int64_t ntasks = ps.nseg_padded / spw;
       const unsigned blocks = static_cast<unsigned>((ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps);
       const int first = q == 0 ? 1 : 0;
-      if (zw == 32)
-        dev::spmm_rooted<32><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
-      else if (zw == 16)
-        dev::spmm_rooted<16><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
-      else
-        dev::spmm_rooted<8><<<blocks, dev::kSpmmWarps * 32, smem, stream_>>>(ps.d_segs, ntasks, colb, Xg, sl, G * zw, fbase, fpad, e.Cps, n_, Pp, d_partial_, first);
+      int part = q;
+      void* args[] = {const_cast<dev::Seg**>(&ps.d_segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
+                      const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
+                      const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
+                      const_cast<int*>(&fpad), const_cast<int32_t*>(&e.Cps), &n_, &Pp, &d_partial_,
+                      const_cast<int*>(&first)};
+      TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {
         const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * fpad;
@@ -991,20 +994,16 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     size_t b0 = 0;
     if (prof_) { b0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
-    const size_t nkeys = static_cast<size_t>(rooted_parts_) * plan_.k;
-    const size_t smem = sizeof(int) * 8 * nkeys, lsmem = sizeof(int) * 9 * nkeys;
-    if (smem > 48 * 1024)
-      TCG_CUDA(cudaFuncSetAttribute(dev::bucket_rows, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    if (lsmem > 48 * 1024)
-      TCG_CUDA(cudaFuncSetAttribute(dev::bucket_long, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(lsmem)));
+    const size_t smem = sizeof(int) * 8 * plan_.k, lsmem = sizeof(int) * 9 * plan_.k;
     uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
+    int64_t* cuts = reinterpret_cast<int64_t*>(arena_ + rcut_off_);
     if (nlong_ > 0) {
       dev::bucket_long<<<static_cast<unsigned>(nlong_), 256, lsmem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_,
-                                                                                plan_.k, d_cuts_, rooted_parts_, rc);
+                                                                                plan_.k, rooted_parts_, rc, cuts);
       ++launches_;
     }
     dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, n_, plan_.k,
-                                                     d_cuts_, rooted_parts_, rc, d_counter_);
+                                                     rooted_parts_, rc, cuts);
     ++launches_;
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }

@@ -192,8 +192,8 @@ class Engine {
   int64_t colb_off_ = -1, boff_off_ = -1;
   bool need_rooted_ = false;         // some node uses the rooted-compressed SpMM
   int rooted_parts_ = 1;             // part count of every rooted SpMM (and of the row bucketing)
-  int64_t rcol_off_ = -1;            // per-coloring (part, color)-sorted packed CSR
-  int32_t* d_cuts_ = nullptr;        // rooted_parts_ + 1 gather-id part boundaries
+  int64_t rcol_off_ = -1;            // per-coloring color-sorted packed CSR
+  int64_t rcut_off_ = -1;            // per-coloring part (color class) cuts, n * (parts + 1)
   void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors);
   std::vector<int64_t> table_off_;   // per node id: arena offset of its table (internal)
   std::vector<int64_t> pprime_off_;  // per node id: offset of P' computed from it

@@ -426,15 +426,6 @@ constexpr uint32_t kPackSentinel = 0xFFFFFFFFu;  // color 31: never a real color
 constexpr int kPackShift = 27;
 constexpr uint32_t kPackMask = (1u << kPackShift) - 1u;
 
-// Key of a neighbour: part(u) * k + color(u); `cuts` holds the nparts + 1
-// gather-id boundaries of the parts (engine.cu parts_for_width).
-__device__ __forceinline__ int bucket_key(int u, const uint8_t* __restrict__ colors,
-                                          const int32_t* __restrict__ cuts, int nparts, int k) {
-  int p = 0;
-  while (p + 1 < nparts && u >= __ldg(cuts + p + 1)) ++p;
-  return p * k + colors[u];
-}
-
 // exclusive scan of cnt[0, nkeys) by one warp, in place
 __device__ __forceinline__ void warp_exclusive_scan(int* cnt, int nkeys, int lane) {
   int run = 0;
@@ -451,38 +442,44 @@ __device__ __forceinline__ void warp_exclusive_scan(int* cnt, int nkeys, int lan
   __syncwarp();
 }
 
-// Per coloring: every CSR row stably counting-sorted by key, entries packed
-// as u | color << 27.  Warp per row over row_order[row0, n) (degree order,
-// dynamic); rows of up to kBucketCache * 32 neighbours are held in registers
-// so both passes cost one round of loads.  Longer rows: bucket_long.
-constexpr int kBucketCache = 8;
+// Per coloring: every CSR row stably counting-sorted by neighbour color,
+// entries packed as u | color << 27, and the row's PART CUTS recorded: the
+// rooted SpMM's parts are contiguous color classes [i*k/P, (i+1)*k/P), so
+// part i of row v is [cut[v*(P+1)+i], cut[v*(P+1)+i+1]) -- whole color runs,
+// and a part's gather footprint is the rows of its colors (~n/P lines).
+// Warp per row over row_order[row0, n) (degree order, static round-robin);
+// rows of up to kBucketCache * 32 neighbours are held in registers so both
+// passes cost one round of loads.  Longer rows: bucket_long.
+constexpr int kBucketCache = 16;
 constexpr int kBucketLong = 1024;  // rows above this go to bucket_long (CTA per row)
 __global__ void __launch_bounds__(256)
 bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
             const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t row0,
-            int32_t n, int k, const int32_t* __restrict__ cuts, int nparts, uint32_t* __restrict__ out,
-            int* __restrict__ next_row) {
+            int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts) {
   extern __shared__ int bsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int nkeys = nparts * k;
-  int* cnt = bsm + warp * nkeys;
+  int* cnt = bsm + warp * k;
   const unsigned lt = (1u << lane) - 1u;
-  for (;;) {
-    int ri = 0;
-    if (lane == 0) ri = row0 + atomicAdd(next_row, 1);
-    ri = __shfl_sync(0xffffffffu, ri, 0);
-    if (ri >= n) return;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t ri = row0 + static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + warp; ri < n; ri += nwarps) {
     const int32_t v = row_order[ri];
     const int64_t b = row_ptr[v], e = row_ptr[v + 1];
     const int d = static_cast<int>(e - b);
-    for (int i = lane; i < nkeys; i += 32) cnt[i] = 0;
+    for (int i = lane; i < k; i += 32) cnt[i] = 0;
     __syncwarp();
+    auto write_cuts = [&]() {
+      if (lane <= nparts) {
+        const int cb = lane * k / nparts;
+        cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + (cb < k ? cnt[cb] : d);
+      }
+      __syncwarp();
+    };
     if (d <= kBucketCache * 32) {
       int u[kBucketCache], key[kBucketCache];
 #pragma unroll
       for (int q = 0; q < kBucketCache; ++q) u[q] = q * 32 + lane < d ? __ldg(col + b + q * 32 + lane) : -1;
 #pragma unroll
-      for (int q = 0; q < kBucketCache; ++q) key[q] = u[q] >= 0 ? bucket_key(u[q], colors, cuts, nparts, k) : -1;
+      for (int q = 0; q < kBucketCache; ++q) key[q] = u[q] >= 0 ? colors[u[q]] : -1;
 #pragma unroll
       for (int q = 0; q < kBucketCache; ++q) {
         if (q * 32 >= d) break;
@@ -490,7 +487,8 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
         if (key[q] >= 0 && (same & lt) == 0) cnt[key[q]] += __popc(same);
         __syncwarp();
       }
-      warp_exclusive_scan(cnt, nkeys, lane);
+      warp_exclusive_scan(cnt, k, lane);
+      write_cuts();
 #pragma unroll
       for (int q = 0; q < kBucketCache; ++q) {
         if (q * 32 >= d) break;
@@ -498,7 +496,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
         const int slot = key[q] >= 0 ? cnt[key[q]] + __popc(same & lt) : 0;
         __syncwarp();
         if (key[q] >= 0) {
-          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(key[q] % k) << kPackShift);
+          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(key[q]) << kPackShift);
           if ((same & lt) == 0) cnt[key[q]] += __popc(same);
         }
         __syncwarp();
@@ -506,21 +504,22 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     } else {
       for (int64_t j = b; j < e; j += 32) {
         const bool ok = j + lane < e;
-        const int key = ok ? bucket_key(col[j + lane], colors, cuts, nparts, k) : -1;
+        const int key = ok ? colors[col[j + lane]] : -1;
         const unsigned same = __match_any_sync(0xffffffffu, key);
         if (ok && (same & lt) == 0) cnt[key] += __popc(same);
         __syncwarp();
       }
-      warp_exclusive_scan(cnt, nkeys, lane);
+      warp_exclusive_scan(cnt, k, lane);
+      write_cuts();
       for (int64_t j = b; j < e; j += 32) {
         const bool ok = j + lane < e;
         const int u = ok ? col[j + lane] : 0;
-        const int key = ok ? bucket_key(u, colors, cuts, nparts, k) : -1;
+        const int key = ok ? colors[u] : -1;
         const unsigned same = __match_any_sync(0xffffffffu, key);
         const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
         __syncwarp();
         if (ok) {
-          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key % k) << kPackShift);
+          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
           if ((same & lt) == 0) cnt[key] += __popc(same);
         }
         __syncwarp();
@@ -530,45 +529,50 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
 }
 
 // Rows longer than kBucketLong (row_order[0, nlong)): one CTA per row; warp w
-// owns the w-th contiguous slice, so offsets ordered (key, warp) keep the sort
-// stable.  smem: cnt[8][nkeys] + tot[nkeys].
+// owns the w-th contiguous slice, so offsets ordered (color, warp) keep the
+// sort stable.  smem: cnt[8][k] + tot[k].
 __global__ void __launch_bounds__(256)
 bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int k,
-            const int32_t* __restrict__ cuts, int nparts, uint32_t* __restrict__ out) {
+            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int k, int nparts,
+            uint32_t* __restrict__ out, int64_t* __restrict__ cuts) {
   extern __shared__ int bsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int nkeys = nparts * k;
-  int* cnt = bsm + warp * nkeys;
-  int* tot = bsm + nw * nkeys;
+  int* cnt = bsm + warp * k;
+  int* tot = bsm + nw * k;
   const unsigned lt = (1u << lane) - 1u;
   const int32_t v = row_order[blockIdx.x];
   const int64_t b = row_ptr[v], e = row_ptr[v + 1];
   const int64_t slice = ((e - b + nw - 1) / nw + 31) / 32 * 32;
-  const int64_t sb = b + warp * slice, se = min(e, sb + slice);
-  for (int i = threadIdx.x; i < (nw + 1) * nkeys; i += blockDim.x) bsm[i] = 0;
+  const int64_t sb = min(e, b + warp * slice), se = min(e, sb + slice);
+  for (int i = threadIdx.x; i < (nw + 1) * k; i += blockDim.x) bsm[i] = 0;
   __syncthreads();
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
-    const int key = ok ? bucket_key(col[j + lane], colors, cuts, nparts, k) : -1;
+    const int key = ok ? colors[col[j + lane]] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     if (ok && (same & lt) == 0) cnt[key] += __popc(same);
     __syncwarp();
   }
   __syncthreads();
-  for (int key = threadIdx.x; key < nkeys; key += blockDim.x) {
+  for (int key = threadIdx.x; key < k; key += blockDim.x) {
     int t = 0;
-    for (int w = 0; w < nw; ++w) t += bsm[w * nkeys + key];
+    for (int w = 0; w < nw; ++w) t += bsm[w * k + key];
     tot[key] = t;
   }
   __syncthreads();
-  if (warp == 0) warp_exclusive_scan(tot, nkeys, lane);
+  if (warp == 0) {
+    warp_exclusive_scan(tot, k, lane);
+    if (lane <= nparts) {
+      const int cb = lane * k / nparts;
+      cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + (cb < k ? tot[cb] : e - b);
+    }
+  }
   __syncthreads();
-  for (int key = threadIdx.x; key < nkeys; key += blockDim.x) {
+  for (int key = threadIdx.x; key < k; key += blockDim.x) {
     int run = tot[key];
     for (int w = 0; w < nw; ++w) {
-      const int c = bsm[w * nkeys + key];
-      bsm[w * nkeys + key] = run;
+      const int c = bsm[w * k + key];
+      bsm[w * k + key] = run;
       run += c;
     }
   }
@@ -576,12 +580,12 @@ bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
     const int u = ok ? col[j + lane] : 0;
-    const int key = ok ? bucket_key(u, colors, cuts, nparts, k) : -1;
+    const int key = ok ? colors[u] : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
     __syncwarp();
     if (ok) {
-      out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key % k) << kPackShift);
+      out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
       if ((same & lt) == 0) cnt[key] += __popc(same);
     }
     __syncwarp();
@@ -632,9 +636,10 @@ rooted_compress(const float* __restrict__ M, int C, const uint8_t* __restrict__ 
 // run per color of its set).  The next round's entries are fetched while the
 // current round's gathers are in flight (its start only depends on the
 // entries' colors).  slot_acc: [k][stride], this group's zw slots at offset 0.
-template <int ZW>
-__global__ void __launch_bounds__(kSpmmWarps * 32, 4)
+template <int ZW, int MINB>
+__global__ void __launch_bounds__(kSpmmWarps * 32, MINB)
 spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __restrict__ colb,
+            const int64_t* __restrict__ cuts, int nparts, int part, const int32_t* __restrict__ slot_row,
             const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
             int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
             double* __restrict__ partial, int first) {
@@ -647,8 +652,17 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   float* acc = racc_sm + static_cast<int64_t>(warp * SPW + g) * fpad;
   for (int i = l; i < fpad; i += G) acc[i] = 0.f;
   const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
-  const uint32_t* cp = colb + s.e_begin;
-  const int len = s.len;
+  // this part's color class of the segment's row: [cut_p, cut_p+1) ∩ segment
+  int64_t lo = s.e_begin, hi = s.e_begin;
+  if (s.dst != kSkip) {
+    const int32_t row = s.dst >= 0 ? s.dst : slot_row[-1 - s.dst];
+    const int64_t* ct = cuts + static_cast<int64_t>(row) * (nparts + 1) + part;
+    lo = max(s.e_begin, ct[0]);
+    hi = min(s.e_begin + s.len, ct[1]);
+    if (hi < lo) hi = lo;
+  }
+  const uint32_t* cp = colb + lo;
+  const int len = static_cast<int>(hi - lo);
   double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
   int cur = -1;
   int pos = 0;  // first unconsumed entry of the segment
@@ -663,22 +677,29 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   uint32_t w[NI];
   fetch(0, w);
   __syncwarp();
+  const float* Xl = X + l * 4;
+  const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (g * G);
   for (;;) {
+    // the round = the prefix of the next R entries sharing entry 0's color
+    // (entry j sits in lane j % G, word j / G of the group)
+    const uint32_t c_round = __shfl_sync(0xffffffffu, w[0], g * G) >> kPackShift;
+    int count = 0;
+#pragma unroll
+    for (int i = 0; i < NI; ++i) {
+      const bool ok = w[i] != kPackSentinel && (w[i] >> kPackShift) == c_round;
+      count += __popc(__ballot_sync(0xffffffffu, ok) & gmask);
+    }
+    if (!__any_sync(0xffffffffu, count > 0)) break;
     uint32_t pk[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) pk[j] = __shfl_sync(0xffffffffu, w[j / G], g * G + (j % G));
-    const uint32_t c_round = pk[0] >> kPackShift;
-    int count = 0;
-#pragma unroll
-    for (int j = 0; j < R; ++j) count += (pk[j] >> kPackShift) == c_round && pk[j] != kPackSentinel;
-    if (!__any_sync(0xffffffffu, count > 0)) break;
     pos += count;
     fetch(pos, w);  // next round's entries, overlapping this round's gathers
     float4 v[R];
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       v[j] = make_float4(0, 0, 0, 0);
-      if (j < count) v[j] = ld_keep_f4(X + static_cast<int64_t>(pk[j] & kPackMask) * ZW + l * 4, pkeep);
+      if (j < count) v[j] = ld_keep_f4(Xl + static_cast<int64_t>(pk[j] & kPackMask) * ZW, pkeep);
     }
     if (count > 0 && static_cast<int>(c_round) != cur) {
       if (cur >= 0) {
