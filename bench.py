@@ -40,7 +40,7 @@ CONFIGS = {
              "R-MAT scale 20 ef100 (.45,.15,.15,.25), k=17 tree"),
 }
 DEFAULT_CONFIG = "cfg3"
-L2_GATHER_PEAK_GBS = 15400.0  # measured: 64 B row gathers from a 64 MB L2-resident panel (profiles/r01_membench.txt)
+L2_GATHER_PEAK_GBS = 19461.3  # measured: 128 B row gathers from a 64 MB L2-resident panel (profiles/r01_membench.txt)
 
 
 def log(*a):
@@ -305,16 +305,19 @@ def run_b200(args, rank, world, local, dist):
                    "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
                    "l2": "inputs larger than L2 (CSR %.0f MB + count tables %.1f GB vs 126 MB L2)"
                          % ((g.csc_col_ptr.nbytes + g.csc_rows.nbytes) / 1e6, need / 1e9)},
-        "roofline": {"kernel": "spmm_panels (+fixup)", "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
+        "roofline": {"kernel": "spmm phase (rooted: bucket_rows + rooted_compress + spmm_rooted + rooted_fixup)",
+                     "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
                      "unit": "GB/s", "frac": spmm_gbs / hbm_peak if spmm_gbs else None,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
                      "alg_bytes_per_launch": per_launch_bytes, "ms_per_launch": per_launch_ms,
                      "launches": tm.spmm_launches, "peak_source": peak_src,
-                     "note": "achieved = SURVEY 8(d) compulsory bytes (4 nnz + 8(n+1) + 8 n C_p) / CUDA-event time; "
-                             "the panel gathers are L2->SM bound, see l2_gather",
+                     "note": "launch = one node-level SpMM; achieved = SURVEY 8(d) compulsory bytes "
+                             "(4 nnz + 8(n+1) + 8 n C_p) / CUDA-event time; traffic = ncu DRAM bytes of the "
+                             "SpMM-phase kernels per node-level SpMM (profiles/ncu_traffic.json); the panel "
+                             "gathers are L2->SM bound, see l2_gather",
                      "l2_gather": {"achieved": gathered_gbs, "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
                                    "frac": gathered_gbs / L2_GATHER_PEAK_GBS if gathered_gbs else None,
-                                   "bytes": "nnz * 64 B * panels per launch"},
+                                   "bytes": "nnz * 4 B * gathered columns (compressed groups x zw, or full panels)"},
                      "ema": {"achieved_gbs": ema_gbs, "frac_hbm": ema_gbs / hbm_peak if ema_gbs else None,
                              "tflops": tm.ema_flops / (tm.ema_ms * 1e-3) / 1e12 if tm.ema_ms else None,
                              "ms_per_coloring": tm.ema_ms / args.steps}},
