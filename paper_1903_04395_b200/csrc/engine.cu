@@ -1,6 +1,7 @@
 // engine.cu -- per-GPU DP engine (see engine.hpp).
 #include "engine.hpp"
 #include "kernels.cuh"
+#include "kernels_rt.cuh"
 
 #include <algorithm>
 #include <cmath>
@@ -240,6 +241,12 @@ void Engine::release_template() {
     dfree(e.d_slot_acc);
     dfree(e.d_slot_col);
     dfree(e.d_pinv);
+    dfree(e.d_pmap);
+    dfree(e.d_omap);
+    dfree(e.d_rt_packed);
+    dfree(e.d_rt_split);
+    dfree(e.d_rt_groups);
+    dfree(e.d_rt_blocks);
   }
   exec_.clear();
   dfree(arena_);
@@ -518,10 +525,120 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     }
     e.d_ins = dupload(ins, stream_);
   }
+  setup_rooted_ema(max_smem);
   TCG_CUDA(cudaStreamSynchronize(stream_));
   have_template_ = true;
   if (n_ >= 0) plan_arena();
   tables_valid_ = false;
+}
+
+// relabeled combinadic index of the set cs[0..h) minus color c (colors above
+// c shift down by one), over k-1 colors
+static int64_t relabeled_index(const int* cs, int h, int c) {
+  int t[kMaxK];
+  int m = 0;
+  for (int i = 0; i < h; ++i)
+    if (cs[i] != c) t[m++] = cs[i] < c ? cs[i] : cs[i] - 1;
+  return index_of(t, m);
+}
+
+// Rooted tables everywhere (kernels_rt.cuh): possible when every internal
+// passive child goes through the rooted SpMM and every node's tile fits smem.
+void Engine::setup_rooted_ema(int max_smem) {
+  rooted_ema_ = false;
+  static const int mode = [] {
+    const char* s = std::getenv("TCG_ROOTED_EMA");
+    return s ? std::atoi(s) : 1;
+  }();
+  static const int blocked_mode = [] {
+    const char* s = std::getenv("TCG_EMA_BLOCKED");
+    return s ? std::atoi(s) : 1;
+  }();
+  const int k = plan_.k;
+  if (!mode || exec_.empty() || k < 2) return;
+  const Binom& B = binom();
+  for (const auto& e : exec_) {
+    if ((!e.p_leaf && !e.rooted) || e.lspmm) return;
+    const int64_t Wa = e.a_leaf ? 0 : B(k - 1, e.sa - 1), Wp = B(k - 1, e.sp), Ws = e.root ? 1 : B(k - 1, e.size - 1);
+    if (Wa >= 65536 || Wp >= 65536 || Ws >= 65536) return;
+    if ((Wa + Wp) * (dev::kTileV + 1) * 4 > max_smem - 4096) return;
+  }
+  std::vector<int> parent(plan_.num_nodes, -1);
+  for (size_t i = 0; i < exec_.size(); ++i) {
+    parent[exec_[i].a] = static_cast<int>(i);
+    parent[exec_[i].p] = static_cast<int>(i);
+  }
+  int cs[kMaxK];
+  for (auto& e : exec_) {
+    e.Wa = e.a_leaf ? 0 : static_cast<int32_t>(B(k - 1, e.sa - 1));
+    e.Wp = static_cast<int32_t>(B(k - 1, e.sp));
+    e.Ws = e.root ? 1 : static_cast<int32_t>(B(k - 1, e.size - 1));
+    // P' storage column -> full combinadic column -> relabeled row per color
+    std::vector<int64_t> full_of;
+    if (e.p_leaf) {
+      e.Cpt = k;
+      for (int d = 0; d < k; ++d) full_of.push_back(d);
+    } else {
+      e.Cpt = e.Cps;
+      full_of.assign(static_cast<size_t>(e.Cps), -1);
+      for (int32_t x = 0; x < e.Cp; ++x) full_of[e.rl_perm[x]] = x;
+    }
+    std::vector<int32_t> pm(static_cast<size_t>(k) * e.Cpt, -1);
+    for (int32_t col = 0; col < e.Cpt; ++col) {
+      if (full_of[col] < 0) continue;
+      set_of(k, full_of[col], e.sp, cs);
+      for (int c = 0; c < k; ++c) {
+        if (std::find(cs, cs + e.sp, c) != cs + e.sp) continue;
+        pm[static_cast<size_t>(c) * e.Cpt + col] = static_cast<int32_t>(relabeled_index(cs, e.sp, c));
+      }
+    }
+    e.d_pmap = dupload(pm, stream_);
+    e.omap.clear();
+    if (!e.root) {
+      const NodeExec& par = exec_[parent[e.id]];
+      if (par.p == e.id && par.rooted) {  // feeds the rooted SpMM: its slot layout
+        const RootedLayout rl = build_rooted_layout(k, e.size);
+        e.Cout = rl.groups * rl.zw;
+        e.omap.assign(static_cast<size_t>(k) * e.Ws, -1);
+        const int slots = rl.groups * rl.zw;
+        for (int c = 0; c < k; ++c)
+          for (int i = 0; i < slots; ++i) {
+            const int32_t col = rl.slot_col[static_cast<size_t>(c) * slots + i];
+            if (col < 0) continue;
+            set_of(k, col, e.size, cs);
+            e.omap[static_cast<size_t>(c) * e.Ws + relabeled_index(cs, e.size, c)] = i;
+          }
+        e.d_omap = dupload(e.omap, stream_);
+      } else {
+        e.Cout = e.Ws;
+      }
+    }
+    if (!e.a_leaf) {
+      const SplitTable st = build_split_table(k - 1, e.root ? k - 1 : e.size - 1, e.sa - 1);
+      e.rt_pairs = st.pairs_per_parent;
+      if (e.root) {
+        std::vector<int2> pr(st.active_index.size());
+        for (size_t i = 0; i < pr.size(); ++i) pr[i] = make_int2(st.active_index[i], st.passive_index[i]);
+        e.d_rt_split = dupload(pr, stream_);
+      } else {
+        std::vector<uint32_t> pk(st.active_index.size());
+        for (size_t i = 0; i < pk.size(); ++i)
+          pk[i] = static_cast<uint32_t>(st.active_index[i]) | (static_cast<uint32_t>(st.passive_index[i]) << 16);
+        e.d_rt_packed = dupload(pk, stream_);
+        if (blocked_mode && k - 1 >= dev::kH1 && (e.rt_pairs >= 16 || blocked_mode == 2)) {
+          std::vector<dev::GroupDesc> gr;
+          std::vector<dev::BlockDesc> bl;
+          build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl);
+          e.rt_blocked = true;
+          e.rt_ngroups = static_cast<int>(gr.size());
+          e.d_rt_groups = dupload(gr, stream_);
+          e.d_rt_blocks = dupload(bl, stream_);
+        }
+      }
+    }
+    e.rt_smem = static_cast<size_t>(e.Wa + e.Wp) * (dev::kTileV + 1) * 4;
+  }
+  rooted_ema_ = true;
 }
 
 void Engine::plan_arena() {
@@ -552,12 +669,28 @@ void Engine::plan_arena() {
       throw invalid_argument("graph too large for the rooted-compressed SpMM (ids >= 2^27); set TCG_ROOTED=0");
     rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
     rcut_off_ = ap.alloc(8 * static_cast<int64_t>(n_) * (rooted_parts_ + 1));
+  }
+  vs_off_ = tiles_off_ = vcnt_off_ = -1;
+  max_tiles_ = static_cast<int>((n_ + dev::kTileV - 1) / dev::kTileV) + plan_.k;
+  if (rooted_ema_) {
+    vs_off_ = ap.alloc(4 * std::max<int64_t>(n_, 1));
+    tiles_off_ = ap.alloc(16 * static_cast<int64_t>(max_tiles_));
+    vcnt_off_ = ap.alloc(4 * static_cast<int64_t>((n_ + dev::kVsChunk - 1) / dev::kVsChunk + 1) * plan_.k);
+    dfree(d_tile_tot_);
+    TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * max_tiles_));
+  }
+  if (need_rooted_) {
     const int slots = sched_.at(1)[0].nslots;
     for (auto& e : exec_)
       if (e.rooted) rooted_partial = std::max<int64_t>(rooted_partial, static_cast<int64_t>(slots) * static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / e.rl_zw))));
   }
   for (auto& e : exec_) {
-    if (!e.p_leaf && e.rooted) {
+    if (!e.p_leaf && e.rooted && rooted_ema_) {
+      // M_p is already in the SpMM's compressed slot layout
+      e.pp_off = ap.alloc(table_bytes(e.Cps));
+      pprime_off_[e.p] = e.pp_off;
+      if (!keep) ap.free(table_off_[e.p]);
+    } else if (!e.p_leaf && e.rooted) {
       // compress M_p (alive), drop it, then P' while the compressed table lives
       e.ct_off = ap.alloc(table_bytes(static_cast<int64_t>(e.rl_groups) * e.rl_zw));
       if (!keep) ap.free(table_off_[e.p]);
@@ -587,7 +720,7 @@ void Engine::plan_arena() {
       if (!keep && !e.a_leaf) ap.free(table_off_[e.a]);
       continue;
     }
-    e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(e.Cs));
+    e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(rooted_ema_ ? e.Cout : e.Cs));
     table_off_[e.id] = e.out_off;
     if (!keep) {
       if (!e.p_leaf) ap.free(e.pp_off);
@@ -849,14 +982,14 @@ void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
 // (part, color)-sorted rows, each producing the group's P' columns.
 void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors) {
   const int zw = e.rl_zw, G = e.rl_groups;
-  float* X = table_ptr(e.ct_off);
-  {
+  const float* X = rooted_ema_ ? M : table_ptr(e.ct_off);
+  if (!rooted_ema_) {
     const int rf = static_cast<int>(dev::table_floats(e.Cp, 1));
     const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (96 << 10) / (4 * rf))));
     const size_t smem = static_cast<size_t>(vpb) * rf * 4;
     TCG_CUDA(cudaFuncSetAttribute(dev::rooted_compress, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dev::rooted_compress<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
-        M, e.Cp, d_colors, e.d_slot_col, G, zw, n_, vpb, X);
+        M, e.Cp, d_colors, e.d_slot_col, G, zw, n_, vpb, table_ptr(e.ct_off));
     ++launches_;
   }
   const PartSchedule& ps = sched_.at(1)[0];  // whole rows; parts = color classes
@@ -951,6 +1084,45 @@ static void launch_root(const NodeExec& e, cudaStream_t s, int32_t n, const floa
                                                       n, rout, racc, tile_tot);
 }
 
+// Rooted eMA of one node over the same-color tiles (kernels_rt.cuh).
+void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, double* d_root_acc) {
+  const int32_t* vs = reinterpret_cast<const int32_t*>(arena_ + vs_off_);
+  const int4* tl = reinterpret_cast<const int4*>(arena_ + tiles_off_);
+  const unsigned grid = static_cast<unsigned>(max_tiles_);
+  auto attr = [&](const void* f) {
+    TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_smem)));
+  };
+  if (e.root) {
+    double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
+    if (e.a_leaf) {
+      attr(reinterpret_cast<const void*>(dev::ema_rt_root<true>));
+      dev::ema_rt_root<true><<<grid, dev::kEmaWarps * 32, e.rt_smem, stream_>>>(
+          A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+    } else {
+      attr(reinterpret_cast<const void*>(dev::ema_rt_root<false>));
+      dev::ema_rt_root<false><<<grid, dev::kEmaWarps * 32, e.rt_smem, stream_>>>(
+          A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+    }
+    return;
+  }
+  float* out = table_ptr(e.out_off);
+  const int warps = std::max(2, std::min(dev::kEmaWarps, (e.Ws + 7) / 8));
+  if (e.a_leaf) {
+    attr(reinterpret_cast<const void*>(dev::ema_rt_node<true>));
+    dev::ema_rt_node<true><<<grid, warps * 32, e.rt_smem, stream_>>>(
+        nullptr, 0, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, nullptr, 0, e.Ws, e.d_omap, e.Cout, n_, out);
+  } else if (e.rt_blocked) {
+    attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
+    dev::ema_rt_blocked<<<grid, 256, e.rt_smem, stream_>>>(
+        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+        static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, out);
+  } else {
+    attr(reinterpret_cast<const void*>(dev::ema_rt_node<false>));
+    dev::ema_rt_node<false><<<grid, warps * 32, e.rt_smem, stream_>>>(
+        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.Cout, n_, out);
+  }
+}
+
 // ---------------------------------------------------------------- one DP
 void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_acc,
                     tcg_node_stats* stats) {
@@ -1008,6 +1180,19 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
   }
+  if (rooted_ema_ && n_ > 0) {
+    // vertices sorted by color into same-color tiles for the rooted eMA
+    size_t b0 = 0;
+    if (prof_) { b0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+    const int nchunks = static_cast<int>((n_ + dev::kVsChunk - 1) / dev::kVsChunk);
+    int* vcnt = reinterpret_cast<int*>(arena_ + vcnt_off_);
+    dev::vsort_count<<<nchunks, 256, 0, stream_>>>(d_colors, n_, plan_.k, vcnt);
+    dev::vsort_scan<<<1, 256, 0, stream_>>>(vcnt, nchunks, plan_.k, reinterpret_cast<int4*>(arena_ + tiles_off_), max_tiles_);
+    dev::vsort_scatter<<<nchunks, 256, 0, stream_>>>(d_colors, n_, plan_.k, vcnt, reinterpret_cast<int32_t*>(arena_ + vs_off_));
+    launches_ += 3;
+    TCG_CUDA(cudaGetLastError());
+    if (prof_) { prof_->ema.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
+  }
   struct Marks { size_t t0, t1, t2; };
   std::vector<Marks> marks;
   for (auto& e : exec_) {
@@ -1039,7 +1224,11 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     size_t q0 = 0;
     if (prof_) { q0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
-    if (n_ > 0) {
+    if (n_ > 0 && rooted_ema_) {
+      launch_rt_ema(e, A, P, d_root_acc);
+      ++launches_;
+      TCG_CUDA(cudaGetLastError());
+    } else if (n_ > 0) {
       const unsigned vgrid = static_cast<unsigned>(std::min<int64_t>(n_, 148 * 16));
       if (e.vtx) {
         auto smem_attr = [&](const void* f) {
@@ -1097,7 +1286,9 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   if (n_ > 0 && !exec_.empty()) {
-    if (exec_.back().vtx)  // vertex-per-CTA root wrote per-vertex values only
+    if (rooted_ema_)
+      dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, max_tiles_, d_total);
+    else if (exec_.back().vtx)  // vertex-per-CTA root wrote per-vertex values only
       dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
                                                 n_, d_total);
     else
@@ -1359,6 +1550,34 @@ void Engine::node_table(int id, int which, double* out) {
   }
   const int64_t off = which == 0 ? table_off_[id] : pprime_off_[id];
   if (off < 0) throw invalid_argument("table not available for this node");
+  if (which == 0 && rooted_ema_) {
+    // rooted table (RR or the SpMM slot layout): expand to the full C(k,s)
+    // columns, zero wherever the set misses the vertex's color
+    for (const auto& e : exec_) {
+      if (e.id != id) continue;
+      const int s = plan_.size[id];
+      std::vector<float> t(dev::table_floats(e.Cout, n));
+      copy_sync(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost);
+      std::vector<int64_t> rel(static_cast<size_t>(C) * k, -1);  // [S][c] relabeled index or -1
+      int cs[kMaxK];
+      for (int64_t S = 0; S < C; ++S) {
+        set_of(plan_.k, S, s, cs);
+        for (int j = 0; j < s; ++j) rel[static_cast<size_t>(S) * k + cs[j]] = relabeled_index(cs, s, cs[j]);
+      }
+      for (int64_t v = 0; v < n; ++v) {
+        const int c = last_colors_[v];
+        for (int64_t S = 0; S < C; ++S) {
+          const int64_t j = rel[static_cast<size_t>(S) * k + c];
+          double x = 0.0;
+          if (j >= 0)
+            x = e.omap.empty() ? t[dev::panel_offset(e.Cout, n, v, j)]
+                               : t[dev::panel_offset(e.Cout, n, v, e.omap[static_cast<size_t>(c) * e.Ws + j])];
+          out[v * C + S] = x;
+        }
+      }
+      return;
+    }
+  }
   if (which == 1) {
     for (const auto& e : exec_)
       if (e.p == id && e.rooted) {  // group-major P': storage column perm[S]

@@ -62,6 +62,23 @@ struct NodeExec {
   int32_t* d_pinv = nullptr;      // [Cps] storage column -> combinadic column (blocked eMA staging)
   int64_t ct_off = -1;            // arena offset of the compressed passive table
   size_t rooted_smem = 0;         // spmm_rooted dynamic smem
+  // rooted eMA (kernels_rt.cuh): same-color vertex tiles of the (k-1)-color
+  // problem (s-1, a-1, p); tables stored rooted (RR) or in the parent SpMM's
+  // slot layout (RS, passive children)
+  int32_t Wa = 0, Wp = 0, Ws = 0; // A columns (RR), staged P rows, relabeled output columns
+  int32_t Cout = 0;               // output table columns (Ws for RR, groups * zw for RS)
+  int32_t Cpt = 0;                // P' storage columns (hist: k)
+  int32_t* d_pmap = nullptr;      // [k][Cpt] P' storage column -> staged row, or -1
+  int32_t* d_omap = nullptr;      // [k][Ws] relabeled output column -> slot (RS only)
+  std::vector<int32_t> omap;      // host copy (node_table expansion)
+  uint32_t* d_rt_packed = nullptr;
+  int2* d_rt_split = nullptr;     // root
+  int rt_pairs = 0;
+  bool rt_blocked = false;
+  void* d_rt_groups = nullptr;
+  void* d_rt_blocks = nullptr;
+  int rt_ngroups = 0;
+  size_t rt_smem = 0;
 };
 
 // SpMM work schedule for one vertex-range part of the gather source.
@@ -195,6 +212,11 @@ class Engine {
   int64_t rcol_off_ = -1;            // per-coloring color-sorted packed CSR
   int64_t rcut_off_ = -1;            // per-coloring part (color class) cuts, n * (parts + 1)
   void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors);
+  bool rooted_ema_ = false;          // every table rooted; eMA on same-color vertex tiles
+  int max_tiles_ = 0;                // ceil(n / 32) + k
+  int64_t vs_off_ = -1, tiles_off_ = -1, vcnt_off_ = -1;  // per-coloring vertex sort
+  void setup_rooted_ema(int max_smem);
+  void launch_rt_ema(const NodeExec& e, const float* A, const float* P, double* d_root_acc);
   std::vector<int64_t> table_off_;   // per node id: arena offset of its table (internal)
   std::vector<int64_t> pprime_off_;  // per node id: offset of P' computed from it
   char* arena_ = nullptr;

@@ -1,0 +1,356 @@
+// kernels_rt.cuh -- eMA over ROOTED tables (same-color vertex tiles).
+//
+// Every non-root table M_x[v,S] is zero unless S contains color(v) (the root
+// of T_x sits on v).  With v's color c fixed, the eMA of a node (s, a, p) is
+// the eMA of the (k-1)-color problem (s-1, a-1, p): output S' = S minus c,
+// active Sa' = Sa minus c, passive Sp (which never contains c), all indexed
+// by the combinadic of the colors relabeled to [0, k-1) ("relabeled index").
+// Vertices are sorted by color once per coloring (vsort_*), so a 32-vertex
+// tile shares c and every lane runs the same split pairs:
+//   * the active table is stored ROOTED (RR): column j = relabeled index of
+//     S minus c (C(k-1, s-1) columns) -- staged as is;
+//   * P' (full, or group-major from the rooted SpMM) is staged through a
+//     per-color map: storage column -> relabeled index, or -1 when it
+//     contains c (those values are never used);
+//   * the output is RR, or -- for a passive child feeding the rooted SpMM --
+//     the SpMM's slot layout (RS) through a per-color output map.
+// FMAs drop to a/k of the full-table eMA, table bytes to s/k.
+#pragma once
+
+namespace tcg {
+namespace dev {
+
+// ----------------------------------------------- per-coloring vertex sort
+constexpr int kVsChunk = 4096;  // vertices per CTA
+
+__global__ void __launch_bounds__(256)
+vsort_count(const uint8_t* __restrict__ colors, int32_t n, int k, int* __restrict__ cnt) {
+  __shared__ int h[32];
+  if (threadIdx.x < 32) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * kVsChunk;
+  for (int i = threadIdx.x; i < kVsChunk; i += blockDim.x) {
+    const int64_t v = b + i;
+    if (v < n) atomicAdd(&h[colors[v]], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < k) cnt[blockIdx.x * k + threadIdx.x] = h[threadIdx.x];
+}
+
+// One CTA: per-(chunk, color) offsets (color-major, chunk order) in place,
+// and the tile table: tile t = {color, first sorted position, count}, tiles
+// numbered color by color; unused entries get color -1.
+__global__ void __launch_bounds__(256)
+vsort_scan(int* __restrict__ cnt, int nchunks, int k, int4* __restrict__ tiles, int max_tiles) {
+  __shared__ int tot[32], start[33], tstart[33];
+  const int c = threadIdx.x;
+  if (c < k) {
+    int t = 0;
+    for (int b = 0; b < nchunks; ++b) t += cnt[b * k + c];
+    tot[c] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    start[0] = tstart[0] = 0;
+    for (int q = 0; q < k; ++q) {
+      start[q + 1] = start[q] + tot[q];
+      tstart[q + 1] = tstart[q] + (tot[q] + 31) / 32;
+    }
+  }
+  __syncthreads();
+  if (c < k) {
+    int run = start[c];
+    for (int b = 0; b < nchunks; ++b) {
+      const int x = cnt[b * k + c];
+      cnt[b * k + c] = run;
+      run += x;
+    }
+  }
+  for (int t = threadIdx.x; t < max_tiles; t += blockDim.x) {
+    int cc = -1;
+    for (int q = 0; q < k; ++q)
+      if (t >= tstart[q] && t < tstart[q + 1]) cc = q;
+    if (cc < 0) {
+      tiles[t] = make_int4(-1, 0, 0, 0);
+    } else {
+      const int s0 = start[cc] + 32 * (t - tstart[cc]);
+      tiles[t] = make_int4(cc, s0, min(32, start[cc + 1] - s0), 0);
+    }
+  }
+}
+
+// Stable scatter: warp w of a chunk owns 512 consecutive vertices.
+__global__ void __launch_bounds__(256)
+vsort_scatter(const uint8_t* __restrict__ colors, int32_t n, int k, const int* __restrict__ off,
+              int32_t* __restrict__ sorted) {
+  __shared__ int wc[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned lt = (1u << lane) - 1u;
+  const int64_t b = static_cast<int64_t>(blockIdx.x) * kVsChunk + warp * (kVsChunk / 8);
+  wc[warp][lane] = 0;
+  __syncwarp();
+  for (int i = 0; i < kVsChunk / 8; i += 32) {
+    const int64_t v = b + i + lane;
+    const int c = v < n ? colors[v] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, c);
+    if (c >= 0 && (same & lt) == 0) wc[warp][c] += __popc(same);
+    __syncwarp();
+  }
+  __syncthreads();
+  if (threadIdx.x < k) {  // warp-major prefix per color, plus the chunk offset
+    int run = off[blockIdx.x * k + threadIdx.x];
+    for (int w = 0; w < 8; ++w) {
+      const int x = wc[w][threadIdx.x];
+      wc[w][threadIdx.x] = run;
+      run += x;
+    }
+  }
+  __syncthreads();
+  for (int i = 0; i < kVsChunk / 8; i += 32) {
+    const int64_t v = b + i + lane;
+    const int c = v < n ? colors[v] : -1;
+    const unsigned same = __match_any_sync(0xffffffffu, c);
+    const int pos = c >= 0 ? wc[warp][c] + __popc(same & lt) : 0;
+    __syncwarp();
+    if (c >= 0) {
+      sorted[pos] = static_cast<int32_t>(v);
+      if ((same & lt) == 0) wc[warp][c] += __popc(same);
+    }
+    __syncwarp();
+  }
+}
+
+// Stage the rows of the (up to 32) tile vertices of a panel table with C
+// storage columns into smem [row][kSpitch] (lane = vertex).  map (nullable):
+// storage column -> smem row, or -1 to drop.  Missing vertices stage zeros.
+template <int kStageU>
+__device__ __forceinline__ void stage_rows(const float* __restrict__ T, int C, int32_t n,
+                                           const int32_t* __restrict__ vids, float* dst,
+                                           const int32_t* __restrict__ map) {
+  const int panels = num_panels(C);
+  const int zl = last_panel_width(C);
+  const int full4 = (panels - 1) * kTileV * (kZ / 4);
+  const int total4 = full4 + kTileV * (zl / 4);
+  for (int base = threadIdx.x; base < total4; base += blockDim.x * kStageU) {
+    float4 x[kStageU];
+    int c0[kStageU], vv[kStageU];
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int f = base + u * blockDim.x;
+      int p, r, zw;
+      if (f < full4) { p = f / (kTileV * 8); r = f % (kTileV * 8); zw = kZ; }
+      else { p = panels - 1; r = f - full4; zw = zl; }
+      const int q4 = zw / 4;
+      vv[u] = r / q4;
+      c0[u] = p * kZ + (r % q4) * 4;
+      x[u] = make_float4(0, 0, 0, 0);
+      const int v = f < total4 ? vids[vv[u]] : -1;
+      if (v >= 0 && c0[u] < C)
+        x[u] = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + static_cast<int64_t>(v) * zw + (r % q4) * 4));
+      if (f >= total4) c0[u] = C;
+    }
+#pragma unroll
+    for (int u = 0; u < kStageU; ++u) {
+      const int c = c0[u];
+      if (c >= C) continue;
+      if (map) {
+        const int4 m = make_int4(__ldg(map + c), c + 1 < C ? __ldg(map + c + 1) : -1,
+                                 c + 2 < C ? __ldg(map + c + 2) : -1, c + 3 < C ? __ldg(map + c + 3) : -1);
+        if (m.x >= 0) dst[m.x * kSpitch + vv[u]] = x[u].x;
+        if (m.y >= 0) dst[m.y * kSpitch + vv[u]] = x[u].y;
+        if (m.z >= 0) dst[m.z * kSpitch + vv[u]] = x[u].z;
+        if (m.w >= 0) dst[m.w * kSpitch + vv[u]] = x[u].w;
+      } else {
+        dst[(c + 0) * kSpitch + vv[u]] = x[u].x;
+        if (c + 1 < C) dst[(c + 1) * kSpitch + vv[u]] = x[u].y;
+        if (c + 2 < C) dst[(c + 2) * kSpitch + vv[u]] = x[u].z;
+        if (c + 3 < C) dst[(c + 3) * kSpitch + vv[u]] = x[u].w;
+      }
+    }
+  }
+}
+
+// Output of 8 consecutive relabeled columns [c0, c0+8) of vertex v: RR (omap
+// null: the table has Ws columns, written as two float4) or RS (column ->
+// slot through omap, table of Cout columns).
+__device__ __forceinline__ void rt_write8(float* __restrict__ out, int Ws, int Cout, const int32_t* __restrict__ omap,
+                                          int32_t n, int64_t v, int c0, const float (&r)[8]) {
+  if (!omap) {
+    const int zw = panel_width(Ws, c0 / kZ);
+    float* dst = out + static_cast<int64_t>(c0 / kZ) * n * kZ + v * zw + (c0 % kZ);
+    if (c0 + 4 <= Ws || (c0 % kZ) + 4 <= zw) reinterpret_cast<float4*>(dst)[0] = make_float4(r[0], r[1], r[2], r[3]);
+    if ((c0 % kZ) + 8 <= zw) reinterpret_cast<float4*>(dst)[1] = make_float4(r[4], r[5], r[6], r[7]);
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (c0 + j < Ws) out[panel_offset(Cout, n, v, __ldg(omap + c0 + j))] = r[j];
+  }
+}
+
+// Generic node (and the active-leaf copy) on a same-color tile.  Warp w
+// computes chunks of 8 output columns for the tile's 32 vertices.
+template <bool ALEAF>
+__global__ void __launch_bounds__(kEmaWarps * 32)
+ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
+            const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
+            const int4* __restrict__ tiles, const uint32_t* __restrict__ packed, int pairs, int Ws,
+            const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  __shared__ int32_t vids[32];
+  const int4 tile = tiles[blockIdx.x];
+  if (tile.x < 0) return;
+  const int c = tile.x;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (threadIdx.x < 32) vids[threadIdx.x] = static_cast<int>(threadIdx.x) < tile.z ? vsorted[tile.y + threadIdx.x] : -1;
+  __syncthreads();
+  float* sA = smem;
+  float* sP = smem + (ALEAF ? 0 : Wa * kSpitch);
+  if (!ALEAF) stage_rows<1>(Am, Wa, n, vids, sA, nullptr);
+  stage_rows<1>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
+  __syncthreads();
+  const int64_t v = vids[lane];
+  const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
+  const int nchunks = (Ws + 7) / 8;
+  for (int q = warp; q < nchunks; q += blockDim.x >> 5) {
+    float r[8];
+    if (ALEAF) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = q * 8 + j < Ws ? sP[(q * 8 + j) * kSpitch + lane] : 0.f;
+    } else {
+      const int nv = min(8, Ws - q * 8);
+      const uint32_t* sp = packed + static_cast<int64_t>(q) * 8 * pairs;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = 0.f;
+      for (int pb = 0; pb < pairs; pb += 32) {
+        uint32_t w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) w[j] = (j < nv && pb + lane < pairs) ? __ldg(sp + j * pairs + pb + lane) : 0u;
+        const int cnt = min(32, pairs - pb);
+        for (int pp = 0; pp < cnt; ++pp) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const uint32_t s = __shfl_sync(0xffffffffu, w[j], pp);
+            r[j] = fmaf(sA[(s & 0xFFFFu) * kSpitch + lane], sP[(s >> 16) * kSpitch + lane], r[j]);
+          }
+        }
+      }
+    }
+    if (v >= 0) rt_write8(out, Ws, Cout, om, n, v, q * 8, r);
+  }
+}
+
+// Register-blocked eMA (see ema_blocked) on a same-color tile of the (k-1)
+// problem; descriptors from build_blocked(k-1, s-1, a-1).
+#define TCG_IJR(I, J) \
+  case I * 8 + J: micro_block<I, J>(sA + bd.a_off * kSpitch + lane, sP + bd.p_off * kSpitch + lane, acc); break;
+
+__global__ void __launch_bounds__(256)
+ema_rt_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
+               const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
+               const int4* __restrict__ tiles, const GroupDesc* __restrict__ groups, int ngroups,
+               const BlockDesc* __restrict__ blocks, int Ws, const int32_t* __restrict__ omap, int Cout,
+               int32_t n, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  __shared__ int next_group;
+  __shared__ int32_t vids[32];
+  const int4 tile = tiles[blockIdx.x];
+  if (tile.x < 0) return;
+  const int c = tile.x;
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32) vids[threadIdx.x] = static_cast<int>(threadIdx.x) < tile.z ? vsorted[tile.y + threadIdx.x] : -1;
+  if (threadIdx.x == 0) next_group = blockDim.x / 32;
+  __syncthreads();
+  float* sA = smem;
+  float* sP = smem + Wa * kSpitch;
+  stage_rows<8>(Am, Wa, n, vids, sA, nullptr);
+  stage_rows<8>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
+  __syncthreads();
+  const int64_t v = vids[lane];
+  const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
+  for (int gi = threadIdx.x >> 5; gi < ngroups;) {
+    const GroupDesc gd = groups[gi];
+    float acc[kMaxAcc];
+#pragma unroll
+    for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
+    for (int b = gd.b0; b < gd.b1; ++b) {
+      const BlockDesc bd = blocks[b];
+      switch (bd.ij) {
+        TCG_IJR(0, 1) TCG_IJR(0, 2) TCG_IJR(0, 3) TCG_IJR(0, 4) TCG_IJR(0, 5) TCG_IJR(0, 6)
+        TCG_IJR(1, 0) TCG_IJR(1, 1) TCG_IJR(1, 2) TCG_IJR(1, 3) TCG_IJR(1, 4) TCG_IJR(1, 5)
+        TCG_IJR(2, 0) TCG_IJR(2, 1) TCG_IJR(2, 2) TCG_IJR(2, 3) TCG_IJR(2, 4)
+        TCG_IJR(3, 0) TCG_IJR(3, 1) TCG_IJR(3, 2) TCG_IJR(3, 3)
+        TCG_IJR(4, 0) TCG_IJR(4, 1) TCG_IJR(4, 2)
+        TCG_IJR(5, 0) TCG_IJR(5, 1)
+        TCG_IJR(6, 0) TCG_IJR(0, 0)
+        default: break;
+      }
+    }
+    if (v >= 0) {
+      const int cnt = cbin(kH1, gd.s1);
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x)
+        if (x < cnt) {
+          const int col = gd.out_off + x;
+          out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
+        }
+    }
+    if (lane == 0) gi = atomicAdd(&next_group, 1);
+    gi = __shfl_sync(0xffffffffu, gi, 0);
+  }
+}
+#undef TCG_IJR
+
+// Root on a same-color tile: fp64 dot product over the C(k-1, a-1) splits of
+// the (k-1) colors (ALEAF: the single P value).  Per-vertex totals to
+// root_out[v]; fixed-order per-tile totals (0 for unused tiles).
+template <bool ALEAF>
+__global__ void __launch_bounds__(kEmaWarps * 32)
+ema_rt_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
+            const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
+            const int4* __restrict__ tiles, const int2* __restrict__ split, int pairs, int32_t n,
+            double* __restrict__ root_out, double* __restrict__ root_acc, double* __restrict__ tile_tot) {
+  extern __shared__ float smem[];
+  __shared__ double red[kEmaWarps][kTileV];
+  __shared__ int32_t vids[32];
+  const int4 tile = tiles[blockIdx.x];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (tile.x < 0) {
+    if (threadIdx.x == 0) tile_tot[blockIdx.x] = 0.0;
+    return;
+  }
+  const int c = tile.x;
+  if (threadIdx.x < 32) vids[threadIdx.x] = static_cast<int>(threadIdx.x) < tile.z ? vsorted[tile.y + threadIdx.x] : -1;
+  __syncthreads();
+  float* sA = smem;
+  float* sP = smem + (ALEAF ? 0 : Wa * kSpitch);
+  if (!ALEAF) stage_rows<1>(Am, Wa, n, vids, sA, nullptr);
+  stage_rows<1>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
+  __syncthreads();
+  double acc = 0;
+  if (ALEAF) {
+    if (warp == 0) acc = static_cast<double>(sP[lane]);
+  } else {
+    for (int p = warp; p < pairs; p += kEmaWarps) {
+      const int2 s = __ldg(split + p);
+      acc = fma(static_cast<double>(sA[s.x * kSpitch + lane]), static_cast<double>(sP[s.y * kSpitch + lane]), acc);
+    }
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double tot = 0;
+    for (int w = 0; w < kEmaWarps; ++w) tot += red[w][lane];
+    const int v = vids[lane];
+    if (v >= 0) {
+      root_out[v] = tot;
+      if (root_acc) root_acc[v] += tot;
+    } else {
+      tot = 0;
+    }
+    for (int o = 16; o; o >>= 1) tot += __shfl_down_sync(0xffffffffu, tot, o);
+    if (lane == 0) tile_tot[blockIdx.x] = tot;
+  }
+}
+
+}  // namespace dev
+}  // namespace tcg

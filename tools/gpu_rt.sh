@@ -1,0 +1,8 @@
+set -x
+mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -15
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -2
+timeout 300 python tools/prof_driver.py --config cfg3 --stats 2>&1 | tail -14
+timeout 300 python tools/prof_driver.py --config cfg2 --colorings 5 --stats 2>&1 | tail -8
+timeout 600 python -m pytest tests/test_sharded.py -x -q -m gpu 2>&1 | tail -3
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_rt_cfg3.csv python tools/prof_driver.py --config cfg3 --warmup 0 --colorings 1 > /dev/null 2>&1
