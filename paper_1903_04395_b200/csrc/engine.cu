@@ -1155,7 +1155,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
           need_hist_ ? table_ptr(hist_off_) : nullptr, dev::panel_width(plan_.k, 0), d_counter_);
       ++launches_;
       TCG_CUDA(cudaGetLastError());
-    } else {
+    } else if (!need_rooted_) {  // (with the rooted SpMM, bucket_rows writes it)
       hist(d_gcolors, table_ptr(hist_off_));
     }
     if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
@@ -1169,13 +1169,16 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     const size_t smem = sizeof(int) * 8 * plan_.k, lsmem = sizeof(int) * 9 * plan_.k;
     uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
     int64_t* cuts = reinterpret_cast<int64_t*>(arena_ + rcut_off_);
+    // the bucketing counts ARE the neighbour color histogram: fused
+    float* hf = need_hist_ ? table_ptr(hist_off_) : nullptr;
+    const int hzw = dev::panel_width(plan_.k, 0);
     if (nlong_ > 0) {
       dev::bucket_long<<<static_cast<unsigned>(nlong_), 256, lsmem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_,
-                                                                                plan_.k, rooted_parts_, rc, cuts);
+                                                                                plan_.k, rooted_parts_, rc, cuts, hf, hzw);
       ++launches_;
     }
     dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, n_, plan_.k,
-                                                     rooted_parts_, rc, cuts);
+                                                     rooted_parts_, rc, cuts, hf, hzw);
     ++launches_;
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }

@@ -455,7 +455,8 @@ constexpr int kBucketLong = 1024;  // rows above this go to bucket_long (CTA per
 __global__ void __launch_bounds__(256)
 bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
             const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t row0,
-            int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts) {
+            int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
+            float* __restrict__ hist, int hzw) {
   extern __shared__ int bsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   int* cnt = bsm + warp * k;
@@ -468,6 +469,12 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     for (int i = lane; i < k; i += 32) cnt[i] = 0;
     __syncwarp();
     auto write_cuts = [&]() {
+      // the exact neighbour color histogram (the P' of a leaf passive child)
+      // is the per-color count: cnt[c+1] - cnt[c] after the scan
+      if (hist && lane < hzw) {
+        const int hi = lane + 1 < k ? cnt[lane + 1] : d;
+        hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(hi - cnt[lane]) : 0.f;
+      }
       if (lane <= nparts) {
         const int cb = lane * k / nparts;
         cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + (cb < k ? cnt[cb] : d);
@@ -534,7 +541,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
 __global__ void __launch_bounds__(256)
 bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
             const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int k, int nparts,
-            uint32_t* __restrict__ out, int64_t* __restrict__ cuts) {
+            uint32_t* __restrict__ out, int64_t* __restrict__ cuts, float* __restrict__ hist, int hzw) {
   extern __shared__ int bsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   int* cnt = bsm + warp * k;
@@ -561,6 +568,8 @@ bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
   }
   __syncthreads();
   if (warp == 0) {
+    if (hist && lane < hzw) hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(tot[lane]) : 0.f;
+    __syncwarp();
     warp_exclusive_scan(tot, k, lane);
     if (lane <= nparts) {
       const int cb = lane * k / nparts;
