@@ -114,6 +114,13 @@ void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
   groups.clear();
   blocks.clear();
   for (auto& g : gs) {
+    // pad of a run's first block = the run's length (runs of one (i, j) pattern)
+    for (size_t b = 0; b < g.b.size();) {
+      size_t e = b;
+      while (e < g.b.size() && g.b[e].ij == g.b[b].ij) ++e;
+      for (size_t q = b; q < e; ++q) g.b[q].pad = static_cast<int32_t>(q == b ? e - b : 0);
+      b = e;
+    }
     g.d.b0 = static_cast<int32_t>(blocks.size());
     blocks.insert(blocks.end(), g.b.begin(), g.b.end());
     g.d.b1 = static_cast<int32_t>(blocks.size());
@@ -242,6 +249,7 @@ void Engine::release_template() {
     dfree(e.d_slot_col);
     dfree(e.d_pinv);
     dfree(e.d_pmap);
+    dfree(e.d_cmap);
     dfree(e.d_omap);
     dfree(e.d_rt_packed);
     dfree(e.d_rt_split);
@@ -612,6 +620,22 @@ void Engine::setup_rooted_ema(int max_smem) {
       } else {
         e.Cout = e.Ws;
       }
+    }
+    if (e.a_leaf && !e.root) {
+      // active leaf: output column -> P' storage column of (S minus c), per color
+      std::vector<int32_t> cm(static_cast<size_t>(k) * e.Cout, -1);
+      std::vector<int32_t> storage_of(e.Cp);
+      for (int32_t x = 0; x < e.Cp; ++x) storage_of[x] = e.p_leaf ? x : e.rl_perm[x];
+      int t[kMaxK];
+      for (int c = 0; c < k; ++c)
+        for (int32_t j = 0; j < e.Ws; ++j) {
+          set_of(k - 1, j, e.size - 1, t);
+          for (int q = 0; q < e.size - 1; ++q) t[q] = t[q] >= c ? t[q] + 1 : t[q];
+          const int32_t src = storage_of[index_of(t, e.size - 1)];
+          const int32_t i = e.omap.empty() ? j : e.omap[static_cast<size_t>(c) * e.Ws + j];
+          if (i >= 0) cm[static_cast<size_t>(c) * e.Cout + i] = src;
+        }
+      e.d_cmap = dupload(cm, stream_);
     }
     if (!e.a_leaf) {
       const SplitTable st = build_split_table(k - 1, e.root ? k - 1 : e.size - 1, e.sa - 1);
@@ -1108,9 +1132,12 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   float* out = table_ptr(e.out_off);
   const int warps = std::max(2, std::min(dev::kEmaWarps, (e.Ws + 7) / 8));
   if (e.a_leaf) {
-    attr(reinterpret_cast<const void*>(dev::ema_rt_node<true>));
-    dev::ema_rt_node<true><<<grid, warps * 32, e.rt_smem, stream_>>>(
-        nullptr, 0, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, nullptr, 0, e.Ws, e.d_omap, e.Cout, n_, out);
+    const int rf = static_cast<int>(dev::table_floats(e.Cpt, 1));
+    const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (48 << 10) / (4 * rf))));
+    const size_t smem = static_cast<size_t>(vpb) * rf * 4;
+    TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
+        P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, out);
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
     dev::ema_rt_blocked<<<grid, 256, e.rt_smem, stream_>>>(
@@ -1183,6 +1210,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
   }
+  d_colors_rt_ = d_colors;
   if (rooted_ema_ && n_ > 0) {
     // vertices sorted by color into same-color tiles for the rooted eMA
     size_t b0 = 0;

@@ -70,6 +70,7 @@ struct NodeExec {
   int32_t Cpt = 0;                // P' storage columns (hist: k)
   int32_t* d_pmap = nullptr;      // [k][Cpt] P' storage column -> staged row, or -1
   int32_t* d_omap = nullptr;      // [k][Ws] relabeled output column -> slot (RS only)
+  int32_t* d_cmap = nullptr;      // active leaf: [k][Cout] output column -> P' storage column
   std::vector<int32_t> omap;      // host copy (node_table expansion)
   uint32_t* d_rt_packed = nullptr;
   int2* d_rt_split = nullptr;     // root
@@ -214,6 +215,7 @@ class Engine {
   void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors);
   bool rooted_ema_ = false;          // every table rooted; eMA on same-color vertex tiles
   int max_tiles_ = 0;                // ceil(n / 32) + k
+  const uint8_t* d_colors_rt_ = nullptr;  // this context's row colors during run_dp
   int64_t vs_off_ = -1, tiles_off_ = -1, vcnt_off_ = -1;  // per-coloring vertex sort
   void setup_rooted_ema(int max_smem);
   void launch_rt_ema(const NodeExec& e, const float* A, const float* P, double* d_root_acc);

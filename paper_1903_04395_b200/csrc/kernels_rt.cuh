@@ -131,22 +131,23 @@ __device__ __forceinline__ void stage_rows(const float* __restrict__ T, int C, i
   const int zl = last_panel_width(C);
   const int full4 = (panels - 1) * kTileV * (kZ / 4);
   const int total4 = full4 + kTileV * (zl / 4);
+  const int lq_last = zl == 32 ? 3 : (zl == 16 ? 2 : 1);  // log2(float4s per row) of the last panel
   for (int base = threadIdx.x; base < total4; base += blockDim.x * kStageU) {
     float4 x[kStageU];
     int c0[kStageU], vv[kStageU];
 #pragma unroll
     for (int u = 0; u < kStageU; ++u) {
       const int f = base + u * blockDim.x;
-      int p, r, zw;
-      if (f < full4) { p = f / (kTileV * 8); r = f % (kTileV * 8); zw = kZ; }
-      else { p = panels - 1; r = f - full4; zw = zl; }
-      const int q4 = zw / 4;
-      vv[u] = r / q4;
-      c0[u] = p * kZ + (r % q4) * 4;
+      int p, r, lq;
+      if (f < full4) { p = f >> 8; r = f & 255; lq = 3; }  // kTileV * 8 float4s per full panel tile
+      else { p = panels - 1; r = f - full4; lq = lq_last; }
+      vv[u] = r >> lq;
+      const int q = r & ((1 << lq) - 1);
+      c0[u] = p * kZ + q * 4;
       x[u] = make_float4(0, 0, 0, 0);
       const int v = f < total4 ? vids[vv[u]] : -1;
       if (v >= 0 && c0[u] < C)
-        x[u] = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + static_cast<int64_t>(v) * zw + (r % q4) * 4));
+        x[u] = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + (static_cast<int64_t>(v) << (lq + 2)) + q * 4));
       if (f >= total4) c0[u] = C;
     }
 #pragma unroll
@@ -239,10 +240,57 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   }
 }
 
+// Active-leaf node: M_s[v,S] = P'[v, S minus c] -- a per-color column
+// permutation of the vertex's P' row: out[v, i] = P'[v, cmap[c][i]] (0 where
+// -1).  A CTA stages the full P' rows of `vpb` consecutive vertices in smem
+// (coalesced 128 B panel rows), then writes the output rows panel by panel
+// (coalesced as well).  Natural vertex order, no tiles.
+__global__ void __launch_bounds__(256)
+ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ colors,
+            const int32_t* __restrict__ cmap, int Cout, int32_t n, int vpb, float* __restrict__ out) {
+  extern __shared__ float crow[];
+  const int pin = num_panels(Cpt), zin = last_panel_width(Cpt);
+  const int rf = (pin - 1) * kZ + zin;
+  const int per = rf / 4;
+  const int64_t u0 = static_cast<int64_t>(blockIdx.x) * vpb;
+  for (int f = threadIdx.x; f < vpb * per; f += blockDim.x) {
+    const int r = f / per, c4 = (f % per) * 4;
+    const int64_t u = u0 + r;
+    if (u >= n) continue;
+    const int p = c4 >> 5, z = c4 & 31;
+    const int zp = p == pin - 1 ? zin : kZ;
+    *reinterpret_cast<float4*>(crow + r * rf + c4) =
+        __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+  }
+  __syncthreads();
+  const int pout = num_panels(Cout), zout = last_panel_width(Cout);
+  const int rout = (pout - 1) * kZ + zout;  // floats per output row (panel-padded)
+  for (int i = threadIdx.x; i < vpb * rout; i += blockDim.x) {
+    // (panel, vertex, slot) order: consecutive threads write one 128 B panel row
+    const int p = i / (vpb * kZ);
+    const int zp = p == pout - 1 ? zout : kZ;
+    const int rem = i - p * vpb * kZ;
+    if (rem >= vpb * zp) continue;
+    const int r = rem / zp, t = rem % zp;
+    const int64_t u = u0 + r;
+    if (u >= n) continue;
+    const int col = p * kZ + t;
+    const int src = col < Cout ? __ldg(cmap + static_cast<int64_t>(colors[u]) * Cout + col) : -1;
+    out[static_cast<int64_t>(p) * n * kZ + u * zp + t] = src >= 0 ? crow[r * rf + src] : 0.f;
+  }
+}
+
 // Register-blocked eMA (see ema_blocked) on a same-color tile of the (k-1)
 // problem; descriptors from build_blocked(k-1, s-1, a-1).
-#define TCG_IJR(I, J) \
-  case I * 8 + J: micro_block<I, J>(sA + bd.a_off * kSpitch + lane, sP + bd.p_off * kSpitch + lane, acc); break;
+// blocks of a group are sorted by pattern; BlockDesc.pad of a run's first
+// block holds the run length, so the pattern dispatch happens once per run
+#define TCG_IJR(I, J)                                                                       \
+  case I * 8 + J:                                                                           \
+    for (int q = 0; q < len; ++q) {                                                         \
+      const BlockDesc bd = q == 0 ? h : blocks[b + q];                                      \
+      micro_block<I, J>(sA + bd.a_off * kSpitch + lane, sP + bd.p_off * kSpitch + lane, acc); \
+    }                                                                                       \
+    break;
 
 __global__ void __launch_bounds__(256)
 ema_rt_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
@@ -272,9 +320,10 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ P
     float acc[kMaxAcc];
 #pragma unroll
     for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
-    for (int b = gd.b0; b < gd.b1; ++b) {
-      const BlockDesc bd = blocks[b];
-      switch (bd.ij) {
+    for (int b = gd.b0; b < gd.b1;) {
+      const BlockDesc h = blocks[b];
+      const int len = h.pad;
+      switch (h.ij) {
         TCG_IJR(0, 1) TCG_IJR(0, 2) TCG_IJR(0, 3) TCG_IJR(0, 4) TCG_IJR(0, 5) TCG_IJR(0, 6)
         TCG_IJR(1, 0) TCG_IJR(1, 1) TCG_IJR(1, 2) TCG_IJR(1, 3) TCG_IJR(1, 4) TCG_IJR(1, 5)
         TCG_IJR(2, 0) TCG_IJR(2, 1) TCG_IJR(2, 2) TCG_IJR(2, 3) TCG_IJR(2, 4)
@@ -284,6 +333,7 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ P
         TCG_IJR(6, 0) TCG_IJR(0, 0)
         default: break;
       }
+      b += len;
     }
     if (v >= 0) {
       const int cnt = cbin(kH1, gd.s1);
