@@ -204,3 +204,49 @@ def test_non_b200_engine_kinds_refused():
     g = T.from_edges([(0, 1)])
     with pytest.raises(T.ParseError):
         T.estimate(g, T.make_template([(0, 1)], 0), T.EngineKind.vectorized, 1, 1)
+
+
+def _rooted_layout(k, s):
+    info = np.zeros(4, np.int32)
+    N.check(N.lib.tcg_rooted_layout(k, s, info.ctypes.data, None, None))
+    zw, groups, full, store = (int(x) for x in info)
+    perm = np.zeros(full, np.int32)
+    slot_col = np.zeros(k * groups * zw, np.int32)
+    N.check(N.lib.tcg_rooted_layout(k, s, info.ctypes.data, perm.ctypes.data, slot_col.ctypes.data))
+    return zw, groups, store, perm, slot_col.reshape(k, groups, zw)
+
+
+@pytest.mark.parametrize("k,s", [(5, 2), (7, 3), (12, 2), (12, 3), (12, 4), (12, 8), (15, 5), (17, 4), (17, 7)])
+def test_rooted_layout_partition(k, s):
+    """Rooted-color compression layout (csrc/host.cpp build_rooted_layout):
+    every color set lands in exactly one group, every group holds at most zw
+    sets of each color, each color's slots of a group list exactly the group's
+    sets containing it, and P' storage columns are a group-major 8-aligned
+    bijection of the combinadic columns."""
+    from math import comb
+    zw, groups, store, perm, slot_col = _rooted_layout(k, s)
+    full = comb(k, s)
+    lb = -(-comb(k - 1, s - 1) // zw)
+    assert lb <= groups <= lb + lb // 16 + 2
+    assert len(set(perm.tolist())) == full and perm.min() >= 0 and perm.max() < store
+    ci = T.ColorIndexer(k)
+    members = {}
+    for c in range(k):
+        seen = set()
+        for g in range(groups):
+            cols = [int(x) for x in slot_col[c, g] if x >= 0]
+            assert len(cols) <= zw
+            for x in cols:
+                assert c in ci.set_of(x, s)
+                assert x not in seen
+                seen.add(x)
+                members.setdefault(x, set()).add(g)
+        # every set containing c has exactly one slot of color c
+        assert seen == {x for x in range(full) if c in ci.set_of(x, s)}
+    # each set belongs to one group for all its colors
+    assert all(len(gs) == 1 for gs in members.values()) and len(members) == full
+    # storage columns: group-major, groups 8-aligned
+    grp = {x: next(iter(members[x])) for x in range(full)}
+    order = sorted(range(full), key=lambda x: perm[x])
+    assert [grp[x] for x in order] == sorted(grp[x] for x in order)
+    assert store % 8 == 0
