@@ -56,10 +56,20 @@ struct ArenaPlanner {
       off = std::max(off, o + b);
     }
     used[off] = bytes;
+    refs[off] = 1;
     peak = std::max(peak, off + bytes);
     return off;
   }
-  void free(int64_t off) { used.erase(off); }
+  // a table shared by several consumers (deduplicated sub-templates) is
+  // released by its last consumer
+  std::map<int64_t, int> refs;
+  void retain(int64_t off) { ++refs[off]; }
+  void free(int64_t off) {
+    if (--refs[off] <= 0) {
+      used.erase(off);
+      refs.erase(off);
+    }
+  }
 };
 
 // g(X2, i): combinadic contribution of the H2 colors of a set whose H1 part has
@@ -534,6 +544,48 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     e.d_ins = dupload(ins, stream_);
   }
   setup_rooted_ema(max_smem);
+  // Identical sub-template computations (same recursive shape and the same
+  // table layout) are computed once: a later duplicate aliases the first
+  // node's table.  (The reference recomputes them; the tables are identical
+  // bit for bit since the kernels and split tables are the same.)
+  {
+    static const int dedup = [] {
+      const char* s = std::getenv("TCG_DEDUP");
+      return s ? std::atoi(s) : 1;
+    }();
+    std::vector<std::string> key(plan_.num_nodes, "L");
+    std::map<std::string, int> first, first_pp;
+    for (size_t i = 0; i < exec_.size(); ++i) {
+      NodeExec& e = exec_[i];
+      const char* lay = rooted_ema_ ? (e.omap.empty() ? "R" : "S") : "F";
+      key[e.id] = "(" + key[e.a] + "," + key[e.p] + ")" + lay;
+      e.dup_of = e.pp_dup_of = -1;
+      if (!dedup || lmode) continue;
+      auto it = first.find(key[e.id]);
+      if (it == first.end() || e.root) {
+        if (!e.root) first.emplace(key[e.id], static_cast<int>(i));
+        // a different node over the same passive table: share its P' (SpMM)
+        if (!e.p_leaf) {
+          auto jt = first_pp.find(key[e.p]);
+          if (jt == first_pp.end()) first_pp.emplace(key[e.p], static_cast<int>(i));
+          else e.pp_dup_of = jt->second;
+        }
+      } else {
+        e.dup_of = it->second;
+      }
+    }
+  }
+  if (std::getenv("TCG_VERBOSE")) {
+    std::fprintf(stderr, "[tcg] k=%d nodes=%d rooted_ema=%d\n", k, plan_.num_nodes, rooted_ema_ ? 1 : 0);
+    for (const auto& e : exec_)
+      std::fprintf(stderr, "[tcg] node %2d (%2d,%2d,%2d) Cp=%d rooted=%d groups=%d zw=%d Cps=%d | Ws=%d Wa=%d Wp=%d Cout=%d "
+                           "%s pairs=%d blocked=%d/%d vtx=%d staged=%d dup_of=%d\n",
+                   e.id, e.size, e.sa, e.sp, e.Cp, e.rooted ? 1 : 0, e.rl_groups, e.rl_zw, e.Cps, e.Ws, e.Wa, e.Wp,
+                   e.Cout, e.omap.empty() ? "RR" : "RS", e.rt_pairs, e.rt_blocked ? 1 : 0, e.blocked ? 1 : 0,
+                   e.vtx ? 1 : 0, e.ema_staged ? 1 : 0, e.dup_of >= 0 ? exec_[e.dup_of].id : -1);
+    for (const auto& e : exec_)
+      if (e.pp_dup_of >= 0) std::fprintf(stderr, "[tcg] node %d shares the SpMM of node %d\n", e.id, exec_[e.pp_dup_of].id);
+  }
   TCG_CUDA(cudaStreamSynchronize(stream_));
   have_template_ = true;
   if (n_ >= 0) plan_arena();
@@ -709,7 +761,25 @@ void Engine::plan_arena() {
       if (e.rooted) rooted_partial = std::max<int64_t>(rooted_partial, static_cast<int64_t>(slots) * static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / e.rl_zw))));
   }
   for (auto& e : exec_) {
-    if (!e.p_leaf && e.rooted && rooted_ema_) {
+    if (e.dup_of >= 0) {  // alias the first occurrence; release this node's own children
+      const NodeExec& x = exec_[e.dup_of];
+      table_off_[e.id] = table_off_[x.id];
+      e.out_off = x.out_off;
+      e.pp_off = x.pp_off;
+      if (!e.p_leaf) pprime_off_[e.p] = pprime_off_[x.p];
+      // (the first occurrence's table was retained once per duplicate when
+      // allocated; this node's parent releases that reference)
+      if (!keep) {
+        if (!e.p_leaf) ap.free(table_off_[e.p]);
+        if (!e.a_leaf) ap.free(table_off_[e.a]);
+      }
+      continue;
+    }
+    if (e.pp_dup_of >= 0) {  // P' identical to an earlier node's: alias it
+      e.pp_off = exec_[e.pp_dup_of].pp_off;
+      pprime_off_[e.p] = e.pp_off;
+      if (!keep) ap.free(table_off_[e.p]);
+    } else if (!e.p_leaf && e.rooted && rooted_ema_) {
       // M_p is already in the SpMM's compressed slot layout
       e.pp_off = ap.alloc(table_bytes(e.Cps));
       pprime_off_[e.p] = e.pp_off;
@@ -737,6 +807,9 @@ void Engine::plan_arena() {
         ap.free(table_off_[e.p]);
       }
     }
+    if (!e.p_leaf && e.pp_dup_of < 0)
+      for (const auto& y : exec_)  // one reference per node sharing this P'
+        if (y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id) ap.retain(e.pp_off);
     if (e.skip_ema) {                 // M of this node is never needed
       table_off_[e.id] = -1;
       e.out_off = -1;
@@ -746,6 +819,8 @@ void Engine::plan_arena() {
     }
     e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(rooted_ema_ ? e.Cout : e.Cs));
     table_off_[e.id] = e.out_off;
+    for (const auto& y : exec_)  // one reference per duplicate's consumer
+      if (y.dup_of >= 0 && exec_[y.dup_of].id == e.id) ap.retain(e.out_off);
     if (!keep) {
       if (!e.p_leaf) ap.free(e.pp_off);
       if (!e.a_leaf) ap.free(table_off_[e.a]);
@@ -1229,8 +1304,15 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
   for (auto& e : exec_) {
     Marks m{0, 0, 0};
     if (stats) m.t0 = mark();
+    if (e.dup_of >= 0) {  // identical to an earlier node: its table is aliased
+      if (stats) { m.t1 = mark(); m.t2 = mark(); }
+      marks.push_back(m);
+      continue;
+    }
     const float* P = H;
-    if (!e.p_leaf && n_ > 0) {
+    if (e.pp_dup_of >= 0) {
+      P = table_ptr(e.pp_off);
+    } else if (!e.p_leaf && n_ > 0) {
       size_t p0 = 0;
       if (prof_) { p0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       if (e.lspmm) {
@@ -1524,7 +1606,8 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
   const Binom& B = binom();
   const double n = n_, nnz = static_cast<double>(nnz_);
   for (auto& e : exec_) {
-    if (!e.p_leaf) {
+    if (e.dup_of >= 0) continue;  // not executed (aliased): no work claimed
+    if (!e.p_leaf && e.pp_dup_of < 0) {
       t.spmm_launches += count;
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
       // columns actually gathered per neighbour

@@ -80,6 +80,8 @@ struct NodeExec {
   void* d_rt_blocks = nullptr;
   int rt_ngroups = 0;
   size_t rt_smem = 0;
+  int dup_of = -1;                // exec index of an identical earlier node (table aliased)
+  int pp_dup_of = -1;             // exec index of an earlier node with the same P' (SpMM skipped)
 };
 
 // SpMM work schedule for one vertex-range part of the gather source.
