@@ -382,6 +382,8 @@ void Engine::set_graph(const Csr& gin) {
     d_row_order_ = dupload(order, stream_);
     nlong_ = 0;
     while (nlong_ < n_ && g.row_ptr[order[nlong_] + 1] - g.row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
+    nsmall_ = nlong_;  // rows of degree <= kBucketSmall: a thread each
+    while (nsmall_ < n_ && g.row_ptr[order[nsmall_] + 1] - g.row_ptr[order[nsmall_]] > dev::kBucketSmall) ++nsmall_;
     TCG_CUDA(cudaMalloc(&d_counter_, 64));
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
@@ -1279,9 +1281,14 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
                                                                                 plan_.k, rooted_parts_, rc, cuts, hf, hzw);
       ++launches_;
     }
-    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, n_, plan_.k,
-                                                     rooted_parts_, rc, cuts, hf, hzw);
+    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, nsmall_,
+                                                     plan_.k, rooted_parts_, rc, cuts, hf, hzw);
     ++launches_;
+    if (nsmall_ < n_) {
+      dev::bucket_small<<<static_cast<unsigned>((n_ - nsmall_ + 255) / 256), 256, 0, stream_>>>(
+          d_row_ptr_, d_col_, d_gcolors, d_row_order_, nsmall_, n_, plan_.k, rooted_parts_, rc, cuts, hf, hzw);
+      ++launches_;
+    }
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
   }

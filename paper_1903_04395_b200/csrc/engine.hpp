@@ -195,6 +195,7 @@ class Engine {
   int max_slots_ = 0;
   int32_t* d_row_order_ = nullptr;   // rows by degree, descending (color_bucket)
   int32_t nlong_ = 0;                // rows of degree > dev::kBucketLong (a prefix of row order)
+  int32_t nsmall_ = 0;               // first row (in row order) of degree <= dev::kBucketSmall
   int* d_counter_ = nullptr;
 
   // template / plan

@@ -1,6 +1,8 @@
 set -x
 timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
-TCG_VERBOSE=1 timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 --stats 2>&1 | tail -26
+python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
+timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 2>&1 | tail -1
 timeout 300 python tools/prof_driver.py --config cfg2 --colorings 5 2>&1 | tail -1
-timeout 600 python tools/prof_driver.py --config cfg5 --warmup 0 --colorings 1 2>&1 | tail -1
 timeout 600 python -m pytest tests/test_sharded.py -x -q -m gpu 2>&1 | tail -2
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q_cfg2.csv python tools/prof_driver.py --config cfg2 --warmup 0 --colorings 1 > /dev/null 2>&1
+ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q_cfg3.csv python tools/prof_driver.py --config cfg3 --warmup 0 --colorings 1 > /dev/null 2>&1
