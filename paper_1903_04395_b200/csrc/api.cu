@@ -73,7 +73,7 @@ extern "C" {
 const char* tcg_last_error(void) { return g_err.c_str(); }
 
 const char* tcg_version(void) {
-  return "treecount-b200 0.1 (sm_100a; fp32 panel tables Z=16, fp64 accumulation/root)";
+  return "treecount-b200 0.2 (sm_100a; fp32 128 B panel tables, rooted-color compression, fp64 accumulation/root)";
 }
 
 // ------------------------------------------------------------------ graph
@@ -234,8 +234,14 @@ int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t
     need(ctx, "ctx");
     need(row_ptr, "row_ptr");
     // the reference's Graph invariants are the caller's contract here (as for
-    // a treecount::Graph); ranges / order / loops are still checked in O(nnz)
-    ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col, /*check_symmetry=*/false));
+    // a treecount::Graph); row_ptr is checked on the host, ids / order / loops
+    // on the device after the upload (O(nnz) there, no host copy)
+    if (n < 0 || row_ptr[0] != 0) throw tcg::invalid_argument("bad CSR row_ptr");
+    for (int32_t v = 0; v < n; ++v)
+      if (row_ptr[v + 1] < row_ptr[v]) throw tcg::invalid_argument("CSR row_ptr not monotone");
+    if (row_ptr[n] > 0) need(col, "col");
+    if (ctx->eng->sharded()) ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col, /*check_symmetry=*/false));
+    else ctx->eng->set_graph_ptrs(n, row_ptr, col, /*validate=*/true);
   });
 }
 

@@ -244,6 +244,9 @@ void Engine::release_graph() {
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
+  host_row_ptr_.clear();
+  host_col_.clear();
+  host_col_.shrink_to_fit();
   n_ = -1;
 }
 
@@ -285,6 +288,10 @@ void Engine::set_shard(int rank, int world, std::unique_ptr<Transport> t) {
 }
 
 void Engine::set_graph(const Csr& gin) {
+  if (!sharded()) {
+    set_graph_ptrs(gin.n, gin.row_ptr.data(), gin.col.data(), false);
+    return;
+  }
   TCG_CUDA(cudaSetDevice(cfg_.device));
   release_graph();
   Csr local;
@@ -321,76 +328,116 @@ void Engine::set_graph(const Csr& gin) {
   const Csr& g = *gp;
   n_ = g.n;
   nnz_ = g.nnz();
-  if (sharded()) {
-    TCG_CUDA(cudaMalloc(&d_xfull_, sizeof(float) * dev::kZ * std::max<int64_t>(nsrc_, 1)));
-    TCG_CUDA(cudaMalloc(&d_colors_pad_, std::max<int64_t>(nsrc_, 1)));
-    // [0, 2048): this rank's totals chunk; [2048, 2048 * (world + 1)): gathered
-    TCG_CUDA(cudaMalloc(&d_gather_, sizeof(double) * 2048 * (world_ + 1)));
-    d_rows_ = dupload(rows_, stream_);
-  }
+  TCG_CUDA(cudaMalloc(&d_xfull_, sizeof(float) * dev::kZ * std::max<int64_t>(nsrc_, 1)));
+  TCG_CUDA(cudaMalloc(&d_colors_pad_, std::max<int64_t>(nsrc_, 1)));
+  // [0, 2048): this rank's totals chunk; [2048, 2048 * (world + 1)): gathered
+  TCG_CUDA(cudaMalloc(&d_gather_, sizeof(double) * 2048 * (world_ + 1)));
+  d_rows_ = dupload(rows_, stream_);
+  host_col_ = g.col;  // (the sharded CSR is a local copy anyway)
+  finish_graph(g.row_ptr.data(), g.col.data(), false);
+}
+
+// Unsharded graph straight from caller buffers (not copied on the host): the
+// CSR goes host -> device once (pinned buffers make this a full-speed DMA),
+// is validated on the device when `validate`, and only O(n) host work builds
+// the whole-row schedule and the degree order.  Vertex-range part schedules
+// (full-table SpMM only) are built on first use (ensure_schedules).
+void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate) {
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  release_graph();
+  nglob_ = n;
+  rows_ = {0, static_cast<int64_t>(n)};
+  nloc_ = n;
+  nsrc_ = n;
+  n_ = n;
+  nnz_ = row_ptr[n];
+  finish_graph(row_ptr, col, validate);
+}
+
+void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool validate) {
+  host_row_ptr_.assign(row_ptr, row_ptr + n_ + 1);
   TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (n_ + 1)));
   TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
-  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, g.row_ptr.data(), sizeof(int64_t) * (n_ + 1),
-                           cudaMemcpyHostToDevice, stream_));
-  if (nnz_)
-    TCG_CUDA(cudaMemcpyAsync(d_col_, g.col.data(), sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice,
-                             stream_));
-  // Parts: the gather source of one panel is n*ZW*4 B; split the vertex
-  // range so each part's rows (the L2-resident working set) fit in
-  // part_bytes_.  Each CSR row is sorted, so a row's neighbours in a part are
-  // one contiguous sub-range.  One schedule set per distinct part count.
+  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyHostToDevice, stream_));
+  if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice, stream_));
+  if (validate && nnz_) {
+    TCG_CUDA(cudaMemsetAsync(reinterpret_cast<int*>(d_scalars_ + 4), 0, sizeof(int), stream_));
+    dev::validate_csr<<<148 * 8, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, reinterpret_cast<int*>(d_scalars_ + 4));
+    ++launches_;
+  }
   // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
   // sparse skewed graphs (cfg2, avg ~30) the hub rows stay L2-resident anyway
   // and extra parts only add output passes (measured: profiles/ DESIGN.md 3).
   if (!std::getenv("TCG_PART_MB"))
     part_bytes_ = (n_ > 0 && nnz_ / std::max(n_, 1) >= 64) ? (64ll << 20) : (128ll << 20);
-  std::vector<int> counts{1};
-  for (int zw : {8, 16, 32}) counts.push_back(parts_for_width(zw));
-  std::sort(counts.begin(), counts.end());
-  counts.erase(std::unique(counts.begin(), counts.end()), counts.end());
   max_slots_ = 0;
-  for (int P : counts) {
-    std::vector<std::vector<int64_t>> bnd(P + 1, std::vector<int64_t>(n_));
-    const int T = std::max(1, std::min(host_threads(), 32));
-    std::vector<std::thread> th;
-    for (int w = 0; w < T; ++w)
-      th.emplace_back([&, w] {
-        for (int64_t v = static_cast<int64_t>(n_) * w / T; v < static_cast<int64_t>(n_) * (w + 1) / T; ++v) {
-          const int32_t* b = g.col.data() + g.row_ptr[v];
-          const int32_t* e = g.col.data() + g.row_ptr[v + 1];
-          bnd[0][v] = g.row_ptr[v];
-          bnd[P][v] = g.row_ptr[v + 1];
-          for (int s = 1; s < P; ++s) {
-            const int64_t cut = static_cast<int64_t>(nsrc_) * s / P;
-            bnd[s][v] = g.row_ptr[v] + (std::lower_bound(b, e, static_cast<int32_t>(cut)) - b);
-          }
-        }
-      });
-    for (auto& t : th) t.join();
-    auto& vec = sched_[P];
-    for (int s = 0; s < P; ++s) {
-      vec.push_back(build_schedule(bnd[s], bnd[s + 1], s == 0, stream_));
-      max_slots_ = std::max(max_slots_, vec.back().nslots);
-    }
+  {  // whole-row schedule: the rooted SpMM, the histogram, P = 1 panels
+    std::vector<int64_t> lo(row_ptr, row_ptr + n_), hi(row_ptr + 1, row_ptr + n_ + 1);
+    sched_[1].push_back(build_schedule(lo, hi, true, stream_));
+    max_slots_ = sched_[1][0].nslots;
   }
-  {  // rows by degree, descending, for the per-coloring color bucketing
+  {  // rows by degree, descending (stable counting sort), for the per-coloring bucketing
+    int64_t maxd = 0;
+    for (int32_t v = 0; v < n_; ++v) maxd = std::max(maxd, row_ptr[v + 1] - row_ptr[v]);
+    std::vector<int64_t> start(static_cast<size_t>(maxd) + 2, 0);
+    for (int32_t v = 0; v < n_; ++v) ++start[maxd - (row_ptr[v + 1] - row_ptr[v]) + 1];
+    for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
     std::vector<int32_t> order(static_cast<size_t>(n_));
-    for (int32_t v = 0; v < n_; ++v) order[v] = v;
-    std::stable_sort(order.begin(), order.end(), [&](int32_t x, int32_t y) {
-      return g.row_ptr[x + 1] - g.row_ptr[x] > g.row_ptr[y + 1] - g.row_ptr[y];
-    });
+    for (int32_t v = 0; v < n_; ++v) order[start[maxd - (row_ptr[v + 1] - row_ptr[v])]++] = v;
     d_row_order_ = dupload(order, stream_);
     nlong_ = 0;
-    while (nlong_ < n_ && g.row_ptr[order[nlong_] + 1] - g.row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
+    while (nlong_ < n_ && row_ptr[order[nlong_] + 1] - row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
     nsmall_ = nlong_;  // rows of degree <= kBucketSmall: a thread each
-    while (nsmall_ < n_ && g.row_ptr[order[nsmall_] + 1] - g.row_ptr[order[nsmall_]] > dev::kBucketSmall) ++nsmall_;
+    while (nsmall_ < n_ && row_ptr[order[nsmall_] + 1] - row_ptr[order[nsmall_]] > dev::kBucketSmall) ++nsmall_;
     TCG_CUDA(cudaMalloc(&d_counter_, 64));
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
   TCG_CUDA(cudaStreamSynchronize(stream_));
+  if (validate && nnz_) {
+    int bad = 0;
+    copy_sync(&bad, reinterpret_cast<int*>(d_scalars_ + 4), sizeof(int), cudaMemcpyDeviceToHost);
+    if (bad) {
+      const int32_t n = n_;
+      release_graph();
+      if (bad == 1) throw invalid_argument("CSR column out of range [0, " + std::to_string(n) + ") or self-loop");
+      throw invalid_argument("CSR row not strictly ascending");
+    }
+  }
   if (have_template_) plan_arena();
   tables_valid_ = false;
+}
+
+// Vertex-range part schedules for the full-table SpMM (P parts per panel).
+void Engine::ensure_schedules(int P) {
+  if (sched_.count(P)) return;
+  if (host_col_.empty() && nnz_) {
+    host_col_.resize(static_cast<size_t>(nnz_));
+    copy_sync(host_col_.data(), d_col_, sizeof(int32_t) * nnz_, cudaMemcpyDeviceToHost);
+  }
+  const int64_t* rp = host_row_ptr_.data();
+  std::vector<std::vector<int64_t>> bnd(P + 1, std::vector<int64_t>(n_));
+  const int T = std::max(1, std::min(host_threads(), 32));
+  std::vector<std::thread> th;
+  for (int w = 0; w < T; ++w)
+    th.emplace_back([&, w] {
+      for (int64_t v = static_cast<int64_t>(n_) * w / T; v < static_cast<int64_t>(n_) * (w + 1) / T; ++v) {
+        const int32_t* b = host_col_.data() + rp[v];
+        const int32_t* e = host_col_.data() + rp[v + 1];
+        bnd[0][v] = rp[v];
+        bnd[P][v] = rp[v + 1];
+        for (int s = 1; s < P; ++s) {
+          const int64_t cut = static_cast<int64_t>(nsrc_) * s / P;
+          bnd[s][v] = rp[v] + (std::lower_bound(b, e, static_cast<int32_t>(cut)) - b);
+        }
+      }
+    });
+  for (auto& t : th) t.join();
+  auto& vec = sched_[P];
+  for (int s = 0; s < P; ++s) {
+    vec.push_back(build_schedule(bnd[s], bnd[s + 1], s == 0, stream_));
+    max_slots_ = std::max(max_slots_, vec.back().nslots);
+  }
 }
 
 // --------------------------------------------------------------- template
@@ -730,6 +777,9 @@ void Engine::plan_arena() {
   const int64_t q_budget = (std::getenv("TCG_Q_GB") ? std::atoll(std::getenv("TCG_Q_GB")) : 12ll) << 30;
   std::vector<int64_t> child_pp(plan_.num_nodes, -1);  // P' kept alive for an LSpMM parent
   int64_t lslots = 0;
+  for (const auto& e : exec_)  // full-table SpMMs: their vertex-range part schedules
+    if (!e.p_leaf && !e.rooted && !e.lspmm && e.pp_dup_of < 0 && e.dup_of < 0)
+      for (int p = 0; p < dev::num_panels(e.Cp); ++p) ensure_schedules(parts_for_width(dev::panel_width(e.Cp, p)));
   const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
   // rooted SpMMs: parts are contiguous COLOR classes (one count for all
   // rooted nodes: the widest compressed panel's), over whole-row schedules
@@ -1720,6 +1770,7 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
   if (cols < 1) throw invalid_argument("cols must be >= 1");
   TCG_CUDA(cudaSetDevice(cfg_.device));
   const int64_t n = n_;
+  for (int p = 0; p < dev::num_panels(cols); ++p) ensure_schedules(parts_for_width(dev::panel_width(cols, p)));
   std::vector<float> xp(dev::table_floats(cols, n), 0.f);
   for (int64_t v = 0; v < n; ++v)
     for (int64_t c = 0; c < cols; ++c) xp[dev::panel_offset(cols, n, v, c)] = x[v * cols + c];

@@ -114,6 +114,9 @@ class Engine {
   ~Engine();
 
   void set_graph(const Csr& g);
+  // unsharded graph from caller buffers (not copied on the host); validate =
+  // check ids / order / loops on the device
+  void set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate);
   void set_template(int k, const int32_t* edges, int root);
   int64_t required_bytes() const;
   const Plan& plan() const { return plan_; }
@@ -192,6 +195,10 @@ class Engine {
   // one-hot histogram's schedule)
   std::map<int, std::vector<PartSchedule>> sched_;
   int parts_for_width(int zw) const;
+  void ensure_schedules(int parts);
+  void finish_graph(const int64_t* row_ptr, const int32_t* col, bool validate);
+  std::vector<int64_t> host_row_ptr_;
+  std::vector<int32_t> host_col_;    // only when part schedules are needed (or sharded)
   int max_slots_ = 0;
   int32_t* d_row_order_ = nullptr;   // rows by degree, descending (color_bucket)
   int32_t nlong_ = 0;                // rows of degree > dev::kBucketLong (a prefix of row order)

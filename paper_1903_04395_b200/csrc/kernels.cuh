@@ -826,6 +826,25 @@ __global__ void rooted_fixup(const int32_t* __restrict__ rows, const int32_t* __
   *y = static_cast<float>(first ? acc : acc + static_cast<double>(*y));
 }
 
+// tcg_set_graph on the device: every id in range, no self-loop, rows strictly
+// ascending (graph.hpp invariants).  Warp per row; bad = 1 (range / loop) or
+// 2 (order), the first writer wins.
+__global__ void __launch_bounds__(256)
+validate_csr(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col, int32_t n, int* __restrict__ bad) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nwarps = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t v = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); v < n; v += nwarps) {
+    const int64_t b = row_ptr[v], e = row_ptr[v + 1];
+    int err = 0;
+    for (int64_t j = b + lane; j < e; j += 32) {
+      const int32_t u = col[j];
+      if (u < 0 || u >= n || u == v) err = 1;
+      else if (j > b && col[j - 1] >= u) err = 2;
+    }
+    if (__any_sync(0xffffffffu, err) && err) atomicCAS(bad, 0, err);
+  }
+}
+
 // Split rows: Y[row] (+)= sum of the row's fp64 partial slots, in slot order.
 __global__ void spmm_fixup(const int32_t* __restrict__ rows, const int32_t* __restrict__ slot_begin,
                            int nrows, const double* __restrict__ partial, float* __restrict__ Y,

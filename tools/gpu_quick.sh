@@ -1,8 +1,9 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py -x -q -m gpu 2>&1 | tail -2
-python -c "import __graft_entry__ as g; g.smoke()" 2>&1 | tail -1
-timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 2>&1 | tail -1
-timeout 300 python tools/prof_driver.py --config cfg2 --colorings 5 2>&1 | tail -1
-timeout 600 python -m pytest tests/test_sharded.py -x -q -m gpu 2>&1 | tail -2
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q_cfg2.csv python tools/prof_driver.py --config cfg2 --warmup 0 --colorings 1 > /dev/null 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_q_cfg3.csv python tools/prof_driver.py --config cfg3 --warmup 0 --colorings 1 > /dev/null 2>&1
+timeout 900 python -m pytest tests/ -x -q -m gpu 2>&1 | tail -2
+python bench.py --steps 3 --warmup 3 --no-cpu-baseline > gpurun_out/b3.json 2> gpurun_out/b3.err; tail -2 gpurun_out/b3.err
+python bench.py --config cfg2 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/b2.json 2> gpurun_out/b2.err
+python -c "
+import json
+for f in ['gpurun_out/b3.json','gpurun_out/b2.json']:
+    d=json.load(open(f)); print(f, d['value'], d['e2e'], d['gpu_launches'])
+"
