@@ -263,16 +263,19 @@ def run_b200(args, rank, world, local, dist):
         barrier(dist, local)
         e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
+        step_ms = []
         for i in range(e_steps):
+            ts = time.perf_counter()
             ectx.set_graph_csr(g.n, rp, cl)
             tot, est, se, pv = ectx.estimate(1 + i * ncol, ncol, per_vertex=True)
+            step_ms.append(round((time.perf_counter() - ts) * 1e3, 2))
         e_s = time.perf_counter() - t0
         barrier(dist, local)
         e_s = allreduce_max(dist, e_s, local)
         e2e = {"value": e_s * 1e3 / (e_steps * ncol * world), "unit": "ms/coloring",
                "h2d_bytes_per_step": int(rp.nbytes + cl.nbytes + 8),
                "d2h_bytes_per_step": int(8 * ncol + 8 * g.n),
-               "colorings_per_step": ncol, "steps": e_steps,
+               "colorings_per_step": ncol, "steps": e_steps, "step_ms": step_ms,
                "note": "per step: tcg_set_graph from pinned host CSR buffers (H2D, device-side validation, "
                        "schedules) + one tcg_estimate (colorings; totals + per-vertex estimates -> host); "
                        "host wall clock, max over ranks"}
