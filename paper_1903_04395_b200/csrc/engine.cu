@@ -263,6 +263,7 @@ void Engine::release_template() {
     dfree(e.d_pinv);
     dfree(e.d_pmap);
     dfree(e.d_cmap);
+    dfree(e.d_imap);
     dfree(e.d_omap);
     dfree(e.d_rt_packed);
     dfree(e.d_rt_split);
@@ -718,6 +719,13 @@ void Engine::setup_rooted_ema(int max_smem) {
             e.omap[static_cast<size_t>(c) * e.Ws + relabeled_index(cs, e.size, c)] = i;
           }
         e.d_omap = dupload(e.omap, stream_);
+        std::vector<int32_t> im(static_cast<size_t>(k) * e.Cout, -1);  // slot -> output column
+        for (int c = 0; c < k; ++c)
+          for (int32_t j = 0; j < e.Ws; ++j) {
+            const int32_t i = e.omap[static_cast<size_t>(c) * e.Ws + j];
+            if (i >= 0) im[static_cast<size_t>(c) * e.Cout + i] = j;
+          }
+        e.d_imap = dupload(im, stream_);
       } else {
         e.Cout = e.Ws;
       }
@@ -761,7 +769,13 @@ void Engine::setup_rooted_ema(int max_smem) {
         }
       }
     }
+    // (+ the RS output tile of the generic node kernel, when it fits)
     e.rt_smem = static_cast<size_t>(e.Wa + e.Wp) * (dev::kTileV + 1) * 4;
+    const size_t out_tile = static_cast<size_t>(e.Ws) * (dev::kTileV + 1) * 4;
+    if (!e.omap.empty() && !e.a_leaf && !e.rt_blocked && e.rt_smem + out_tile <= static_cast<size_t>(max_smem) - 4096)
+      e.rt_smem += out_tile;
+    else
+      dfree(e.d_imap);  // scattered RS writes instead
   }
   rooted_ema_ = true;
 }
@@ -1263,8 +1277,10 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (48 << 10) / (4 * rf))));
     const size_t smem = static_cast<size_t>(vpb) * rf * 4;
     TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    int L = 1;  // lanes per row: enough for the row's float4s and the output panel's slots
+    while (L < 32 && (L * 4 < rf || L < std::min(32, e.Cout))) L *= 2;
     dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
-        P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, out);
+        P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, L, out);
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
     dev::ema_rt_blocked<<<grid, 256, e.rt_smem, stream_>>>(
@@ -1273,7 +1289,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   } else {
     attr(reinterpret_cast<const void*>(dev::ema_rt_node<false>));
     dev::ema_rt_node<false><<<grid, warps * 32, e.rt_smem, stream_>>>(
-        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.Cout, n_, out);
+        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);
   }
 }
 

@@ -71,6 +71,7 @@ struct NodeExec {
   int32_t* d_pmap = nullptr;      // [k][Cpt] P' storage column -> staged row, or -1
   int32_t* d_omap = nullptr;      // [k][Ws] relabeled output column -> slot (RS only)
   int32_t* d_cmap = nullptr;      // active leaf: [k][Cout] output column -> P' storage column
+  int32_t* d_imap = nullptr;      // RS: [k][Cout] slot -> relabeled output column, or -1
   std::vector<int32_t> omap;      // host copy (node_table expansion)
   uint32_t* d_rt_packed = nullptr;
   int2* d_rt_split = nullptr;     // root

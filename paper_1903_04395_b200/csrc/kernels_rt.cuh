@@ -195,7 +195,8 @@ __global__ void __launch_bounds__(kEmaWarps * 32)
 ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
             const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
             const int4* __restrict__ tiles, const uint32_t* __restrict__ packed, int pairs, int Ws,
-            const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out) {
+            const int32_t* __restrict__ omap, const int32_t* __restrict__ imap, int Cout, int32_t n,
+            float* __restrict__ out) {
   extern __shared__ float smem[];
   __shared__ int32_t vids[32];
   const int4 tile = tiles[blockIdx.x];
@@ -211,6 +212,9 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   __syncthreads();
   const int64_t v = vids[lane];
   const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
+  // RS output: staged in smem [Ws][kSpitch], then written as coalesced slot
+  // rows through the per-color inverse map (imap: slot -> output column)
+  float* sO = smem + (ALEAF ? 0 : Wa * kSpitch) + Wp * kSpitch;
   const int nchunks = (Ws + 7) / 8;
   for (int q = warp; q < nchunks; q += blockDim.x >> 5) {
     float r[8];
@@ -236,7 +240,29 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
         }
       }
     }
-    if (v >= 0) rt_write8(out, Ws, Cout, om, n, v, q * 8, r);
+    if (om && imap) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (q * 8 + j < Ws) sO[(q * 8 + j) * kSpitch + lane] = r[j];
+    } else if (v >= 0) {
+      rt_write8(out, Ws, Cout, om, n, v, q * 8, r);
+    }
+  }
+  if (om && imap) {
+    __syncthreads();
+    const int32_t* im = imap + static_cast<int64_t>(c) * Cout;
+    const int pout = num_panels(Cout), zout = last_panel_width(Cout);
+    for (int rr = warp; rr < 32; rr += blockDim.x >> 5) {
+      const int64_t u = vids[rr];
+      if (u < 0) continue;
+      for (int p = 0; p < pout; ++p) {
+        const int zp = p == pout - 1 ? zout : kZ;
+        if (lane < zp) {
+          const int j = p * kZ + lane < Cout ? __ldg(im + p * kZ + lane) : -1;
+          out[static_cast<int64_t>(p) * n * kZ + u * zp + lane] = j >= 0 ? sO[j * kSpitch + rr] : 0.f;
+        }
+      }
+    }
   }
 }
 
@@ -247,36 +273,38 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
 // (coalesced as well).  Natural vertex order, no tiles.
 __global__ void __launch_bounds__(256)
 ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ colors,
-            const int32_t* __restrict__ cmap, int Cout, int32_t n, int vpb, float* __restrict__ out) {
+            const int32_t* __restrict__ cmap, int Cout, int32_t n, int vpb, int L, float* __restrict__ out) {
+  // L lanes per vertex row (a power of two <= 32, sized to the rows on the host)
   extern __shared__ float crow[];
+  const int lane = threadIdx.x & 31, sub = lane & (L - 1);
+  const int grp = static_cast<int>(threadIdx.x) / L, ngrp = blockDim.x / L;
   const int pin = num_panels(Cpt), zin = last_panel_width(Cpt);
-  const int rf = (pin - 1) * kZ + zin;
-  const int per = rf / 4;
+  const int rf = (pin - 1) * kZ + zin;  // floats of one panel-padded row
   const int64_t u0 = static_cast<int64_t>(blockIdx.x) * vpb;
-  for (int f = threadIdx.x; f < vpb * per; f += blockDim.x) {
-    const int r = f / per, c4 = (f % per) * 4;
+  for (int r = grp; r < vpb; r += ngrp) {  // stage: 128 B panel rows, float4 per lane
     const int64_t u = u0 + r;
-    if (u >= n) continue;
-    const int p = c4 >> 5, z = c4 & 31;
-    const int zp = p == pin - 1 ? zin : kZ;
-    *reinterpret_cast<float4*>(crow + r * rf + c4) =
-        __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+    if (u >= n) break;
+    for (int c4 = sub * 4; c4 < rf; c4 += L * 4) {
+      const int p = c4 >> 5, z = c4 & 31;
+      const int zp = p == pin - 1 ? zin : kZ;
+      *reinterpret_cast<float4*>(crow + r * rf + c4) =
+          __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+    }
   }
   __syncthreads();
   const int pout = num_panels(Cout), zout = last_panel_width(Cout);
-  const int rout = (pout - 1) * kZ + zout;  // floats per output row (panel-padded)
-  for (int i = threadIdx.x; i < vpb * rout; i += blockDim.x) {
-    // (panel, vertex, slot) order: consecutive threads write one 128 B panel row
-    const int p = i / (vpb * kZ);
-    const int zp = p == pout - 1 ? zout : kZ;
-    const int rem = i - p * vpb * kZ;
-    if (rem >= vpb * zp) continue;
-    const int r = rem / zp, t = rem % zp;
+  for (int r = grp; r < vpb; r += ngrp) {  // write: consecutive lanes -> consecutive slots of a row
     const int64_t u = u0 + r;
-    if (u >= n) continue;
-    const int col = p * kZ + t;
-    const int src = col < Cout ? __ldg(cmap + static_cast<int64_t>(colors[u]) * Cout + col) : -1;
-    out[static_cast<int64_t>(p) * n * kZ + u * zp + t] = src >= 0 ? crow[r * rf + src] : 0.f;
+    if (u >= n) break;
+    const int32_t* cm = cmap + static_cast<int64_t>(colors[u]) * Cout;
+    for (int p = 0; p < pout; ++p) {
+      const int zp = p == pout - 1 ? zout : kZ;
+      for (int t = sub; t < zp; t += L) {
+        const int col = p * kZ + t;
+        const int src = col < Cout ? __ldg(cm + col) : -1;
+        out[static_cast<int64_t>(p) * n * kZ + u * zp + t] = src >= 0 ? crow[r * rf + src] : 0.f;
+      }
+    }
   }
 }
 

@@ -378,3 +378,39 @@ def test_isolated_and_empty_rows():
     c = ctx_for(g, t)
     total, pv, _ = c.run_coloring(2, per_vertex=True)
     assert total == 0.0 and np.all(pv == 0)
+
+
+def test_set_graph_csr_validated_on_device():
+    """tcg_set_graph uploads the caller's CSR and checks the reference's Graph
+    invariants on the device: ids in range, no self-loops, rows strictly
+    ascending (graph.hpp:65-95 produces exactly such rows)."""
+    c = T.Context(0)
+    c.set_template(T.make_template([(0, 1), (1, 2)], 0))
+    rp = np.array([0, 1, 3, 4], np.int64)
+    c.set_graph_csr(3, rp, np.array([1, 0, 2, 1], np.int32))  # the path 0-1-2
+    total, _, _ = c.run_coloring(1)
+    assert total >= 0
+    for bad in ([1, 0, 3, 1],      # id out of range
+                [1, 1, 2, 1],      # self-loop in row 1
+                [1, 2, 0, 1]):     # row 1 not ascending
+        with pytest.raises(T.ParseError):
+            c.set_graph_csr(3, rp, np.array(bad, np.int32))
+    with pytest.raises(T.ParseError):
+        c.set_graph_csr(3, np.array([0, 2, 1, 4], np.int64), np.array([1, 0, 2, 1], np.int32))
+    # the context is usable again after a rejected graph
+    c.set_graph_csr(3, rp, np.array([1, 0, 2, 1], np.int32))
+    assert c.run_coloring(1)[0] == total
+
+
+def test_host_csr_and_graph_handle_agree():
+    """The e2e entry (host CSR buffers, device validation, O(n) host schedules)
+    and the Graph-handle entry give identical results."""
+    g = T.generate_rmat(T.RmatSpec(13, 24 << 13, .45, .15, .15, .25, 4))
+    t = T.template_from_parents(CFG_TEMPLATES["cfg3"], 0)
+    a = ctx_for(g, t)
+    b = T.Context(0)
+    b.set_template(t)
+    b.set_graph_csr(g.n, np.ascontiguousarray(g.csc_col_ptr), np.ascontiguousarray(g.csc_rows))
+    ta, pa, _ = a.run_coloring(3, per_vertex=True)
+    tb, pb, _ = b.run_coloring(3, per_vertex=True)
+    assert ta == tb and np.array_equal(pa, pb)
