@@ -244,6 +244,9 @@ void Engine::release_graph() {
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
+  dfree(d_lchunks_);
+  dfree(d_lfirst_);
+  nlchunks_ = 0;
   host_row_ptr_.clear();
   host_col_.clear();
   host_col_.shrink_to_fit();
@@ -388,6 +391,23 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
     d_row_order_ = dupload(order, stream_);
     nlong_ = 0;
     while (nlong_ < n_ && row_ptr[order[nlong_] + 1] - row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
+    {  // hub rows -> chunks of kLongChunk entries (offsets within the row)
+      std::vector<int4> ch;
+      std::vector<int32_t> first{0};
+      for (int32_t r = 0; r < nlong_; ++r) {
+        const int32_t v = order[r];
+        const int64_t d = row_ptr[v + 1] - row_ptr[v];
+        int32_t q = 0;
+        for (int64_t o = 0; o < d; o += dev::kLongChunk, ++q)
+          ch.push_back(make_int4(v, static_cast<int32_t>(o), static_cast<int32_t>(std::min<int64_t>(d, o + dev::kLongChunk)), q));
+        first.push_back(static_cast<int32_t>(ch.size()));
+      }
+      nlchunks_ = static_cast<int32_t>(ch.size());
+      if (nlchunks_) {
+        d_lchunks_ = dupload(ch, stream_);
+        d_lfirst_ = dupload(first, stream_);
+      }
+    }
     nsmall_ = nlong_;  // rows of degree <= kBucketSmall: a thread each
     while (nsmall_ < n_ && row_ptr[order[nsmall_] + 1] - row_ptr[order[nsmall_]] > dev::kBucketSmall) ++nsmall_;
     TCG_CUDA(cudaMalloc(&d_counter_, 64));
@@ -811,6 +831,7 @@ void Engine::plan_arena() {
       throw invalid_argument("graph too large for the rooted-compressed SpMM (ids >= 2^27); set TCG_ROOTED=0");
     rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
     rcut_off_ = ap.alloc(8 * static_cast<int64_t>(n_) * (rooted_parts_ + 1));
+    lcnt_off_ = ap.alloc(4 * 32 * static_cast<int64_t>(std::max(nlchunks_, 1)));
   }
   vs_off_ = tiles_off_ = vcnt_off_ = -1;
   max_tiles_ = static_cast<int>((n_ + dev::kTileV - 1) / dev::kTileV) + plan_.k;
@@ -1259,13 +1280,14 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   };
   if (e.root) {
     double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
+    const int rwarps = std::max(2, std::min(dev::kEmaWarps, e.rt_pairs / 4));  // warps split the pairs
     if (e.a_leaf) {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<true>));
-      dev::ema_rt_root<true><<<grid, dev::kEmaWarps * 32, e.rt_smem, stream_>>>(
+      dev::ema_rt_root<true><<<grid, 64, e.rt_smem, stream_>>>(
           A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     } else {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<false>));
-      dev::ema_rt_root<false><<<grid, dev::kEmaWarps * 32, e.rt_smem, stream_>>>(
+      dev::ema_rt_root<false><<<grid, rwarps * 32, e.rt_smem, stream_>>>(
           A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     }
     return;
@@ -1336,16 +1358,21 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     size_t b0 = 0;
     if (prof_) { b0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
-    const size_t smem = sizeof(int) * 8 * plan_.k, lsmem = sizeof(int) * 9 * plan_.k;
+    const size_t smem = sizeof(int) * 8 * plan_.k;
     uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
     int64_t* cuts = reinterpret_cast<int64_t*>(arena_ + rcut_off_);
     // the bucketing counts ARE the neighbour color histogram: fused
     float* hf = need_hist_ ? table_ptr(hist_off_) : nullptr;
     const int hzw = dev::panel_width(plan_.k, 0);
-    if (nlong_ > 0) {
-      dev::bucket_long<<<static_cast<unsigned>(nlong_), 256, lsmem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_,
-                                                                                plan_.k, rooted_parts_, rc, cuts, hf, hzw);
-      ++launches_;
+    if (nlong_ > 0) {  // hub rows: chunked over many CTAs
+      int* ccnt = reinterpret_cast<int*>(arena_ + lcnt_off_);
+      dev::bucket_long_count<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
+                                                                                     plan_.k, ccnt);
+      dev::bucket_long_scan<<<static_cast<unsigned>((nlong_ + 7) / 8), 256, 0, stream_>>>(
+          d_lchunks_, d_lfirst_, d_row_ptr_, nlong_, plan_.k, rooted_parts_, ccnt, cuts, hf, hzw);
+      dev::bucket_long_scatter<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
+                                                                                       plan_.k, ccnt, rc);
+      launches_ += 3;
     }
     dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, nsmall_,
                                                      plan_.k, rooted_parts_, rc, cuts, hf, hzw);
@@ -1366,7 +1393,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     const int nchunks = static_cast<int>((n_ + dev::kVsChunk - 1) / dev::kVsChunk);
     int* vcnt = reinterpret_cast<int*>(arena_ + vcnt_off_);
     dev::vsort_count<<<nchunks, 256, 0, stream_>>>(d_colors, n_, plan_.k, vcnt);
-    dev::vsort_scan<<<1, 256, 0, stream_>>>(vcnt, nchunks, plan_.k, reinterpret_cast<int4*>(arena_ + tiles_off_), max_tiles_);
+    dev::vsort_scan<<<1, 1024, 0, stream_>>>(vcnt, nchunks, plan_.k, reinterpret_cast<int4*>(arena_ + tiles_off_), max_tiles_);
     dev::vsort_scatter<<<nchunks, 256, 0, stream_>>>(d_colors, n_, plan_.k, vcnt, reinterpret_cast<int32_t*>(arena_ + vs_off_));
     launches_ += 3;
     TCG_CUDA(cudaGetLastError());

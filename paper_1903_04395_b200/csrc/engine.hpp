@@ -204,6 +204,10 @@ class Engine {
   int32_t* d_row_order_ = nullptr;   // rows by degree, descending (color_bucket)
   int32_t nlong_ = 0;                // rows of degree > dev::kBucketLong (a prefix of row order)
   int32_t nsmall_ = 0;               // first row (in row order) of degree <= dev::kBucketSmall
+  int4* d_lchunks_ = nullptr;        // hub-row chunks {row, begin, end, index in row}
+  int32_t* d_lfirst_ = nullptr;      // first chunk of each hub row (nlong_ + 1)
+  int32_t nlchunks_ = 0;
+  int64_t lcnt_off_ = -1;            // per-coloring chunk color counts [chunks][32]
   int* d_counter_ = nullptr;
 
   // template / plan

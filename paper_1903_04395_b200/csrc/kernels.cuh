@@ -590,24 +590,19 @@ bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ co
     cuts[static_cast<int64_t>(v) * (nparts + 1) + part] = b + below(part * k / nparts);
 }
 
-// Rows longer than kBucketLong (row_order[0, nlong)): one CTA per row; warp w
-// owns the w-th contiguous slice, so offsets ordered (color, warp) keep the
-// sort stable.  smem: cnt[8][k] + tot[k].
-__global__ void __launch_bounds__(256)
-bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int k, int nparts,
-            uint32_t* __restrict__ out, int64_t* __restrict__ cuts, float* __restrict__ hist, int hzw) {
-  extern __shared__ int bsm[];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int* cnt = bsm + warp * k;
-  int* tot = bsm + nw * k;
+// Rows longer than kBucketLong are cut into chunks of <= kLongChunk entries,
+// one CTA each, so a hub row (cfg2: 64K neighbours) is spread over many SMs.
+// chunk = {row, begin, end (offsets within the row), chunk index within the
+// row}.  Three passes:
+// per-chunk color counts, a per-row scan (color-major, chunk order: stable),
+// and the scatter (warp w of a chunk owns its w-th contiguous slice).
+constexpr int kLongChunk = 4096;
+
+// per-warp color counts of this CTA's chunk slice into cnt[8][k] (smem)
+__device__ __forceinline__ void long_chunk_counts(const int32_t* __restrict__ col, const uint8_t* __restrict__ colors,
+                                                  int64_t sb, int64_t se, int* cnt) {
+  const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
-  const int32_t v = row_order[blockIdx.x];
-  const int64_t b = row_ptr[v], e = row_ptr[v + 1];
-  const int64_t slice = ((e - b + nw - 1) / nw + 31) / 32 * 32;
-  const int64_t sb = min(e, b + warp * slice), se = min(e, sb + slice);
-  for (int i = threadIdx.x; i < (nw + 1) * k; i += blockDim.x) bsm[i] = 0;
-  __syncthreads();
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
     const int key = ok ? colors[col[j + lane]] : -1;
@@ -615,32 +610,91 @@ bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     if (ok && (same & lt) == 0) cnt[key] += __popc(same);
     __syncwarp();
   }
+}
+
+__global__ void __launch_bounds__(256)
+bucket_long_count(const int4* __restrict__ chunks, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                  const uint8_t* __restrict__ colors, int k, int* __restrict__ ccnt) {
+  __shared__ int wc[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int4 ch = chunks[blockIdx.x];
+  wc[warp][lane] = 0;
+  __syncwarp();
+  const int64_t rb = row_ptr[ch.x];
+  const int64_t slice = (kLongChunk / 8);
+  const int64_t sb = min(rb + ch.z, rb + ch.y + warp * slice);
+  const int64_t se = min(rb + ch.z, sb + slice);
+  long_chunk_counts(col, colors, sb, se, wc[warp]);
   __syncthreads();
-  for (int key = threadIdx.x; key < k; key += blockDim.x) {
+  if (threadIdx.x < k) {
     int t = 0;
-    for (int w = 0; w < nw; ++w) t += bsm[w * k + key];
-    tot[key] = t;
+    for (int w = 0; w < 8; ++w) t += wc[w][threadIdx.x];
+    ccnt[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x] = t;
   }
+}
+
+// warp per long row: lane c = color; per-chunk offsets (in place), histogram, cuts
+__global__ void __launch_bounds__(256)
+bucket_long_scan(const int4* __restrict__ chunks, const int32_t* __restrict__ row_first_chunk, const int64_t* __restrict__ row_ptr,
+                 int nlong, int k, int nparts, int* __restrict__ ccnt, int64_t* __restrict__ cuts,
+                 float* __restrict__ hist, int hzw) {
+  const int lane = threadIdx.x & 31;
+  const int r = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
+  if (r >= nlong) return;
+  const int c0 = row_first_chunk[r], c1 = row_first_chunk[r + 1];
+  const int32_t v = chunks[c0].x;
+  const int64_t b = row_ptr[v];
+  int tot = 0;
+  if (lane < k)
+    for (int c = c0; c < c1; ++c) tot += ccnt[static_cast<int64_t>(c) * 32 + lane];
+  if (hist && lane < hzw) hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(tot) : 0.f;
+  int incl = tot;  // exclusive scan over colors
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += y;
+  }
+  const int base = incl - tot;
+  const int total = __shfl_sync(0xffffffffu, incl, 31);
+  for (int part = 0; part <= nparts; ++part) {
+    const int cb = part * k / nparts;
+    const int at = cb < k ? __shfl_sync(0xffffffffu, base, cb) : total;
+    if (lane == 0) cuts[static_cast<int64_t>(v) * (nparts + 1) + part] = b + at;
+  }
+  if (lane < k) {
+    int run = base;
+    for (int c = c0; c < c1; ++c) {
+      const int x = ccnt[static_cast<int64_t>(c) * 32 + lane];
+      ccnt[static_cast<int64_t>(c) * 32 + lane] = run;
+      run += x;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256)
+bucket_long_scatter(const int4* __restrict__ chunks, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
+                    const uint8_t* __restrict__ colors, int k, const int* __restrict__ ccnt, uint32_t* __restrict__ out) {
+  __shared__ int wc[8][32];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned lt = (1u << lane) - 1u;
+  const int4 ch = chunks[blockIdx.x];
+  wc[warp][lane] = 0;
+  __syncwarp();
+  const int64_t rb = row_ptr[ch.x];
+  const int64_t slice = (kLongChunk / 8);
+  const int64_t sb = min(rb + ch.z, rb + ch.y + warp * slice);
+  const int64_t se = min(rb + ch.z, sb + slice);
+  long_chunk_counts(col, colors, sb, se, wc[warp]);
   __syncthreads();
-  if (warp == 0) {
-    if (hist && lane < hzw) hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(tot[lane]) : 0.f;
-    __syncwarp();
-    warp_exclusive_scan(tot, k, lane);
-    if (lane <= nparts) {
-      const int cb = lane * k / nparts;
-      cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + (cb < k ? tot[cb] : e - b);
+  if (threadIdx.x < k) {  // warp-major prefix per color + the chunk's row offset
+    int run = ccnt[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x];
+    for (int w = 0; w < 8; ++w) {
+      const int x = wc[w][threadIdx.x];
+      wc[w][threadIdx.x] = run;
+      run += x;
     }
   }
   __syncthreads();
-  for (int key = threadIdx.x; key < k; key += blockDim.x) {
-    int run = tot[key];
-    for (int w = 0; w < nw; ++w) {
-      const int c = bsm[w * k + key];
-      bsm[w * k + key] = run;
-      run += c;
-    }
-  }
-  __syncthreads();
+  int* cnt = wc[warp];
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
     const int u = ok ? col[j + lane] : 0;
@@ -649,7 +703,7 @@ bucket_long(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
     __syncwarp();
     if (ok) {
-      out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
+      out[rb + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
       if ((same & lt) == 0) cnt[key] += __popc(same);
     }
     __syncwarp();

@@ -40,14 +40,25 @@ vsort_count(const uint8_t* __restrict__ colors, int32_t n, int k, int* __restric
 // One CTA: per-(chunk, color) offsets (color-major, chunk order) in place,
 // and the tile table: tile t = {color, first sorted position, count}, tiles
 // numbered color by color; unused entries get color -1.
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(1024)
 vsort_scan(int* __restrict__ cnt, int nchunks, int k, int4* __restrict__ tiles, int max_tiles) {
+  // warp c scans color c's chunk counts (chunk order); then the tile table
   __shared__ int tot[32], start[33], tstart[33];
-  const int c = threadIdx.x;
-  if (c < k) {
-    int t = 0;
-    for (int b = 0; b < nchunks; ++b) t += cnt[b * k + c];
-    tot[c] = t;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  if (warp < k) {
+    int run = 0;
+    for (int b0 = 0; b0 < nchunks; b0 += 32) {
+      const int b = b0 + lane;
+      const int x = b < nchunks ? cnt[b * k + warp] : 0;
+      int incl = x;
+      for (int o = 1; o < 32; o <<= 1) {
+        const int y = __shfl_up_sync(0xffffffffu, incl, o);
+        if (lane >= o) incl += y;
+      }
+      if (b < nchunks) cnt[b * k + warp] = run + incl - x;  // color-local offset
+      run += __shfl_sync(0xffffffffu, incl, 31);
+    }
+    if (lane == 0) tot[warp] = run;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -58,14 +69,8 @@ vsort_scan(int* __restrict__ cnt, int nchunks, int k, int4* __restrict__ tiles, 
     }
   }
   __syncthreads();
-  if (c < k) {
-    int run = start[c];
-    for (int b = 0; b < nchunks; ++b) {
-      const int x = cnt[b * k + c];
-      cnt[b * k + c] = run;
-      run += x;
-    }
-  }
+  if (warp < k)
+    for (int b = lane; b < nchunks; b += 32) cnt[b * k + warp] += start[warp];
   for (int t = threadIdx.x; t < max_tiles; t += blockDim.x) {
     int cc = -1;
     for (int q = 0; q < k; ++q)
@@ -391,7 +396,7 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   __shared__ double red[kEmaWarps][kTileV];
   __shared__ int32_t vids[32];
   const int4 tile = tiles[blockIdx.x];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   if (tile.x < 0) {
     if (threadIdx.x == 0) tile_tot[blockIdx.x] = 0.0;
     return;
@@ -408,7 +413,7 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   if (ALEAF) {
     if (warp == 0) acc = static_cast<double>(sP[lane]);
   } else {
-    for (int p = warp; p < pairs; p += kEmaWarps) {
+    for (int p = warp; p < pairs; p += nw) {
       const int2 s = __ldg(split + p);
       acc = fma(static_cast<double>(sA[s.x * kSpitch + lane]), static_cast<double>(sP[s.y * kSpitch + lane]), acc);
     }
@@ -417,7 +422,7 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   __syncthreads();
   if (warp == 0) {
     double tot = 0;
-    for (int w = 0; w < kEmaWarps; ++w) tot += red[w][lane];
+    for (int w = 0; w < nw; ++w) tot += red[w][lane];
     const int v = vids[lane];
     if (v >= 0) {
       root_out[v] = tot;
