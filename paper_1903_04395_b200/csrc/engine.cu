@@ -649,10 +649,10 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     std::fprintf(stderr, "[tcg] k=%d nodes=%d rooted_ema=%d\n", k, plan_.num_nodes, rooted_ema_ ? 1 : 0);
     for (const auto& e : exec_)
       std::fprintf(stderr, "[tcg] node %2d (%2d,%2d,%2d) Cp=%d rooted=%d groups=%d zw=%d Cps=%d | Ws=%d Wa=%d Wp=%d Cout=%d "
-                           "%s pairs=%d blocked=%d/%d vtx=%d staged=%d dup_of=%d\n",
+                           "%s pairs=%d blocked=%d/%d vtx=%d/%d staged=%d dup_of=%d\n",
                    e.id, e.size, e.sa, e.sp, e.Cp, e.rooted ? 1 : 0, e.rl_groups, e.rl_zw, e.Cps, e.Ws, e.Wa, e.Wp,
                    e.Cout, e.omap.empty() ? "RR" : "RS", e.rt_pairs, e.rt_blocked ? 1 : 0, e.blocked ? 1 : 0,
-                   e.vtx ? 1 : 0, e.ema_staged ? 1 : 0, e.dup_of >= 0 ? exec_[e.dup_of].id : -1);
+                   e.vtx ? 1 : 0, e.rt_vtx ? 1 : 0, e.ema_staged ? 1 : 0, e.dup_of >= 0 ? exec_[e.dup_of].id : -1);
     for (const auto& e : exec_)
       if (e.pp_dup_of >= 0) std::fprintf(stderr, "[tcg] node %d shares the SpMM of node %d\n", e.id, exec_[e.pp_dup_of].id);
   }
@@ -687,11 +687,26 @@ void Engine::setup_rooted_ema(int max_smem) {
   const int k = plan_.k;
   if (!mode || exec_.empty() || k < 2) return;
   const Binom& B = binom();
-  for (const auto& e : exec_) {
+  static const int vtx_mode = [] {  // 2: every non-leaf node vertex-per-CTA (tests)
+    const char* s = std::getenv("TCG_RT_VTX");
+    return s ? std::atoi(s) : 1;
+  }();
+  auto row_floats = [](int64_t C) { return C <= 0 ? 0 : dev::table_floats(C, 1); };
+  for (auto& e : exec_) {
     if ((!e.p_leaf && !e.rooted) || e.lspmm) return;
     const int64_t Wa = e.a_leaf ? 0 : B(k - 1, e.sa - 1), Wp = B(k - 1, e.sp), Ws = e.root ? 1 : B(k - 1, e.size - 1);
     if (Wa >= 65536 || Wp >= 65536 || Ws >= 65536) return;
-    if ((Wa + Wp) * (dev::kTileV + 1) * 4 > max_smem - 4096) return;
+    e.rt_vtx = false;
+    if (e.a_leaf && !e.root) {  // ema_rt_copy: one P' row per vertex at least
+      if (4 * row_floats(e.p_leaf ? k : e.Cps) > max_smem - 4096) return;
+      continue;
+    }
+    const bool tile_fits = (Wa + Wp) * (dev::kTileV + 1) * 4 <= max_smem - 4096;
+    if (tile_fits && !(vtx_mode == 2 && !e.a_leaf && (e.root || k - 1 >= dev::kH1))) continue;
+    // vertex-per-CTA: the vertex's RR A row and its relabeled P row
+    if (!vtx_mode || e.a_leaf || (!e.root && k - 1 < dev::kH1)) return;
+    if (4 * (row_floats(Wa) + Wp + 4) > max_smem - 4096) return;
+    e.rt_vtx = true;
   }
   std::vector<int> parent(plan_.num_nodes, -1);
   for (size_t i = 0; i < exec_.size(); ++i) {
@@ -778,7 +793,7 @@ void Engine::setup_rooted_ema(int max_smem) {
         for (size_t i = 0; i < pk.size(); ++i)
           pk[i] = static_cast<uint32_t>(st.active_index[i]) | (static_cast<uint32_t>(st.passive_index[i]) << 16);
         e.d_rt_packed = dupload(pk, stream_);
-        if (blocked_mode && k - 1 >= dev::kH1 && (e.rt_pairs >= 16 || blocked_mode == 2)) {
+        if (e.rt_vtx || (blocked_mode && k - 1 >= dev::kH1 && (e.rt_pairs >= 16 || blocked_mode == 2))) {
           std::vector<dev::GroupDesc> gr;
           std::vector<dev::BlockDesc> bl;
           build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl);
@@ -788,6 +803,11 @@ void Engine::setup_rooted_ema(int max_smem) {
           e.d_rt_blocks = dupload(bl, stream_);
         }
       }
+    }
+    if (e.rt_vtx) {
+      e.rt_smem = static_cast<size_t>(4 * (row_floats(e.Wa) + e.Wp));
+      dfree(e.d_imap);
+      continue;
     }
     // (+ the RS output tile of the generic node kernel, when it fits)
     e.rt_smem = static_cast<size_t>(e.Wa + e.Wp) * (dev::kTileV + 1) * 4;
@@ -1278,6 +1298,21 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   auto attr = [&](const void* f) {
     TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_smem)));
   };
+  if (e.rt_vtx) {
+    const unsigned vgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n_, 148 * 16)));
+    if (e.root) {
+      double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
+      attr(reinterpret_cast<const void*>(dev::ema_rtv_root));
+      dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
+                                                             e.rt_pairs, n_, rout, d_root_acc);
+    } else {
+      attr(reinterpret_cast<const void*>(dev::ema_rtv_blocked));
+      dev::ema_rtv_blocked<<<vgrid, 256, e.rt_smem, stream_>>>(
+          A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+          static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off));
+    }
+    return;
+  }
   if (e.root) {
     double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
     const int rwarps = std::max(2, std::min(dev::kEmaWarps, e.rt_pairs / 4));  // warps split the pairs
@@ -1499,7 +1534,10 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
   }
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   if (n_ > 0 && !exec_.empty()) {
-    if (rooted_ema_)
+    if (rooted_ema_ && exec_.back().rt_vtx)  // per-vertex values only
+      dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
+                                                n_, d_total);
+    else if (rooted_ema_)
       dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, max_tiles_, d_total);
     else if (exec_.back().vtx)  // vertex-per-CTA root wrote per-vertex values only
       dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),

@@ -81,6 +81,7 @@ struct NodeExec {
   void* d_rt_blocks = nullptr;
   int rt_ngroups = 0;
   size_t rt_smem = 0;
+  bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int dup_of = -1;                // exec index of an identical earlier node (table aliased)
   int pp_dup_of = -1;             // exec index of an earlier node with the same P' (SpMM skipped)
 };

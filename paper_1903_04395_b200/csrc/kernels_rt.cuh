@@ -435,5 +435,125 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, 
   }
 }
 
+// ------------------------------------------- vertex-per-CTA rooted eMA
+// Nodes whose 32-vertex tile does not fit in shared memory (k = 15/17: cfg5
+// node 1 stages C(16,7) + C(16,4) floats per vertex) run the rooted (k-1)
+// problem one vertex per CTA: the vertex's RR active row and its P' row,
+// mapped to relabeled indices through the vertex color's pmap, are staged
+// contiguously in smem and the threads split the output groups of the
+// register-blocked descriptors (build_blocked(k-1, s-1, a-1)).  a/k of the
+// full-table FMAs, s/k of its table bytes.
+
+// P' row of vertex v (Cpt storage columns) -> dst[pm[col]] (relabeled index;
+// -1: the column contains the vertex color and is never used)
+__device__ __forceinline__ void stage_row_pmap(const float* __restrict__ T, int Cpt, int32_t n, int64_t v,
+                                               float* dst, const int32_t* __restrict__ pm) {
+  const int panels = num_panels(Cpt);
+  const int zl = last_panel_width(Cpt);
+  const int total4 = ((panels - 1) * kZ + zl) / 4;
+  for (int f = threadIdx.x; f < total4; f += blockDim.x) {
+    const int c0 = f * 4;
+    if (c0 >= Cpt) continue;
+    const int p = c0 / kZ, z4 = c0 % kZ;
+    const int zw = p == panels - 1 ? zl : kZ;
+    const float4 x = __ldg(reinterpret_cast<const float4*>(T + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
+    const int m0 = __ldg(pm + c0);
+    const int m1 = c0 + 1 < Cpt ? __ldg(pm + c0 + 1) : -1;
+    const int m2 = c0 + 2 < Cpt ? __ldg(pm + c0 + 2) : -1;
+    const int m3 = c0 + 3 < Cpt ? __ldg(pm + c0 + 3) : -1;
+    if (m0 >= 0) dst[m0] = x.x;
+    if (m1 >= 0) dst[m1] = x.y;
+    if (m2 >= 0) dst[m2] = x.z;
+    if (m3 >= 0) dst[m3] = x.w;
+  }
+}
+
+#define TCG_IJRV(I, J) \
+  case I * 8 + J: micro_block_v<I, J>(sA + bd.x, sP + bd.y, acc); break;
+
+__global__ void __launch_bounds__(256)
+ema_rtv_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
+                const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
+                const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks, int Ws,
+                const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  float* sA = smem;
+  float* sP = smem + row_floats(Wa);
+  const int T = blockDim.x;
+  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    const int c = colors[v];
+    __syncthreads();
+    stage_row(Am, Wa, n, v, sA);
+    stage_row_pmap(Pm, Cpt, n, v, sP, pmap + static_cast<int64_t>(c) * Cpt);
+    __syncthreads();
+    const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
+    for (int r = 0;; ++r) {
+      const int gi = (r & 1) ? (r + 1) * T - 1 - static_cast<int>(threadIdx.x) : r * T + static_cast<int>(threadIdx.x);
+      if (r * T >= ngroups) break;
+      if (gi >= ngroups) continue;
+      const GroupDesc gd = groups[gi];
+      float acc[kMaxAcc];
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
+      for (int b = gd.b0; b < gd.b1; ++b) {
+        const BlockDesc b4 = blocks[b];
+        const int2 bd = make_int2(b4.a_off, b4.p_off);
+        switch (b4.ij) {
+          TCG_IJRV(0, 1) TCG_IJRV(0, 2) TCG_IJRV(0, 3) TCG_IJRV(0, 4) TCG_IJRV(0, 5) TCG_IJRV(0, 6)
+          TCG_IJRV(1, 0) TCG_IJRV(1, 1) TCG_IJRV(1, 2) TCG_IJRV(1, 3) TCG_IJRV(1, 4) TCG_IJRV(1, 5)
+          TCG_IJRV(2, 0) TCG_IJRV(2, 1) TCG_IJRV(2, 2) TCG_IJRV(2, 3) TCG_IJRV(2, 4)
+          TCG_IJRV(3, 0) TCG_IJRV(3, 1) TCG_IJRV(3, 2) TCG_IJRV(3, 3)
+          TCG_IJRV(4, 0) TCG_IJRV(4, 1) TCG_IJRV(4, 2)
+          TCG_IJRV(5, 0) TCG_IJRV(5, 1)
+          TCG_IJRV(6, 0) TCG_IJRV(0, 0)
+          default: break;
+        }
+      }
+      const int cnt = cbin(kH1, gd.s1);
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x)
+        if (x < cnt) {
+          const int col = gd.out_off + x;
+          out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
+        }
+    }
+  }
+}
+#undef TCG_IJRV
+
+// Root, one vertex per CTA: fp64 dot product over the relabeled split pairs,
+// fixed-order block reduction -> root_out[v] (root_reduce then sums root_out).
+__global__ void __launch_bounds__(256)
+ema_rtv_root(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
+             const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors, const int2* __restrict__ split,
+             int pairs, int32_t n, double* __restrict__ root_out, double* __restrict__ root_acc) {
+  extern __shared__ float smem[];
+  __shared__ double red[256];
+  float* sA = smem;
+  float* sP = smem + row_floats(Wa);
+  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
+    const int c = colors[v];
+    __syncthreads();
+    stage_row(Am, Wa, n, v, sA);
+    stage_row_pmap(Pm, Cpt, n, v, sP, pmap + static_cast<int64_t>(c) * Cpt);
+    __syncthreads();
+    double acc = 0;
+    for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
+      const int2 s = __ldg(split + p);
+      acc = fma(static_cast<double>(sA[s.x]), static_cast<double>(sP[s.y]), acc);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o; o >>= 1) {
+      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      root_out[v] = red[0];
+      if (root_acc) root_acc[v] += red[0];
+    }
+  }
+}
+
 }  // namespace dev
 }  // namespace tcg

@@ -1,0 +1,5 @@
+# rooted vertex-per-CTA eMA: parity + cfg5 timing
+set -x
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests/test_gpu_modes.py tests/test_gpu_parity.py -x -q -m gpu -k "modes or k15 or large_k or node_tables or cfg1" 2>&1 | tail -15
+TCG_VERBOSE=1 timeout 600 python tools/prof_driver.py --config cfg5 --colorings 1 --stats 2>&1 | tail -60
