@@ -83,9 +83,10 @@ int64_t h2_offset(uint32_t x2, int i) {
 }
 
 // Output groups and blocks of the color-split eMA for a node (s, a) with k colors.
+// h1: colors of the register-blocked H1 (pattern code i * shift + j)
 void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
-                   std::vector<dev::BlockDesc>& blocks) {
-  const int h1 = dev::kH1, p = s - a;
+                   std::vector<dev::BlockDesc>& blocks, int h1 = dev::kH1, int shift = 8) {
+  const int p = s - a;
   struct G { dev::GroupDesc d; int64_t work; std::vector<dev::BlockDesc> b; };
   std::vector<G> gs;
   const uint32_t h2mask = (k >= 32 ? ~0u : ((1u << k) - 1)) & ~((1u << h1) - 1);
@@ -105,7 +106,7 @@ void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
           if (__builtin_popcount(a2) == ac) {
             const uint32_t p2 = s2 & ~a2;
             g.b.push_back(dev::BlockDesc{static_cast<int32_t>(h2_offset(a2, i)),
-                                         static_cast<int32_t>(h2_offset(p2, j)), i * 8 + j, 0});
+                                         static_cast<int32_t>(h2_offset(p2, j)), i * shift + j, 0});
             g.work += dev::cbin(h1, i) * dev::cbin(h1 - i, j);
           }
           if (a2 == s2) break;
@@ -272,6 +273,7 @@ void Engine::release_template() {
     dfree(e.d_rt_split);
     dfree(e.d_rt_groups);
     dfree(e.d_rt_blocks);
+    dfree(e.d_rtv_blocks);
   }
   exec_.clear();
   dfree(arena_);
@@ -796,7 +798,21 @@ void Engine::setup_rooted_ema(int max_smem) {
         if (e.rt_vtx || (blocked_mode && k - 1 >= dev::kH1 && (e.rt_pairs >= 16 || blocked_mode == 2))) {
           std::vector<dev::GroupDesc> gr;
           std::vector<dev::BlockDesc> bl;
-          build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl);
+          if (e.rt_vtx) {  // vertex-per-CTA: the widest H1 the (k-1) colors allow (<= 8)
+            static const int hmax = [] {
+              const char* s = std::getenv("TCG_RTV_H");
+              return s ? std::atoi(s) : 6;
+            }();
+            e.rtv_h = std::max(dev::kH1, std::min(hmax, k - 1));
+            build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl, e.rtv_h, 16);
+            std::vector<uint2> b2(bl.size());  // packed 8 B descriptors
+            for (size_t i = 0; i < bl.size(); ++i)
+              b2[i] = make_uint2(static_cast<uint32_t>(bl[i].a_off) | (static_cast<uint32_t>(bl[i].p_off) << 16),
+                                 static_cast<uint32_t>(bl[i].ij) | (static_cast<uint32_t>(bl[i].pad) << 8));
+            e.d_rtv_blocks = dupload(b2, stream_);
+          } else {
+            build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl);
+          }
           e.rt_blocked = true;
           e.rt_ngroups = static_cast<int>(gr.size());
           e.d_rt_groups = dupload(gr, stream_);
@@ -805,7 +821,18 @@ void Engine::setup_rooted_ema(int max_smem) {
       }
     }
     if (e.rt_vtx) {
-      e.rt_smem = static_cast<size_t>(4 * (row_floats(e.Wa) + e.Wp));
+      if (e.root) {
+        e.rt_smem = static_cast<size_t>(4 * (row_floats(e.Wa) + e.Wp));
+      } else {  // V vertices per pass: two CTAs per SM when V >= 2 fits
+        auto stride = [](int64_t f, int V) { return (f + 31) / 32 * 32 + (V > 1 ? 32 / V : 0); };
+        const int64_t half = (max_smem - 4096) / 2;
+        int V = 8;
+        while (V > 1 && 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) > half) V /= 2;
+        e.rtv_V = V;
+        e.rtv_sa = static_cast<int>(stride(row_floats(e.Wa), V));
+        e.rtv_sp = static_cast<int>(stride(e.Wp, V));
+        e.rt_smem = static_cast<size_t>(4 * V * (e.rtv_sa + e.rtv_sp));
+      }
       dfree(e.d_imap);
       continue;
     }
@@ -1299,17 +1326,20 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_smem)));
   };
   if (e.rt_vtx) {
-    const unsigned vgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n_, 148 * 16)));
+    const unsigned vgrid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>((n_ + e.rtv_V - 1) / e.rtv_V, e.root ? 148 * 16 : 148 * 2 * 8)));
     if (e.root) {
       double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
       attr(reinterpret_cast<const void*>(dev::ema_rtv_root));
       dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
-      attr(reinterpret_cast<const void*>(dev::ema_rtv_blocked));
-      dev::ema_rtv_blocked<<<vgrid, 256, e.rt_smem, stream_>>>(
+      auto kern = e.rtv_h == 8 ? dev::ema_rtv_blocked<8> : e.rtv_h == 7 ? dev::ema_rtv_blocked<7> : dev::ema_rtv_blocked<6>;
+      attr(reinterpret_cast<const void*>(kern));
+      kern<<<vgrid, 256, e.rt_smem, stream_>>>(
           A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
-          static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off));
+          static_cast<const uint2*>(e.d_rtv_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V,
+          e.rtv_sa, e.rtv_sp);
     }
     return;
   }

@@ -82,6 +82,8 @@ struct NodeExec {
   int rt_ngroups = 0;
   size_t rt_smem = 0;
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
+  int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
+  void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)  // vertices per pass, their smem row strides
   int dup_of = -1;                // exec index of an identical earlier node (table aliased)
   int pp_dup_of = -1;             // exec index of an earlier node with the same P' (SpMM skipped)
 };

@@ -468,58 +468,141 @@ __device__ __forceinline__ void stage_row_pmap(const float* __restrict__ T, int 
   }
 }
 
-#define TCG_IJRV(I, J) \
-  case I * 8 + J: micro_block_v<I, J>(sA + bd.x, sP + bd.y, acc); break;
+// ---- H-colour register blocking (H = 6/7/8), generic over H: the
+// H1-subset micro-patterns (i, j) of build_blocked(k', s', a', H), pattern
+// code i * 16 + j.  Triples (a1, p1, a1|p1) of a pattern are one constexpr
+// table per (H, i, j).
+template <int H, int I, int J>
+struct TripTab {
+  static constexpr int NT = cbin(H, I) * cbin(H - I, J);
+  struct Arr { Trip t[NT > 0 ? NT : 1]; };
+  static constexpr int rank(unsigned m) {
+    int idx = 0, pos = 0;
+    for (int c = 0; c < H; ++c)
+      if (m >> c & 1u) idx += cbin(c, ++pos);
+    return idx;
+  }
+  static constexpr Arr make() {
+    Arr r{};
+    int n = 0;
+    for (unsigned am = 0; am < (1u << H); ++am) {
+      if (cpop(am) != I) continue;
+      for (unsigned pm = 0; pm < (1u << H); ++pm)
+        if (cpop(pm) == J && !(am & pm)) r.t[n++] = Trip{rank(am), rank(pm), rank(am | pm)};
+    }
+    return r;
+  }
+  static constexpr Arr tab = make();
+};
 
-__global__ void __launch_bounds__(256)
+template <int H, int I, int J, int... T>
+__device__ __forceinline__ void micro_fma_h(const float* a, const float* p, float* acc,
+                                            std::integer_sequence<int, T...>) {
+  ((acc[TripTab<H, I, J>::tab.t[T].o] =
+        fmaf(a[TripTab<H, I, J>::tab.t[T].a], p[TripTab<H, I, J>::tab.t[T].p], acc[TripTab<H, I, J>::tab.t[T].o])),
+   ...);
+}
+
+template <int H, int I, int J>
+__device__ __forceinline__ void micro_block_h(const float* __restrict__ sa, const float* __restrict__ sp,
+                                              float* acc) {
+  if constexpr (I + J <= H) {
+    constexpr int NA = cbin(H, I), NP = cbin(H, J);
+    float a[NA], p[NP];
+#pragma unroll
+    for (int x = 0; x < NA; ++x) a[x] = sa[x];
+#pragma unroll
+    for (int x = 0; x < NP; ++x) p[x] = sp[x];
+    micro_fma_h<H, I, J>(a, p, acc, std::make_integer_sequence<int, TripTab<H, I, J>::NT>{});
+  }
+}
+
+// one run of blocks with the same pattern (I, J): descriptors {a_off | p_off << 16}
+// prefetched one block ahead
+#define TCG_HC(I, J)                                                                 \
+  case I * 16 + J: {                                                                 \
+    uint32_t d = h.x;                                                                \
+    for (int q = 1;; ++q) {                                                          \
+      const uint32_t dn = q < len ? __ldg(&blocks[b + q].x) : 0u;                    \
+      micro_block_h<H, I, J>(sA + (d & 0xFFFFu), sP + (d >> 16), acc);               \
+      if (q >= len) break;                                                           \
+      d = dn;                                                                        \
+    }                                                                                \
+  } break;
+#define TCG_HCASES                                                                                        \
+  TCG_HC(0, 0) TCG_HC(0, 1) TCG_HC(0, 2) TCG_HC(0, 3) TCG_HC(0, 4) TCG_HC(0, 5) TCG_HC(0, 6) TCG_HC(0, 7) \
+  TCG_HC(0, 8) TCG_HC(1, 0) TCG_HC(1, 1) TCG_HC(1, 2) TCG_HC(1, 3) TCG_HC(1, 4) TCG_HC(1, 5) TCG_HC(1, 6) \
+  TCG_HC(1, 7) TCG_HC(2, 0) TCG_HC(2, 1) TCG_HC(2, 2) TCG_HC(2, 3) TCG_HC(2, 4) TCG_HC(2, 5) TCG_HC(2, 6) \
+  TCG_HC(3, 0) TCG_HC(3, 1) TCG_HC(3, 2) TCG_HC(3, 3) TCG_HC(3, 4) TCG_HC(3, 5) TCG_HC(4, 0) TCG_HC(4, 1) \
+  TCG_HC(4, 2) TCG_HC(4, 3) TCG_HC(4, 4) TCG_HC(5, 0) TCG_HC(5, 1) TCG_HC(5, 2) TCG_HC(5, 3) TCG_HC(6, 0) \
+  TCG_HC(6, 1) TCG_HC(6, 2) TCG_HC(7, 0) TCG_HC(7, 1) TCG_HC(8, 0)
+
+// V vertices per pass (staged at strides sa/sp floats, == 32/V mod 32 so the
+// V lanes sharing a group hit different banks).  Work items (group, vertex)
+// are ordered group-major over groups sorted by work; warps take TASKS of 32
+// consecutive items from a per-pass queue (largest first), so a warp runs
+// 32/V groups of one shape (convergent pattern dispatch, shared descriptors)
+// and the pass ends balanced.  Blocks come in runs of one pattern: packed
+// 8 B descriptors {a_off | p_off << 16, pattern | run length << 8 (at the
+// run's first block)}, one dispatch per run.
+template <int H>
+__global__ void __launch_bounds__(256, 2)
 ema_rtv_blocked(const float* __restrict__ Am, int Wa, const float* __restrict__ Pm, int Cpt,
                 const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
-                const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks, int Ws,
-                const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out) {
+                const GroupDesc* __restrict__ groups, int ngroups, const uint2* __restrict__ blocks, int Ws,
+                const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out, int V, int sa,
+                int sp) {
+  constexpr int kAcc = cbin(H, H / 2);
   extern __shared__ float smem[];
-  float* sA = smem;
-  float* sP = smem + row_floats(Wa);
-  const int T = blockDim.x;
-  for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
-    const int c = colors[v];
+  __shared__ int next_task;
+  float* sP0 = smem + V * sa;
+  const int lane = threadIdx.x & 31;
+  const int items = ngroups * V;
+  const int ntasks = (items + 31) / 32;
+  for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * V; v0 < n; v0 += static_cast<int64_t>(gridDim.x) * V) {
     __syncthreads();
-    stage_row(Am, Wa, n, v, sA);
-    stage_row_pmap(Pm, Cpt, n, v, sP, pmap + static_cast<int64_t>(c) * Cpt);
+    if (threadIdx.x == 0) next_task = blockDim.x >> 5;
+    for (int j = 0; j < V && v0 + j < n; ++j) {
+      stage_row(Am, Wa, n, v0 + j, smem + j * sa);
+      stage_row_pmap(Pm, Cpt, n, v0 + j, sP0 + j * sp, pmap + static_cast<int64_t>(colors[v0 + j]) * Cpt);
+    }
     __syncthreads();
-    const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
-    for (int r = 0;; ++r) {
-      const int gi = (r & 1) ? (r + 1) * T - 1 - static_cast<int>(threadIdx.x) : r * T + static_cast<int>(threadIdx.x);
-      if (r * T >= ngroups) break;
-      if (gi >= ngroups) continue;
-      const GroupDesc gd = groups[gi];
-      float acc[kMaxAcc];
+    for (int task = threadIdx.x >> 5; task < ntasks;) {
+      const int it = task * 32 + lane;
+      const int gi = it / V, j = it - gi * V;
+      const int64_t v = v0 + j;
+      if (it < items && v < n) {
+        const float* sA = smem + j * sa;
+        const float* sP = sP0 + j * sp;
+        const GroupDesc gd = groups[gi];
+        float acc[kAcc];
 #pragma unroll
-      for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
-      for (int b = gd.b0; b < gd.b1; ++b) {
-        const BlockDesc b4 = blocks[b];
-        const int2 bd = make_int2(b4.a_off, b4.p_off);
-        switch (b4.ij) {
-          TCG_IJRV(0, 1) TCG_IJRV(0, 2) TCG_IJRV(0, 3) TCG_IJRV(0, 4) TCG_IJRV(0, 5) TCG_IJRV(0, 6)
-          TCG_IJRV(1, 0) TCG_IJRV(1, 1) TCG_IJRV(1, 2) TCG_IJRV(1, 3) TCG_IJRV(1, 4) TCG_IJRV(1, 5)
-          TCG_IJRV(2, 0) TCG_IJRV(2, 1) TCG_IJRV(2, 2) TCG_IJRV(2, 3) TCG_IJRV(2, 4)
-          TCG_IJRV(3, 0) TCG_IJRV(3, 1) TCG_IJRV(3, 2) TCG_IJRV(3, 3)
-          TCG_IJRV(4, 0) TCG_IJRV(4, 1) TCG_IJRV(4, 2)
-          TCG_IJRV(5, 0) TCG_IJRV(5, 1)
-          TCG_IJRV(6, 0) TCG_IJRV(0, 0)
-          default: break;
+        for (int x = 0; x < kAcc; ++x) acc[x] = 0.f;
+        for (int b = gd.b0; b < gd.b1;) {
+          const uint2 h = __ldg(blocks + b);
+          const int len = static_cast<int>(h.y >> 8);
+          switch (h.y & 0xFFu) {
+            TCG_HCASES
+            default: break;
+          }
+          b += len;
         }
+        const int32_t* om = omap ? omap + static_cast<int64_t>(colors[v]) * Ws : nullptr;
+        const int cnt = cbin(H, gd.s1);
+#pragma unroll
+        for (int x = 0; x < kAcc; ++x)
+          if (x < cnt) {
+            const int col = gd.out_off + x;
+            out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
+          }
       }
-      const int cnt = cbin(kH1, gd.s1);
-#pragma unroll
-      for (int x = 0; x < kMaxAcc; ++x)
-        if (x < cnt) {
-          const int col = gd.out_off + x;
-          out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
-        }
+      if (lane == 0) task = atomicAdd(&next_task, 1);
+      task = __shfl_sync(0xffffffffu, task, 0);
     }
   }
 }
-#undef TCG_IJRV
+#undef TCG_HC
+#undef TCG_HCASES
 
 // Root, one vertex per CTA: fp64 dot product over the relabeled split pairs,
 // fixed-order block reduction -> root_out[v] (root_reduce then sums root_out).

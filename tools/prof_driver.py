@@ -14,8 +14,11 @@ ap.add_argument("--config", default="cfg3")
 ap.add_argument("--warmup", type=int, default=1)
 ap.add_argument("--colorings", type=int, default=1)
 ap.add_argument("--stats", action="store_true", help="print per-node device times")
+ap.add_argument("--scale", type=int, default=0, help="override the R-MAT scale (edge factor kept)")
 a = ap.parse_args()
 spec, parents, _, _ = bench.CONFIGS[a.config]
+if a.scale:
+    spec = (a.scale, (spec[1] >> spec[0]) << a.scale) + tuple(spec[2:])
 g = T.generate_rmat(T.RmatSpec(*spec))
 t = T.template_from_parents(parents, 0)
 ctx = T.Context(0)
