@@ -35,6 +35,9 @@ CONFIGS = {
              "R-MAT scale 20 ef16 (.57,.19,.19,.05), k=7 complete binary tree"),
     "cfg3": ((20, 100 << 20, .45, .15, .15, .25, 1), [-1, 0, 1, 2, 0, 4, 4, 6, 0, 8, 9, 9], 3,
              "R-MAT scale 20 ef100 (.45,.15,.15,.25), k=12 tree"),
+    "cfg4": ((22, 32 << 22, .57, .19, .19, .05, 1),
+             [-1, 0, 1, 2, 3, 0, 5, 6, 0, 8, 8, 10, 10, 12, 13], 2,
+             "R-MAT scale 22 ef32 (.57,.19,.19,.05), k=15 tree"),
     "cfg5": ((20, 100 << 20, .45, .15, .15, .25, 1),
              [-1, 0, 1, 2, 3, 4, 0, 6, 7, 8, 0, 10, 11, 11, 0, 14, 15], 1,
              "R-MAT scale 20 ef100 (.45,.15,.15,.25), k=17 tree"),

@@ -274,6 +274,8 @@ void Engine::release_template() {
     dfree(e.d_rt_groups);
     dfree(e.d_rt_blocks);
     dfree(e.d_rtv_blocks);
+    dfree(e.d_emap);
+    dfree(e.d_amap);
   }
   exec_.clear();
   dfree(arena_);
@@ -782,6 +784,42 @@ void Engine::setup_rooted_ema(int max_smem) {
           if (i >= 0) cm[static_cast<size_t>(c) * e.Cout + i] = src;
         }
       e.d_cmap = dupload(cm, stream_);
+      if (!e.p_leaf) {
+        // streamed SpMM epilogue (pstream_copy): P' storage column -> output
+        // column.  RS outputs: the slot.  RR outputs are stored PACKED in P'
+        // storage order instead (column q = rank of the storage column among
+        // those without c), so each group lands on a contiguous run of the
+        // row; the consumer stages them through amap [k][Ws]: q -> RR column.
+        std::vector<int32_t> em(static_cast<size_t>(k) * e.Cps, -1);
+        if (e.omap.empty()) {
+          std::vector<int32_t> am(static_cast<size_t>(k) * e.Ws, -1);
+          std::vector<int32_t> rr_of(e.Cps);
+          for (int c = 0; c < k; ++c) {
+            std::fill(rr_of.begin(), rr_of.end(), -1);
+            for (int32_t i = 0; i < e.Cout; ++i) {
+              const int32_t src = cm[static_cast<size_t>(c) * e.Cout + i];
+              if (src >= 0) rr_of[src] = i;
+            }
+            int32_t q = 0;
+            for (int32_t x = 0; x < e.Cps; ++x)
+              if (rr_of[x] >= 0) {
+                em[static_cast<size_t>(c) * e.Cps + x] = q;
+                am[static_cast<size_t>(c) * e.Ws + q] = rr_of[x];
+                ++q;
+              }
+            if (q != e.Ws) throw logic_error("packed active-leaf layout does not cover the rooted columns");
+          }
+          e.amap_host = am;
+          e.d_amap = dupload(am, stream_);
+        } else {
+          for (int c = 0; c < k; ++c)
+            for (int32_t i = 0; i < e.Cout; ++i) {
+              const int32_t src = cm[static_cast<size_t>(c) * e.Cout + i];
+              if (src >= 0) em[static_cast<size_t>(c) * e.Cps + src] = i;
+            }
+        }
+        e.d_emap = dupload(em, stream_);
+      }
     }
     if (!e.a_leaf) {
       const SplitTable st = build_split_table(k - 1, e.root ? k - 1 : e.size - 1, e.sa - 1);
@@ -847,8 +885,28 @@ void Engine::setup_rooted_ema(int max_smem) {
   rooted_ema_ = true;
 }
 
+// Streamed active-leaf SpMMs (NodeExec::pstream) trade the full P' for a
+// per-group scatter: used when the plan with full P' tables does not fit the
+// device (or the memory budget).  TCG_PSTREAM: 0 never, 1 when needed
+// (default), 2 always (also with TCG_KEEP_TABLES; tests).
 void Engine::plan_arena() {
+  static const int pstream_mode = [] {
+    const char* s = std::getenv("TCG_PSTREAM");
+    return s ? std::atoi(s) : 1;
+  }();
+  plan_arena_once(pstream_mode == 2);
+  if (pstream_mode == 1 && !(cfg_.flags & TCG_KEEP_TABLES)) {
+    size_t fr = 0, tot = 0;
+    TCG_CUDA(cudaMemGetInfo(&fr, &tot));
+    int64_t limit = static_cast<int64_t>(fr) + (arena_ ? arena_alloc_ : 0) - partial_bytes_ - (3ll << 30);
+    if (cfg_.memory_budget > 0) limit = std::min<int64_t>(limit, cfg_.memory_budget);
+    if (arena_bytes_ > limit) plan_arena_once(true);
+  }
+}
+
+void Engine::plan_arena_once(bool allow_stream) {
   const bool keep = cfg_.flags & TCG_KEEP_TABLES;
+  for (auto& e : exec_) e.pstream = false;
   ArenaPlanner ap;
   table_off_.assign(plan_.num_nodes, -1);
   pprime_off_.assign(plan_.num_nodes, -1);
@@ -909,6 +967,26 @@ void Engine::plan_arena() {
       }
       continue;
     }
+    e.pstream = false;
+    if (allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.d_emap && e.pp_dup_of < 0) {
+      bool shared = false;
+      for (const auto& y : exec_) shared |= y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id;
+      e.pstream = !shared;
+    }
+    if (e.pstream) {  // scratch for one group's P' columns + the output; M_p read meanwhile
+      e.Ct = 0;
+      for (int g = 0; g < e.rl_groups; ++g)
+        e.Ct = std::max(e.Ct, (g + 1 < e.rl_groups ? e.rl_fbase[g + 1] : e.Cps) - e.rl_fbase[g]);
+      e.pp_off = ap.alloc(table_bytes(e.Ct));
+      pprime_off_[e.p] = -1;
+      e.out_off = ap.alloc(table_bytes(e.Cout));
+      table_off_[e.id] = e.out_off;
+      for (const auto& y : exec_)
+        if (y.dup_of >= 0 && exec_[y.dup_of].id == e.id) ap.retain(e.out_off);
+      if (!keep) ap.free(table_off_[e.p]);
+      ap.free(e.pp_off);
+      continue;
+    }
     if (e.pp_dup_of >= 0) {  // P' identical to an earlier node's: alias it
       e.pp_off = exec_[e.pp_dup_of].pp_off;
       pprime_off_[e.p] = e.pp_off;
@@ -959,6 +1037,16 @@ void Engine::plan_arena() {
       if (!e.p_leaf) ap.free(e.pp_off);
       if (!e.a_leaf) ap.free(table_off_[e.a]);
     }
+  }
+  // consumers of a packed (streamed, RR) active table stage it through its amap
+  for (auto& e : exec_) {
+    e.d_amap_in = nullptr;
+    if (e.a_leaf) continue;
+    for (const auto& x : exec_)
+      if (x.id == e.a) {
+        const NodeExec& src = x.dup_of >= 0 ? exec_[x.dup_of] : x;
+        if (src.pstream && src.omap.empty()) e.d_amap_in = src.d_amap;
+      }
   }
   arena_bytes_ = ap.peak;
   partial_bytes_ = std::max<int64_t>(std::max<int64_t>(static_cast<int64_t>(max_slots_), lslots) * dev::kZ * 8,
@@ -1213,7 +1301,7 @@ void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
 // Rooted-color compressed SpMM (host.hpp RootedLayout, kernels.cuh): compress
 // M_p to its color-rooted slots, then one pass per (group, part) over the
 // (part, color)-sorted rows, each producing the group's P' columns.
-void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors) {
+void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out) {
   const int zw = e.rl_zw, G = e.rl_groups;
   const float* X = rooted_ema_ ? M : table_ptr(e.ct_off);
   if (!rooted_ema_) {
@@ -1246,8 +1334,10 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
       tr_->allgather(Xg, sizeof(float) * static_cast<size_t>(n_) * zw, d_xfull_, stream_);
       Xg = d_xfull_;
     }
-    const int fbase = e.rl_fbase[g];
-    const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - fbase;
+    const int gbase = e.rl_fbase[g];
+    const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - gbase;
+    const int fbase = out ? 0 : gbase;       // streamed: the group's columns at 0 of the scratch
+    const int32_t Cst = out ? e.Ct : e.Cps;
     const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * fpad * 4;
     const int16_t* sl = e.d_slot_acc + static_cast<int64_t>(g) * zw;
     int slot_stride = G * zw;
@@ -1259,16 +1349,22 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
       void* args[] = {const_cast<dev::Seg**>(&ps.d_segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
                       const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
                       const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
-                      const_cast<int*>(&fpad), const_cast<int32_t*>(&e.Cps), &n_, &Pp, &d_partial_,
+                      const_cast<int*>(&fpad), const_cast<int32_t*>(&Cst), &n_, &Pp, &d_partial_,
                       const_cast<int*>(&first)};
       TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {
         const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * fpad;
         dev::rooted_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
-            ps.d_split_rows, ps.d_slot_begin, ps.nsplit_rows, d_partial_, fbase, fpad, e.Cps, n_, Pp, first);
+            ps.d_split_rows, ps.d_slot_begin, ps.nsplit_rows, d_partial_, fbase, fpad, Cst, n_, Pp, first);
         ++launches_;
       }
+    }
+    if (out) {  // the group's P' columns are complete: scatter into the active-leaf output
+      const int64_t total = static_cast<int64_t>(n_) * fpad;
+      dev::pstream_copy<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 64)), 256, 0, stream_>>>(
+          Pp, e.Ct, fpad, e.d_emap + gbase, e.Cps, d_colors, e.Cout, n_, out);
+      ++launches_;
     }
   }
   TCG_CUDA(cudaGetLastError());
@@ -1331,13 +1427,13 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     if (e.root) {
       double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
       attr(reinterpret_cast<const void*>(dev::ema_rtv_root));
-      dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
+      dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
       auto kern = e.rtv_h == 8 ? dev::ema_rtv_blocked<8> : e.rtv_h == 7 ? dev::ema_rtv_blocked<7> : dev::ema_rtv_blocked<6>;
       attr(reinterpret_cast<const void*>(kern));
       kern<<<vgrid, 256, e.rt_smem, stream_>>>(
-          A, e.Wa, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
           static_cast<const uint2*>(e.d_rtv_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V,
           e.rtv_sa, e.rtv_sp);
     }
@@ -1349,11 +1445,11 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     if (e.a_leaf) {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<true>));
       dev::ema_rt_root<true><<<grid, 64, e.rt_smem, stream_>>>(
-          A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     } else {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<false>));
       dev::ema_rt_root<false><<<grid, rwarps * 32, e.rt_smem, stream_>>>(
-          A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     }
     return;
   }
@@ -1371,12 +1467,12 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
     dev::ema_rt_blocked<<<grid, 256, e.rt_smem, stream_>>>(
-        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+        A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
         static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, out);
   } else {
     attr(reinterpret_cast<const void*>(dev::ema_rt_node<false>));
     dev::ema_rt_node<false><<<grid, warps * 32, e.rt_smem, stream_>>>(
-        A, e.Wa, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);
+        A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);
   }
 }
 
@@ -1485,6 +1581,8 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
         for (auto& x : exec_)
           if (x.id == e.p) c = &x;
         lspmm(e, c->p_leaf ? H : table_ptr(c->pp_off), table_ptr(e.pp_off));
+      } else if (e.rooted && e.pstream) {
+        rooted_spmm(e, table_ptr(table_off_[e.p]), table_ptr(e.pp_off), d_colors, table_ptr(e.out_off));
       } else if (e.rooted) {
         rooted_spmm(e, table_ptr(table_off_[e.p]), table_ptr(e.pp_off), d_colors);
       } else {
@@ -1502,7 +1600,9 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     size_t q0 = 0;
     if (prof_) { q0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
     const float* A = e.a_leaf ? nullptr : table_ptr(table_off_[e.a]);
-    if (n_ > 0 && rooted_ema_) {
+    if (n_ > 0 && rooted_ema_ && e.pstream) {
+      // (the SpMM wrote the output)
+    } else if (n_ > 0 && rooted_ema_) {
       launch_rt_ema(e, A, P, d_root_acc);
       ++launches_;
       TCG_CUDA(cudaGetLastError());
@@ -1846,12 +1946,17 @@ void Engine::node_table(int id, int which, double* out) {
         set_of(plan_.k, S, s, cs);
         for (int j = 0; j < s; ++j) rel[static_cast<size_t>(S) * k + cs[j]] = relabeled_index(cs, s, cs[j]);
       }
+      std::vector<int32_t> qof(e.amap_host.size());
+      for (int c = 0; c < k && !e.amap_host.empty(); ++c)
+        for (int32_t q = 0; q < e.Ws; ++q) qof[static_cast<size_t>(c) * e.Ws + e.amap_host[static_cast<size_t>(c) * e.Ws + q]] = q;
       for (int64_t v = 0; v < n; ++v) {
         const int c = last_colors_[v];
         for (int64_t S = 0; S < C; ++S) {
           const int64_t j = rel[static_cast<size_t>(S) * k + c];
           double x = 0.0;
-          if (j >= 0)
+          if (j >= 0 && e.pstream && e.omap.empty())  // packed: q with amap[c][q] == j
+            x = t[dev::panel_offset(e.Cout, n, v, qof[static_cast<size_t>(c) * e.Ws + j])];
+          else if (j >= 0)
             x = e.omap.empty() ? t[dev::panel_offset(e.Cout, n, v, j)]
                                : t[dev::panel_offset(e.Cout, n, v, e.omap[static_cast<size_t>(c) * e.Ws + j])];
           out[v * C + S] = x;

@@ -83,7 +83,16 @@ struct NodeExec {
   size_t rt_smem = 0;
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
-  void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)  // vertices per pass, their smem row strides
+  void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)
+  // active-leaf node with an unshared rooted SpMM: P' is never materialized --
+  // each group's columns go to an n x Ct scratch table and are scattered into
+  // the output (RR or RS) right after the group's last part (pstream_copy)
+  bool pstream = false;
+  int32_t Ct = 0;
+  int32_t* d_emap = nullptr;      // [k][Cps] P' storage column -> output column (RS slot / packed q), or -1
+  int32_t* d_amap = nullptr;      // packed RR output: [k][Ws] q -> RR column (for its consumer's staging)
+  std::vector<int32_t> amap_host;
+  const int32_t* d_amap_in = nullptr;  // this node's ACTIVE input is packed: stage it through this map  // vertices per pass, their smem row strides
   int dup_of = -1;                // exec index of an identical earlier node (table aliased)
   int pp_dup_of = -1;             // exec index of an earlier node with the same P' (SpMM skipped)
 };
@@ -143,6 +152,7 @@ class Engine {
   void release_graph();
   void release_template();
   void plan_arena();
+  void plan_arena_once(bool allow_stream);
   void ensure_arena();
   void ensure_colors(int64_t bytes);
   void gen_colors(const uint64_t* seeds, int count, uint8_t* d_out);
@@ -230,7 +240,8 @@ class Engine {
   int rooted_parts_ = 1;             // part count of every rooted SpMM (and of the row bucketing)
   int64_t rcol_off_ = -1;            // per-coloring color-sorted packed CSR
   int64_t rcut_off_ = -1;            // per-coloring part (color class) cuts, n * (parts + 1)
-  void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors);
+  // Pp: full P' (group-major), or the n x Ct scratch of a streamed node (out = its output table)
+  void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out = nullptr);
   bool rooted_ema_ = false;          // every table rooted; eMA on same-color vertex tiles
   int max_tiles_ = 0;                // ceil(n / 32) + k
   const uint8_t* d_colors_rt_ = nullptr;  // this context's row colors during run_dp

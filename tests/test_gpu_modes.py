@@ -7,7 +7,10 @@ child process):
   nodes take;
 * TCG_ROOTED_EMA=0 -- full-table eMA (ema_node / ema_blocked / ema_vtx_*)
   behind the rooted SpMM;
-* TCG_ROOTED=0 -- full-table panel SpMM and full-table eMA.
+* TCG_ROOTED=0 -- full-table panel SpMM and full-table eMA;
+* TCG_PSTREAM=2 -- streamed active-leaf SpMM epilogues (P' never
+  materialized) also in contexts that keep their tables, so every node table
+  of a streamed node is checked; TCG_PSTREAM=0 -- always a full P'.
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -67,8 +70,9 @@ print("OK")
 """
 
 
-@pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"}],
-                         ids=["rt_vtx_all", "full_table_ema", "full_table_spmm"])
+@pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"},
+                                 {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}],
+                         ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
