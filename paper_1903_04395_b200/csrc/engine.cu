@@ -207,6 +207,13 @@ Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
     throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor));
   if (const char* e = std::getenv("TCG_PART_MB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 20;
+  if (const char* e = std::getenv("TCG_PART_KB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 10;  // tests
+  // rooted SpMM: ONE part (whole rows, one launch per group) unless
+  // TCG_ROOTED_PARTS=1 splits it into colour classes of ~TCG_PART_MB.  Every
+  // extra part re-reads and re-writes the group's P' columns; measured on
+  // B200 that costs more than the L2 misses of the unsplit gather source
+  // (cfg3 49.9 -> 47.9 ms, cfg4 1666 -> 1049 ms).
+  if (const char* e = std::getenv("TCG_ROOTED_PARTS")) rooted_part_mb_ = std::atoi(e);
   if (const char* e = std::getenv("TCG_L2_PERSIST"); e && std::atoi(e) > 0) {
     int win = 0;
     TCG_CUDA(cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, cfg.device));
@@ -376,7 +383,7 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
   // sparse skewed graphs (cfg2, avg ~30) the hub rows stay L2-resident anyway
   // and extra parts only add output passes (measured: profiles/ DESIGN.md 3).
-  if (!std::getenv("TCG_PART_MB"))
+  if (!std::getenv("TCG_PART_MB") && !std::getenv("TCG_PART_KB"))
     part_bytes_ = (n_ > 0 && nnz_ / std::max(n_, 1) >= 64) ? (64ll << 20) : (128ll << 20);
   max_slots_ = 0;
   {  // whole-row schedule: the rooted SpMM, the histogram, P = 1 panels
@@ -927,7 +934,7 @@ void Engine::plan_arena_once(bool allow_stream) {
   for (auto& e : exec_)
     if (e.rooted) {
       need_rooted_ = true;
-      rooted_parts_ = std::max(rooted_parts_, std::min(plan_.k, parts_for_width(e.rl_zw)));
+      rooted_parts_ = std::max(rooted_parts_, std::min(plan_.k, rooted_part_mb_ > 0 ? parts_for_width(e.rl_zw) : 1));
     }
   rcol_off_ = rcut_off_ = -1;
   int64_t rooted_partial = 0;

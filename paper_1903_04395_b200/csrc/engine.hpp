@@ -178,7 +178,8 @@ class Engine {
   cudaStream_t stream_ = nullptr;
   int64_t launches_ = 0;
   uint64_t limit_override_ = 0;
-  int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per SpMM part (measured best on cfg3)
+  int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per full-table SpMM part
+  int rooted_part_mb_ = 0;           // > 0: split the rooted SpMM into colour-class parts of part_bytes_
   int64_t persist_max_ = 0;          // > 0: pin each part's gather window in L2 (TCG_L2_PERSIST=MB)
 
   // sharding: this rank owns global rows [rows_[rank], rows_[rank+1]); tables

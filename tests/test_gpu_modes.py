@@ -10,7 +10,9 @@ child process):
 * TCG_ROOTED=0 -- full-table panel SpMM and full-table eMA;
 * TCG_PSTREAM=2 -- streamed active-leaf SpMM epilogues (P' never
   materialized) also in contexts that keep their tables, so every node table
-  of a streamed node is checked; TCG_PSTREAM=0 -- always a full P'.
+  of a streamed node is checked; TCG_PSTREAM=0 -- always a full P';
+* TCG_ROOTED_PARTS=1 with TCG_PART_KB=16 -- the rooted SpMM split into
+  colour-class parts (P' accumulated across parts).
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -71,8 +73,9 @@ print("OK")
 
 
 @pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"},
-                                 {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}],
-                         ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off"])
+                                 {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"}],
+                         ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
+                              "rooted_parts"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
