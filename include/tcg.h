@@ -169,7 +169,9 @@ int tcg_estimate(tcg_ctx* ctx, uint64_t seed, int iterations, double* rooted_tot
 
 /* Inspection (TCG_KEEP_TABLES): node table of the last coloring as
  * vertex-major fp64 n x C(k,|T_s|); which = 0 node table, 1 the SpMM output
- * P' computed from it (passive children only).  Root: C = 1. */
+ * P' computed from it (passive children only).  Root: C = 1.  P'[v, T] is
+ * only computed where T misses c(v) -- the only columns any eMA reads, since
+ * M_a[v, Sa] = 0 unless c(v) is in Sa -- and exported as 0 elsewhere. */
 int tcg_node_table(tcg_ctx* ctx, int node_id, int which, double* out);
 /* Kernel-level hook: Y = A X for a vertex-major fp32 n x C host matrix,
  * through the production SpMM kernel (la_kernels.hpp:83-102 semantics). */

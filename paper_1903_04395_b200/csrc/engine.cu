@@ -10,6 +10,7 @@
 #include <cstring>
 #include <map>
 #include <thread>
+#include <type_traits>
 
 namespace tcg {
 
@@ -272,6 +273,7 @@ void Engine::release_template() {
     dfree(e.d_slot_acc);
     dfree(e.d_slot_col);
     dfree(e.d_pinv);
+    dfree(e.d_xmap);
     dfree(e.d_pmap);
     dfree(e.d_cmap);
     dfree(e.d_imap);
@@ -537,6 +539,31 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
         e.d_slot_col = dupload(rl.slot_col, stream_);
         e.d_pinv = dupload(rl.inv, stream_);
         for (auto& q : pr) q.y = rl.perm[q.y];
+        // pair layout candidate: the row's color never occurs in a consumed
+        // P' column, so per (neighbour color, row color) only C(k-2, sp-1)
+        // sets are gathered -- worth it when the copies' lines are >= 20%
+        // fewer and one vertex's copies stay small (k x groups x zw floats)
+        static const int pair_mode = [] {
+          const char* s = std::getenv("TCG_PAIR");
+          return s ? std::atoi(s) : 1;
+        }();
+        if (pair_mode && k >= 3) {
+          RootedLayout r1 = build_rooted_layout(k - 1, e.sp);
+          int fpad1 = 0;
+          for (int g = 0; g < r1.groups; ++g)
+            fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
+          const size_t smem1 = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * fpad1 * 4;
+          const int64_t wx = B(k - 1, e.sp - 1);
+          const int64_t lines_old = static_cast<int64_t>(rl.groups) * rl.zw, lines_new = static_cast<int64_t>(r1.groups) * r1.zw;
+          const int64_t copy_bytes = 4ll * k * lines_new;
+          if (pair_mode == 2 || (5 * lines_new <= 4 * lines_old && copy_bytes <= 8192)) {
+            if (smem1 <= static_cast<size_t>(max_smem) - 4096 && 4 * 32 * (wx + 1) <= max_smem - 4096 && wx < 32768) {
+              e.pair_cand = true;
+              e.pr = std::move(r1);
+              e.Wx = static_cast<int32_t>(wx);
+            }
+          }
+        }
       }
     }
     e.d_split = dupload(pr, stream_);
@@ -659,9 +686,9 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   if (std::getenv("TCG_VERBOSE")) {
     std::fprintf(stderr, "[tcg] k=%d nodes=%d rooted_ema=%d\n", k, plan_.num_nodes, rooted_ema_ ? 1 : 0);
     for (const auto& e : exec_)
-      std::fprintf(stderr, "[tcg] node %2d (%2d,%2d,%2d) Cp=%d rooted=%d groups=%d zw=%d Cps=%d | Ws=%d Wa=%d Wp=%d Cout=%d "
+      std::fprintf(stderr, "[tcg] node %2d (%2d,%2d,%2d) Cp=%d rooted=%d pair=%d groups=%d zw=%d Cps=%d | Ws=%d Wa=%d Wp=%d Cout=%d "
                            "%s pairs=%d blocked=%d/%d vtx=%d/%d staged=%d dup_of=%d\n",
-                   e.id, e.size, e.sa, e.sp, e.Cp, e.rooted ? 1 : 0, e.rl_groups, e.rl_zw, e.Cps, e.Ws, e.Wa, e.Wp,
+                   e.id, e.size, e.sa, e.sp, e.Cp, e.rooted ? 1 : 0, e.pair ? 1 : 0, e.rl_groups, e.rl_zw, e.Cps, e.Ws, e.Wa, e.Wp,
                    e.Cout, e.omap.empty() ? "RR" : "RS", e.rt_pairs, e.rt_blocked ? 1 : 0, e.blocked ? 1 : 0,
                    e.vtx ? 1 : 0, e.rt_vtx ? 1 : 0, e.ema_staged ? 1 : 0, e.dup_of >= 0 ? exec_[e.dup_of].id : -1);
     for (const auto& e : exec_)
@@ -719,12 +746,48 @@ void Engine::setup_rooted_ema(int max_smem) {
     if (4 * (row_floats(Wa) + Wp + 4) > max_smem - 4096) return;
     e.rt_vtx = true;
   }
+  // pair layout for the candidates (needs the rooted eMA; unsharded): the
+  // SpMM layout fields now describe the (k-1)-color layout
+  int cs[kMaxK];
+  for (auto& e : exec_) {
+    e.pair = e.pair_cand && !sharded();
+    if (!e.pair) continue;
+    const RootedLayout& r1 = e.pr;
+    e.Cps = r1.store_cols;
+    e.rl_zw = r1.zw;
+    e.rl_groups = r1.groups;
+    e.rl_fbase = r1.fbase;
+    e.rl_fsize = r1.fsize;
+    e.rl_perm = r1.perm;  // (k-1)-color combinadic column -> storage column
+    int fpad1 = 0;
+    for (int g = 0; g < r1.groups; ++g)
+      fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
+    e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * fpad1 * 4;
+    dfree(e.d_slot_acc);
+    e.d_slot_acc = dupload(r1.slot_acc, stream_);
+    // copy (cu, cv) slot -> RR column of the set relative to cu
+    const int slots = r1.groups * r1.zw;
+    std::vector<int16_t> xm(static_cast<size_t>(k) * k * slots, -1);
+    for (int cu = 0; cu < k; ++cu)
+      for (int cv = 0; cv < k; ++cv) {
+        if (cu == cv) continue;
+        const int cr = cu - (cu > cv ? 1 : 0);
+        for (int i = 0; i < slots; ++i) {
+          const int32_t col1 = r1.slot_col[static_cast<size_t>(cr) * slots + i];
+          if (col1 < 0) continue;
+          set_of(k - 1, col1, e.sp, cs);
+          for (int q = 0; q < e.sp; ++q) cs[q] = cs[q] >= cv ? cs[q] + 1 : cs[q];  // actual colors
+          xm[(static_cast<size_t>(cu) * k + cv) * slots + i] = static_cast<int16_t>(relabeled_index(cs, e.sp, cu));
+        }
+      }
+    dfree(e.d_xmap);
+    e.d_xmap = dupload(xm, stream_);
+  }
   std::vector<int> parent(plan_.num_nodes, -1);
   for (size_t i = 0; i < exec_.size(); ++i) {
     parent[exec_[i].a] = static_cast<int>(i);
     parent[exec_[i].p] = static_cast<int>(i);
   }
-  int cs[kMaxK];
   for (auto& e : exec_) {
     e.Wa = e.a_leaf ? 0 : static_cast<int32_t>(B(k - 1, e.sa - 1));
     e.Wp = static_cast<int32_t>(B(k - 1, e.sp));
@@ -737,9 +800,13 @@ void Engine::setup_rooted_ema(int max_smem) {
     } else {
       e.Cpt = e.Cps;
       full_of.assign(static_cast<size_t>(e.Cps), -1);
-      for (int32_t x = 0; x < e.Cp; ++x) full_of[e.rl_perm[x]] = x;
+      if (!e.pair)
+        for (int32_t x = 0; x < e.Cp; ++x) full_of[e.rl_perm[x]] = x;
     }
     std::vector<int32_t> pm(static_cast<size_t>(k) * e.Cpt, -1);
+    if (e.pair)  // storage column -> its relabeled (k-1)-color index, for every row color
+      for (int c = 0; c < k; ++c)
+        for (int32_t col = 0; col < e.Cpt; ++col) pm[static_cast<size_t>(c) * e.Cpt + col] = e.pr.inv[col];
     for (int32_t col = 0; col < e.Cpt; ++col) {
       if (full_of[col] < 0) continue;
       set_of(k, full_of[col], e.sp, cs);
@@ -752,7 +819,7 @@ void Engine::setup_rooted_ema(int max_smem) {
     e.omap.clear();
     if (!e.root) {
       const NodeExec& par = exec_[parent[e.id]];
-      if (par.p == e.id && par.rooted) {  // feeds the rooted SpMM: its slot layout
+      if (par.p == e.id && par.rooted && !par.pair) {  // feeds the rooted SpMM: its slot layout
         const RootedLayout rl = build_rooted_layout(k, e.size);
         e.Cout = rl.groups * rl.zw;
         e.omap.assign(static_cast<size_t>(k) * e.Ws, -1);
@@ -780,18 +847,19 @@ void Engine::setup_rooted_ema(int max_smem) {
       // active leaf: output column -> P' storage column of (S minus c), per color
       std::vector<int32_t> cm(static_cast<size_t>(k) * e.Cout, -1);
       std::vector<int32_t> storage_of(e.Cp);
-      for (int32_t x = 0; x < e.Cp; ++x) storage_of[x] = e.p_leaf ? x : e.rl_perm[x];
+      for (int32_t x = 0; x < e.Cp; ++x) storage_of[x] = e.p_leaf ? x : (e.pair ? 0 : e.rl_perm[x]);
       int t[kMaxK];
       for (int c = 0; c < k; ++c)
         for (int32_t j = 0; j < e.Ws; ++j) {
           set_of(k - 1, j, e.size - 1, t);
           for (int q = 0; q < e.size - 1; ++q) t[q] = t[q] >= c ? t[q] + 1 : t[q];
-          const int32_t src = storage_of[index_of(t, e.size - 1)];
+          // (pair layout: P' is stored by the relabeled index of S minus c: j)
+          const int32_t src = e.pair ? e.rl_perm[j] : storage_of[index_of(t, e.size - 1)];
           const int32_t i = e.omap.empty() ? j : e.omap[static_cast<size_t>(c) * e.Ws + j];
           if (i >= 0) cm[static_cast<size_t>(c) * e.Cout + i] = src;
         }
       e.d_cmap = dupload(cm, stream_);
-      if (!e.p_leaf) {
+      if (!e.p_leaf && !e.pair) {
         // streamed SpMM epilogue (pstream_copy): P' storage column -> output
         // column.  RS outputs: the slot.  RR outputs are stored PACKED in P'
         // storage order instead (column q = rank of the storage column among
@@ -929,11 +997,12 @@ void Engine::plan_arena_once(bool allow_stream) {
   const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
   // rooted SpMMs: parts are contiguous COLOR classes (one count for all
   // rooted nodes: the widest compressed panel's), over whole-row schedules
-  need_rooted_ = false;
+  need_rooted_ = need_pair_ = false;
   rooted_parts_ = 1;
   for (auto& e : exec_)
     if (e.rooted) {
       need_rooted_ = true;
+      need_pair_ |= e.pair;
       rooted_parts_ = std::max(rooted_parts_, std::min(plan_.k, rooted_part_mb_ > 0 ? parts_for_width(e.rl_zw) : 1));
     }
   rcol_off_ = rcut_off_ = -1;
@@ -944,6 +1013,14 @@ void Engine::plan_arena_once(bool allow_stream) {
     rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
     rcut_off_ = ap.alloc(8 * static_cast<int64_t>(n_) * (rooted_parts_ + 1));
     lcnt_off_ = ap.alloc(4 * 32 * static_cast<int64_t>(std::max(nlchunks_, 1)));
+  }
+  pseg_off_ = pkey_off_ = pperm_off_ = pcnt_off_ = -1;
+  if (need_pair_) {  // per-coloring color-ordered whole-row segments
+    const int64_t nseg = sched_.at(1)[0].nseg_padded;
+    pseg_off_ = ap.alloc(static_cast<int64_t>(sizeof(dev::Seg)) * nseg);
+    pkey_off_ = ap.alloc(nseg);
+    pperm_off_ = ap.alloc(4 * nseg);
+    pcnt_off_ = ap.alloc(4 * ((nseg + dev::kVsChunk - 1) / dev::kVsChunk + 1) * (plan_.k + 1));
   }
   vs_off_ = tiles_off_ = vcnt_off_ = -1;
   max_tiles_ = static_cast<int>((n_ + dev::kTileV - 1) / dev::kTileV) + plan_.k;
@@ -959,6 +1036,12 @@ void Engine::plan_arena_once(bool allow_stream) {
     for (auto& e : exec_)
       if (e.rooted) rooted_partial = std::max<int64_t>(rooted_partial, static_cast<int64_t>(slots) * static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / e.rl_zw))));
   }
+  // tables read by a pair expansion must be plain RR (not streamed-packed)
+  std::vector<char> feeds_pair(plan_.num_nodes, 0);
+  for (const auto& y : exec_)
+    if (y.pair) feeds_pair[y.p] = 1;
+  for (const auto& x : exec_)
+    if (x.dup_of >= 0 && feeds_pair[x.id]) feeds_pair[exec_[x.dup_of].id] = 1;
   for (auto& e : exec_) {
     if (e.dup_of >= 0) {  // alias the first occurrence; release this node's own children
       const NodeExec& x = exec_[e.dup_of];
@@ -975,7 +1058,8 @@ void Engine::plan_arena_once(bool allow_stream) {
       continue;
     }
     e.pstream = false;
-    if (allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.d_emap && e.pp_dup_of < 0) {
+    if (allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.d_emap && e.pp_dup_of < 0 &&
+        !feeds_pair[e.id]) {
       bool shared = false;
       for (const auto& y : exec_) shared |= y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id;
       e.pstream = !shared;
@@ -998,6 +1082,14 @@ void Engine::plan_arena_once(bool allow_stream) {
       e.pp_off = exec_[e.pp_dup_of].pp_off;
       pprime_off_[e.p] = e.pp_off;
       if (!keep) ap.free(table_off_[e.p]);
+    } else if (!e.p_leaf && e.rooted && rooted_ema_ && e.pair) {
+      // RR M_p expanded into its per-row-color copies, then dropped; P'
+      // while the copies live
+      e.ct_off = ap.alloc(4ll * plan_.k * e.rl_groups * e.rl_zw * n_);
+      if (!keep) ap.free(table_off_[e.p]);
+      e.pp_off = ap.alloc(table_bytes(e.Cps));
+      pprime_off_[e.p] = e.pp_off;
+      if (!keep) ap.free(e.ct_off);
     } else if (!e.p_leaf && e.rooted && rooted_ema_) {
       // M_p is already in the SpMM's compressed slot layout
       e.pp_off = ap.alloc(table_bytes(e.Cps));
@@ -1311,6 +1403,18 @@ void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
 void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out) {
   const int zw = e.rl_zw, G = e.rl_groups;
   const float* X = rooted_ema_ ? M : table_ptr(e.ct_off);
+  int64_t xstride = 0;  // pair layout: floats between the copies of two row colors
+  if (e.pair) {
+    if (sharded()) throw logic_error("pair-layout SpMM on a sharded context");
+    float* cp = table_ptr(e.ct_off);
+    const size_t smem = static_cast<size_t>(4) * 32 * (e.Wx + 1);
+    TCG_CUDA(cudaFuncSetAttribute(dev::pair_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    dev::pair_expand<<<static_cast<unsigned>((n_ + 31) / 32), 256, smem, stream_>>>(M, e.Wx, d_colors, e.d_xmap, plan_.k, G, zw,
+                                                                                      n_, cp);
+    ++launches_;
+    X = cp;
+    xstride = static_cast<int64_t>(G) * n_ * zw;
+  }
   if (!rooted_ema_) {
     const int rf = static_cast<int>(dev::table_floats(e.Cp, 1));
     const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (96 << 10) / (4 * rf))));
@@ -1327,16 +1431,23 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const char* s = std::getenv("TCG_ROOTED_MINB");
     return s ? std::atoi(s) : 4;
   }();
-  const void* kern = minb == 4 ? (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 4>)
-                                  : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 4>)
-                                             : reinterpret_cast<const void*>(dev::spmm_rooted<8, 4>))
-                               : (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 1>)
-                                  : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 1>)
-                                             : reinterpret_cast<const void*>(dev::spmm_rooted<8, 1>));
+  auto pick = [&](auto pair_tag) -> const void* {
+    constexpr bool P = decltype(pair_tag)::value;
+    return minb == 4 ? (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 4, P>)
+                        : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 4, P>)
+                                   : reinterpret_cast<const void*>(dev::spmm_rooted<8, 4, P>))
+                     : (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 1, P>)
+                        : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 1, P>)
+                                   : reinterpret_cast<const void*>(dev::spmm_rooted<8, 1, P>));
+  };
+  const void* kern = e.pair ? pick(std::true_type{}) : pick(std::false_type{});
+  // pair: the rows in color order (this coloring's re-ordered schedule)
+  const dev::Seg* segs = e.pair ? reinterpret_cast<const dev::Seg*>(arena_ + pseg_off_) : ps.d_segs;
+  const uint8_t* rowc = e.pair ? d_colors : nullptr;
   TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rooted_smem)));
   const int spw = 128 / zw;
   for (int g = 0; g < G; ++g) {
-    const float* Xg = X + static_cast<int64_t>(g) * n_ * dev::kZ;
+    const float* Xg = X + static_cast<int64_t>(g) * n_ * (e.pair ? zw : dev::kZ);
     if (sharded()) {
       tr_->allgather(Xg, sizeof(float) * static_cast<size_t>(n_) * zw, d_xfull_, stream_);
       Xg = d_xfull_;
@@ -1353,11 +1464,11 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
       const unsigned blocks = static_cast<unsigned>((ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps);
       const int first = q == 0 ? 1 : 0;
       int part = q;
-      void* args[] = {const_cast<dev::Seg**>(&ps.d_segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
+      void* args[] = {const_cast<dev::Seg**>(&segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
                       const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
                       const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
                       const_cast<int*>(&fpad), const_cast<int32_t*>(&Cst), &n_, &Pp, &d_partial_,
-                      const_cast<int*>(&first)};
+                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride};
       TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {
@@ -1535,20 +1646,36 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     if (nlong_ > 0) {  // hub rows: chunked over many CTAs
       int* ccnt = reinterpret_cast<int*>(arena_ + lcnt_off_);
       dev::bucket_long_count<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
-                                                                                     plan_.k, ccnt);
+                                                                                     d_colors, plan_.k, ccnt);
       dev::bucket_long_scan<<<static_cast<unsigned>((nlong_ + 7) / 8), 256, 0, stream_>>>(
-          d_lchunks_, d_lfirst_, d_row_ptr_, nlong_, plan_.k, rooted_parts_, ccnt, cuts, hf, hzw);
+          d_lchunks_, d_lfirst_, d_row_ptr_, d_colors, nlong_, plan_.k, rooted_parts_, ccnt, cuts, hf, hzw);
       dev::bucket_long_scatter<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
-                                                                                       plan_.k, ccnt, rc);
+                                                                                       d_colors, plan_.k, ccnt, rc);
       launches_ += 3;
     }
-    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_row_order_, nlong_, nsmall_,
+    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nlong_, nsmall_,
                                                      plan_.k, rooted_parts_, rc, cuts, hf, hzw);
     ++launches_;
     if (nsmall_ < n_) {
       dev::bucket_small<<<static_cast<unsigned>((n_ - nsmall_ + 255) / 256), 256, 0, stream_>>>(
-          d_row_ptr_, d_col_, d_gcolors, d_row_order_, nsmall_, n_, plan_.k, rooted_parts_, rc, cuts, hf, hzw);
+          d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nsmall_, n_, plan_.k, rooted_parts_, rc, cuts, hf, hzw);
       ++launches_;
+    }
+    if (need_pair_) {  // whole-row segments re-ordered by row color (stable)
+      const PartSchedule& ps = sched_.at(1)[0];
+      const int64_t nseg = ps.nseg_padded;
+      const int nchunks = static_cast<int>((nseg + dev::kVsChunk - 1) / dev::kVsChunk);
+      uint8_t* keys = reinterpret_cast<uint8_t*>(arena_ + pkey_off_);
+      int* pcnt = reinterpret_cast<int*>(arena_ + pcnt_off_);
+      int32_t* perm = reinterpret_cast<int32_t*>(arena_ + pperm_off_);
+      dev::seg_keys<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(ps.d_segs, nseg, ps.d_slot_row, d_colors,
+                                                                                   plan_.k, keys);
+      dev::vsort_count<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), plan_.k + 1, pcnt);
+      dev::vsort_scan<<<1, 1024, 0, stream_>>>(pcnt, nchunks, plan_.k + 1, nullptr, 0);
+      dev::vsort_scatter<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), plan_.k + 1, pcnt, perm);
+      dev::seg_gather<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(
+          ps.d_segs, perm, nseg, reinterpret_cast<dev::Seg*>(arena_ + pseg_off_));
+      launches_ += 5;
     }
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
@@ -1977,8 +2104,37 @@ void Engine::node_table(int id, int which, double* out) {
       if (e.p == id && e.rooted) {  // group-major P': storage column perm[S]
         std::vector<float> t(dev::table_floats(e.Cps, n));
         copy_sync(t.data(), arena_ + off, t.size() * 4, cudaMemcpyDeviceToHost);
+        // columns containing c(v) are not computed by the rooted SpMM (never
+        // consumed): exported as 0
+        const int sp = plan_.size[id];
+        std::vector<uint32_t> mask(static_cast<size_t>(C));
+        int cs[kMaxK];
+        for (int64_t c = 0; c < C; ++c) {
+          set_of(plan_.k, c, sp, cs);
+          uint32_t m = 0;
+          for (int j = 0; j < sp; ++j) m |= 1u << cs[j];
+          mask[static_cast<size_t>(c)] = m;
+        }
+        std::vector<int64_t> rel;  // pair layout: [S][c] relabeled index of S past c
+        if (e.pair) {
+          rel.assign(static_cast<size_t>(C) * k, -1);
+          for (int64_t c = 0; c < C; ++c) {
+            set_of(plan_.k, c, sp, cs);
+            for (int q = 0; q < k; ++q)
+              if (!(mask[static_cast<size_t>(c)] >> q & 1u)) {
+                int tt[kMaxK];
+                for (int j = 0; j < sp; ++j) tt[j] = cs[j] > q ? cs[j] - 1 : cs[j];
+                rel[static_cast<size_t>(c) * k + q] = index_of(tt, sp);
+              }
+          }
+        }
         for (int64_t v = 0; v < n; ++v)
-          for (int64_t c = 0; c < C; ++c) out[v * C + c] = t[dev::panel_offset(e.Cps, n, v, e.rl_perm[c])];
+          for (int64_t c = 0; c < C; ++c) {
+            const int cv = last_colors_[v];
+            if (mask[static_cast<size_t>(c)] >> cv & 1u) { out[v * C + c] = 0.0; continue; }
+            const int64_t col = e.pair ? e.rl_perm[rel[static_cast<size_t>(c) * k + cv]] : e.rl_perm[c];
+            out[v * C + c] = t[dev::panel_offset(e.Cps, n, v, col)];
+          }
         return;
       }
   }

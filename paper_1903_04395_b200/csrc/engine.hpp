@@ -60,8 +60,16 @@ struct NodeExec {
   int16_t* d_slot_acc = nullptr;  // [k][groups * zw]
   int32_t* d_slot_col = nullptr;  // [k][groups * zw]
   int32_t* d_pinv = nullptr;      // [Cps] storage column -> combinadic column (blocked eMA staging)
-  int64_t ct_off = -1;            // arena offset of the compressed passive table
+  int64_t ct_off = -1;            // arena offset of the compressed passive table (pair: its copies)
   size_t rooted_smem = 0;         // spmm_rooted dynamic smem
+  // pair layout (host.hpp build_pair_layout, rooted eMA only): the rl_*
+  // fields, Cps and d_slot_acc then describe the (k-1)-color layout of the
+  // sets that miss the ROW's color; the RR passive table is expanded into one
+  // copy per row color (pair_expand) and P' is stored relative to c(v)
+  bool pair_cand = false, pair = false;
+  RootedLayout pr;                // the (k-1)-color layout (candidates)
+  int32_t Wx = 0;                 // RR columns of the passive table, C(k-1, sp-1)
+  int16_t* d_xmap = nullptr;      // [k][k][groups * zw] copy slot -> RR column, or -1
   // rooted eMA (kernels_rt.cuh): same-color vertex tiles of the (k-1)-color
   // problem (s-1, a-1, p); tables stored rooted (RR) or in the parent SpMM's
   // slot layout (RS, passive children)
@@ -238,6 +246,8 @@ class Engine {
   bool need_bucket_ = false;         // some node uses the leaf-pushed SpMM
   int64_t colb_off_ = -1, boff_off_ = -1;
   bool need_rooted_ = false;         // some node uses the rooted-compressed SpMM
+  bool need_pair_ = false;           // some node uses the pair layout: per-coloring color-ordered segments
+  int64_t pseg_off_ = -1, pkey_off_ = -1, pperm_off_ = -1, pcnt_off_ = -1;
   int rooted_parts_ = 1;             // part count of every rooted SpMM (and of the row bucketing)
   int64_t rcol_off_ = -1;            // per-coloring color-sorted packed CSR
   int64_t rcut_off_ = -1;            // per-coloring part (color class) cuts, n * (parts + 1)

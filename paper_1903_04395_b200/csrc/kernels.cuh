@@ -426,6 +426,20 @@ constexpr uint32_t kPackSentinel = 0xFFFFFFFFu;  // color 31: never a real color
 constexpr int kPackShift = 27;
 constexpr uint32_t kPackMask = (1u << kPackShift) - 1u;
 
+// Neighbour colors are sorted in the row's ROTATED order: key(c) = (c - cv - 1)
+// mod k for a row of color cv, so the run of the row's own color comes last
+// and the part cuts stop before it.  Those neighbours only feed the P'
+// columns containing c(v), which no consumer reads (M_a[v, Sa] = 0 unless
+// c(v) is in Sa), so the rooted SpMM never walks them.
+__device__ __forceinline__ int rot_key(int c, int cv, int k) {
+  const int r = c - cv - 1;
+  return r < 0 ? r + k : r;
+}
+__device__ __forceinline__ int unrot_key(int r, int cv, int k) {
+  const int c = r + cv + 1;
+  return c >= k ? c - k : c;
+}
+
 // exclusive scan of cnt[0, nkeys) by one warp, in place
 __device__ __forceinline__ void warp_exclusive_scan(int* cnt, int nkeys, int lane) {
   int run = 0;
@@ -454,8 +468,8 @@ constexpr int kBucketCache = 16;
 constexpr int kBucketLong = 1024;  // rows above this go to bucket_long (CTA per row)
 __global__ void __launch_bounds__(256)
 bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-            const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t row0,
-            int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
+            const uint8_t* __restrict__ colors, const uint8_t* __restrict__ rowc, const int32_t* __restrict__ row_order,
+            int32_t row0, int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
             float* __restrict__ hist, int hzw) {
   extern __shared__ int bsm[];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -466,18 +480,20 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     const int32_t v = row_order[ri];
     const int64_t b = row_ptr[v], e = row_ptr[v + 1];
     const int d = static_cast<int>(e - b);
+    const int cv = rowc[v];
     for (int i = lane; i < k; i += 32) cnt[i] = 0;
     __syncwarp();
     auto write_cuts = [&]() {
       // the exact neighbour color histogram (the P' of a leaf passive child)
-      // is the per-color count: cnt[c+1] - cnt[c] after the scan
+      // is the per-key count: cnt[r+1] - cnt[r] after the scan
       if (hist && lane < hzw) {
-        const int hi = lane + 1 < k ? cnt[lane + 1] : d;
-        hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(hi - cnt[lane]) : 0.f;
+        const int r = lane < k ? rot_key(lane, cv, k) : 0;
+        const int hi = r + 1 < k ? cnt[r + 1] : d;
+        hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(hi - cnt[r]) : 0.f;
       }
-      if (lane <= nparts) {
+      if (lane <= nparts) {  // the last cut stops before the own-color run
         const int cb = lane * k / nparts;
-        cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + (cb < k ? cnt[cb] : d);
+        cuts[static_cast<int64_t>(v) * (nparts + 1) + lane] = b + cnt[cb < k ? cb : k - 1];
       }
       __syncwarp();
     };
@@ -486,7 +502,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
 #pragma unroll
       for (int q = 0; q < kBucketCache; ++q) u[q] = q * 32 + lane < d ? __ldg(col + b + q * 32 + lane) : -1;
 #pragma unroll
-      for (int q = 0; q < kBucketCache; ++q) key[q] = u[q] >= 0 ? colors[u[q]] : -1;
+      for (int q = 0; q < kBucketCache; ++q) key[q] = u[q] >= 0 ? rot_key(colors[u[q]], cv, k) : -1;
 #pragma unroll
       for (int q = 0; q < kBucketCache; ++q) {
         if (q * 32 >= d) break;
@@ -503,7 +519,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
         const int slot = key[q] >= 0 ? cnt[key[q]] + __popc(same & lt) : 0;
         __syncwarp();
         if (key[q] >= 0) {
-          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(key[q]) << kPackShift);
+          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(unrot_key(key[q], cv, k)) << kPackShift);
           if ((same & lt) == 0) cnt[key[q]] += __popc(same);
         }
         __syncwarp();
@@ -511,7 +527,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
     } else {
       for (int64_t j = b; j < e; j += 32) {
         const bool ok = j + lane < e;
-        const int key = ok ? colors[col[j + lane]] : -1;
+        const int key = ok ? rot_key(colors[col[j + lane]], cv, k) : -1;
         const unsigned same = __match_any_sync(0xffffffffu, key);
         if (ok && (same & lt) == 0) cnt[key] += __popc(same);
         __syncwarp();
@@ -521,12 +537,12 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
       for (int64_t j = b; j < e; j += 32) {
         const bool ok = j + lane < e;
         const int u = ok ? col[j + lane] : 0;
-        const int key = ok ? colors[u] : -1;
+        const int key = ok ? rot_key(colors[u], cv, k) : -1;
         const unsigned same = __match_any_sync(0xffffffffu, key);
         const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
         __syncwarp();
         if (ok) {
-          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
+          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(unrot_key(key, cv, k)) << kPackShift);
           if ((same & lt) == 0) cnt[key] += __popc(same);
         }
         __syncwarp();
@@ -544,12 +560,13 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
 constexpr int kBucketSmall = 8;
 __global__ void __launch_bounds__(256)
 bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-             const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t row0, int32_t n,
-             int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
+             const uint8_t* __restrict__ colors, const uint8_t* __restrict__ rowc, const int32_t* __restrict__ row_order,
+             int32_t row0, int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
              float* __restrict__ hist, int hzw) {
   const int64_t ri = row0 + static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (ri >= n) return;
   const int32_t v = row_order[ri];
+  const int cv = rowc[v];
   const int64_t b = row_ptr[v];
   const int d = static_cast<int>(row_ptr[v + 1] - b);
   uint32_t key[kBucketSmall];  // color << 28 | position << 24 ... packed with the id below
@@ -557,7 +574,7 @@ bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ co
 #pragma unroll
   for (int j = 0; j < kBucketSmall; ++j) u[j] = j < d ? __ldg(col + b + j) : 0;
 #pragma unroll
-  for (int j = 0; j < kBucketSmall; ++j) key[j] = j < d ? (static_cast<uint32_t>(colors[u[j]]) << 4 | j) : 0xFFFFu;
+  for (int j = 0; j < kBucketSmall; ++j) key[j] = j < d ? (static_cast<uint32_t>(rot_key(colors[u[j]], cv, k)) << 4 | j) : 0xFFFFu;
   // Batcher odd-even merge sort network for 8 keys
 #define TCG_CX(a, b) { const uint32_t x = min(key[a], key[b]), y = max(key[a], key[b]); key[a] = x; key[b] = y; }
   TCG_CX(0, 1) TCG_CX(2, 3) TCG_CX(4, 5) TCG_CX(6, 7)
@@ -574,7 +591,7 @@ bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ co
       int uu = u[0];  // u[pos] with static register indices
 #pragma unroll
       for (int q = 1; q < kBucketSmall; ++q) uu = pos == q ? u[q] : uu;
-      out[b + j] = static_cast<uint32_t>(uu) | ((key[j] >> 4) << kPackShift);
+      out[b + j] = static_cast<uint32_t>(uu) | (static_cast<uint32_t>(unrot_key(static_cast<int>(key[j] >> 4), cv, k)) << kPackShift);
     }
   }
   auto below = [&](int c) {  // entries of color < c
@@ -584,10 +601,12 @@ bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ co
     return x;
   };
   if (hist)
-    for (int c = 0; c < hzw; ++c)
-      hist[static_cast<int64_t>(v) * hzw + c] = c < k ? static_cast<float>(below(c + 1) - below(c)) : 0.f;
-  for (int part = 0; part <= nparts; ++part)
-    cuts[static_cast<int64_t>(v) * (nparts + 1) + part] = b + below(part * k / nparts);
+    for (int c = 0; c < hzw; ++c) {
+      const int r = c < k ? rot_key(c, cv, k) : 0;
+      hist[static_cast<int64_t>(v) * hzw + c] = c < k ? static_cast<float>(below(r + 1) - below(r)) : 0.f;
+    }
+  for (int part = 0; part <= nparts; ++part)  // the last cut stops before the own-color run
+    cuts[static_cast<int64_t>(v) * (nparts + 1) + part] = b + below(min(part * k / nparts, k - 1));
 }
 
 // Rows longer than kBucketLong are cut into chunks of <= kLongChunk entries,
@@ -600,12 +619,12 @@ constexpr int kLongChunk = 4096;
 
 // per-warp color counts of this CTA's chunk slice into cnt[8][k] (smem)
 __device__ __forceinline__ void long_chunk_counts(const int32_t* __restrict__ col, const uint8_t* __restrict__ colors,
-                                                  int64_t sb, int64_t se, int* cnt) {
+                                                  int64_t sb, int64_t se, int* cnt, int cv, int k) {
   const int lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
-    const int key = ok ? colors[col[j + lane]] : -1;
+    const int key = ok ? rot_key(colors[col[j + lane]], cv, k) : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     if (ok && (same & lt) == 0) cnt[key] += __popc(same);
     __syncwarp();
@@ -614,7 +633,7 @@ __device__ __forceinline__ void long_chunk_counts(const int32_t* __restrict__ co
 
 __global__ void __launch_bounds__(256)
 bucket_long_count(const int4* __restrict__ chunks, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                  const uint8_t* __restrict__ colors, int k, int* __restrict__ ccnt) {
+                  const uint8_t* __restrict__ colors, const uint8_t* __restrict__ rowc, int k, int* __restrict__ ccnt) {
   __shared__ int wc[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int4 ch = chunks[blockIdx.x];
@@ -624,7 +643,7 @@ bucket_long_count(const int4* __restrict__ chunks, const int64_t* __restrict__ r
   const int64_t slice = (kLongChunk / 8);
   const int64_t sb = min(rb + ch.z, rb + ch.y + warp * slice);
   const int64_t se = min(rb + ch.z, sb + slice);
-  long_chunk_counts(col, colors, sb, se, wc[warp]);
+  long_chunk_counts(col, colors, sb, se, wc[warp], rowc[ch.x], k);
   __syncthreads();
   if (threadIdx.x < k) {
     int t = 0;
@@ -636,7 +655,7 @@ bucket_long_count(const int4* __restrict__ chunks, const int64_t* __restrict__ r
 // warp per long row: lane c = color; per-chunk offsets (in place), histogram, cuts
 __global__ void __launch_bounds__(256)
 bucket_long_scan(const int4* __restrict__ chunks, const int32_t* __restrict__ row_first_chunk, const int64_t* __restrict__ row_ptr,
-                 int nlong, int k, int nparts, int* __restrict__ ccnt, int64_t* __restrict__ cuts,
+                 const uint8_t* __restrict__ rowc, int nlong, int k, int nparts, int* __restrict__ ccnt, int64_t* __restrict__ cuts,
                  float* __restrict__ hist, int hzw) {
   const int lane = threadIdx.x & 31;
   const int r = static_cast<int>((static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5);
@@ -647,17 +666,18 @@ bucket_long_scan(const int4* __restrict__ chunks, const int32_t* __restrict__ ro
   int tot = 0;
   if (lane < k)
     for (int c = c0; c < c1; ++c) tot += ccnt[static_cast<int64_t>(c) * 32 + lane];
-  if (hist && lane < hzw) hist[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(tot) : 0.f;
+  const int cv = rowc[v];  // lane = rotated key; its color's histogram entry
+  if (hist && lane < k) hist[static_cast<int64_t>(v) * hzw + unrot_key(lane, cv, k)] = static_cast<float>(tot);
+  if (hist && lane >= k && lane < hzw) hist[static_cast<int64_t>(v) * hzw + lane] = 0.f;
   int incl = tot;  // exclusive scan over colors
   for (int o = 1; o < 32; o <<= 1) {
     const int y = __shfl_up_sync(0xffffffffu, incl, o);
     if (lane >= o) incl += y;
   }
   const int base = incl - tot;
-  const int total = __shfl_sync(0xffffffffu, incl, 31);
   for (int part = 0; part <= nparts; ++part) {
     const int cb = part * k / nparts;
-    const int at = cb < k ? __shfl_sync(0xffffffffu, base, cb) : total;
+    const int at = __shfl_sync(0xffffffffu, base, cb < k ? cb : k - 1);  // (before the own-color run)
     if (lane == 0) cuts[static_cast<int64_t>(v) * (nparts + 1) + part] = b + at;
   }
   if (lane < k) {
@@ -672,7 +692,8 @@ bucket_long_scan(const int4* __restrict__ chunks, const int32_t* __restrict__ ro
 
 __global__ void __launch_bounds__(256)
 bucket_long_scatter(const int4* __restrict__ chunks, const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-                    const uint8_t* __restrict__ colors, int k, const int* __restrict__ ccnt, uint32_t* __restrict__ out) {
+                    const uint8_t* __restrict__ colors, const uint8_t* __restrict__ rowc, int k, const int* __restrict__ ccnt,
+                    uint32_t* __restrict__ out) {
   __shared__ int wc[8][32];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned lt = (1u << lane) - 1u;
@@ -683,7 +704,8 @@ bucket_long_scatter(const int4* __restrict__ chunks, const int64_t* __restrict__
   const int64_t slice = (kLongChunk / 8);
   const int64_t sb = min(rb + ch.z, rb + ch.y + warp * slice);
   const int64_t se = min(rb + ch.z, sb + slice);
-  long_chunk_counts(col, colors, sb, se, wc[warp]);
+  const int cv = rowc[ch.x];
+  long_chunk_counts(col, colors, sb, se, wc[warp], cv, k);
   __syncthreads();
   if (threadIdx.x < k) {  // warp-major prefix per color + the chunk's row offset
     int run = ccnt[static_cast<int64_t>(blockIdx.x) * 32 + threadIdx.x];
@@ -698,12 +720,12 @@ bucket_long_scatter(const int4* __restrict__ chunks, const int64_t* __restrict__
   for (int64_t j = sb; j < se; j += 32) {
     const bool ok = j + lane < se;
     const int u = ok ? col[j + lane] : 0;
-    const int key = ok ? colors[u] : -1;
+    const int key = ok ? rot_key(colors[u], cv, k) : -1;
     const unsigned same = __match_any_sync(0xffffffffu, key);
     const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
     __syncwarp();
     if (ok) {
-      out[rb + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(key) << kPackShift);
+      out[rb + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(unrot_key(key, cv, k)) << kPackShift);
       if ((same & lt) == 0) cnt[key] += __popc(same);
     }
     __syncwarp();
@@ -754,13 +776,16 @@ rooted_compress(const float* __restrict__ M, int C, const uint8_t* __restrict__ 
 // run per color of its set).  The next round's entries are fetched while the
 // current round's gathers are in flight (its start only depends on the
 // entries' colors).  slot_acc: [k][stride], this group's zw slots at offset 0.
-template <int ZW, int MINB>
+// PAIR (pair layout, host.hpp): the row's color cv picks the source copy
+// X + cv * xstride, whose slots are indexed by the neighbour color relabeled
+// past cv (slot_acc: [k-1][stride]); P' is stored relative to cv as well.
+template <int ZW, int MINB, bool PAIR>
 __global__ void __launch_bounds__(kSpmmWarps * 32, MINB)
 spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __restrict__ colb,
             const int64_t* __restrict__ cuts, int nparts, int part, const int32_t* __restrict__ slot_row,
             const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
             int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
-            double* __restrict__ partial, int first) {
+            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride) {
   constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
   extern __shared__ float racc_sm[];
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
@@ -772,8 +797,10 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
   // this part's color class of the segment's row: [cut_p, cut_p+1) ∩ segment
   int64_t lo = s.e_begin, hi = s.e_begin;
+  uint32_t cv = 0;
   if (s.dst != kSkip) {
     const int32_t row = s.dst >= 0 ? s.dst : slot_row[-1 - s.dst];
+    if (PAIR) cv = rowc[row];
     const int64_t* ct = cuts + static_cast<int64_t>(row) * (nparts + 1) + part;
     lo = max(s.e_begin, ct[0]);
     hi = min(s.e_begin + s.len, ct[1]);
@@ -795,12 +822,14 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   uint32_t w[NI];
   fetch(0, w);
   __syncwarp();
-  const float* Xl = X + l * 4;
+  const float* Xl = X + (PAIR ? static_cast<int64_t>(cv) * xstride : 0) + l * 4;
   const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (g * G);
   for (;;) {
     // the round = the prefix of the next R entries sharing entry 0's color
     // (entry j sits in lane j % G, word j / G of the group)
     const uint32_t c_round = __shfl_sync(0xffffffffu, w[0], g * G) >> kPackShift;
+    // the slot table's color index: relabeled past cv in the pair layout
+    const uint32_t c_slot = PAIR ? c_round - (c_round > cv ? 1u : 0u) : c_round;
     int count = 0;
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
@@ -819,7 +848,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
       v[j] = make_float4(0, 0, 0, 0);
       if (j < count) v[j] = ld_keep_f4(Xl + static_cast<int64_t>(pk[j] & kPackMask) * ZW, pkeep);
     }
-    if (count > 0 && static_cast<int>(c_round) != cur) {
+    if (count > 0 && static_cast<int>(c_slot) != cur) {
       if (cur >= 0) {
         const short4 sl = __ldg(reinterpret_cast<const short4*>(slot_acc + static_cast<int64_t>(cur) * slot_stride + l * 4));
         if (sl.x >= 0) acc[sl.x] += static_cast<float>(r0);
@@ -828,7 +857,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
         if (sl.w >= 0) acc[sl.w] += static_cast<float>(r3);
         r0 = r1 = r2 = r3 = 0;
       }
-      cur = static_cast<int>(c_round);
+      cur = static_cast<int>(c_slot);
     }
 #pragma unroll
     for (int wd = R / 2; wd; wd >>= 1)
@@ -878,6 +907,73 @@ __global__ void rooted_fixup(const int32_t* __restrict__ rows, const int32_t* __
   for (int s = slot_begin[r]; s < slot_begin[r + 1]; ++s) acc += partial[static_cast<int64_t>(s) * fpad + a];
   float* y = Y + panel_offset(Cstore, n, rows[r], fbase + a);
   *y = static_cast<float>(first ? acc : acc + static_cast<double>(*y));
+}
+
+// Pair layout (host.hpp PairLayout): the passive table M_p, stored RR (column
+// j = relabeled index of S minus c(u) over the other k-1 colors), is expanded
+// into one copy per row color cv != c(u): copy (cv, l) of vertex u holds, in
+// slot order, M_p[u, S] for the sets S of pair group l (sets over the k-1
+// colors other than cv) that contain c(u).  A CTA stages the RR rows of 32
+// consecutive vertices, then writes each copy's 32 rows (zw floats each) as
+// one contiguous block.  xmap: [c(u)][cv][L * zw] -> RR column, or -1.
+__global__ void __launch_bounds__(256)
+pair_expand(const float* __restrict__ M, int Wx, const uint8_t* __restrict__ colors, const int16_t* __restrict__ xmap,
+            int k, int L, int zw, int32_t n, float* __restrict__ out) {
+  extern __shared__ float xrow[];  // [32][Wx + 1]
+  __shared__ uint8_t cu_s[32];
+  const int64_t u0 = static_cast<int64_t>(blockIdx.x) * 32;
+  const int pitch = Wx + 1;
+  if (threadIdx.x < 32) cu_s[threadIdx.x] = u0 + threadIdx.x < n ? colors[u0 + threadIdx.x] : 0;
+  // stage: panel p of the RR table holds the tile's 32 rows contiguously
+  const int panels = num_panels(Wx);
+  for (int p = 0; p < panels; ++p) {
+    const int zp = panel_width(Wx, p);
+    const float* src = M + static_cast<int64_t>(p) * n * kZ + u0 * zp;
+    for (int f = threadIdx.x; f < 32 * zp / 4; f += blockDim.x) {
+      const int r = (f * 4) / zp, c4 = (f * 4) % zp;
+      if (u0 + r >= n) continue;
+      const float4 x = __ldg(reinterpret_cast<const float4*>(src + static_cast<int64_t>(r) * zp + c4));
+      const int c0 = p * kZ + c4;  // (the last panel may be wider than its columns)
+      float* d = xrow + r * pitch + c0;
+      if (c0 < Wx) d[0] = x.x;
+      if (c0 + 1 < Wx) d[1] = x.y;
+      if (c0 + 2 < Wx) d[2] = x.z;
+      if (c0 + 3 < Wx) d[3] = x.w;
+    }
+  }
+  __syncthreads();
+  const int per = 32 * zw / 4;  // float4s of one copy's tile block
+  const int total = k * L * per;
+  for (int i = threadIdx.x; i < total; i += blockDim.x) {
+    const int q = i / per, f = i % per;
+    const int cv = q / L, l = q % L;
+    const int r = (f * 4) / zw, j = (f * 4) % zw;
+    const int64_t u = u0 + r;
+    const int cu = cu_s[r];
+    if (u >= n || cu == cv) continue;
+    const short4 m = __ldg(reinterpret_cast<const short4*>(xmap + ((static_cast<int64_t>(cu) * k + cv) * L + l) * zw + j));
+    const float* xr = xrow + r * pitch;
+    const float4 val = make_float4(m.x >= 0 ? xr[m.x] : 0.f, m.y >= 0 ? xr[m.y] : 0.f, m.z >= 0 ? xr[m.z] : 0.f,
+                                   m.w >= 0 ? xr[m.w] : 0.f);
+    __stcs(reinterpret_cast<float4*>(out + (static_cast<int64_t>(q) * n + u) * zw + j), val);
+  }
+}
+
+// Per coloring, the whole-row segment schedule re-ordered by the row's color
+// (stable: length order within a color), so that the pair SpMM's rows of one
+// color -- which all gather from copy cv -- run together and the copy's
+// lines stay in L2.  Key k = padding.
+__global__ void seg_keys(const Seg* __restrict__ segs, int64_t nseg, const int32_t* __restrict__ slot_row,
+                         const uint8_t* __restrict__ rowc, int k, uint8_t* __restrict__ keys) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= nseg) return;
+  const Seg s = segs[i];
+  keys[i] = s.dst == kSkip ? static_cast<uint8_t>(k) : rowc[s.dst >= 0 ? s.dst : slot_row[-1 - s.dst]];
+}
+__global__ void seg_gather(const Seg* __restrict__ segs, const int32_t* __restrict__ perm, int64_t nseg,
+                           Seg* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < nseg) out[i] = segs[perm[i]];
 }
 
 // tcg_set_graph on the device: every id in range, no self-loop, rows strictly

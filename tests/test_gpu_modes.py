@@ -12,7 +12,9 @@ child process):
   materialized) also in contexts that keep their tables, so every node table
   of a streamed node is checked; TCG_PSTREAM=0 -- always a full P';
 * TCG_ROOTED_PARTS=1 with TCG_PART_KB=16 -- the rooted SpMM split into
-  colour-class parts (P' accumulated across parts).
+  colour-class parts (P' accumulated across parts);
+* TCG_PAIR=0 -- no pair layout (every rooted SpMM over the k-color slot
+  layout); TCG_PAIR=2 -- the pair layout for every node whose copies fit.
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -73,9 +75,10 @@ print("OK")
 
 
 @pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"},
-                                 {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"}],
+                                 {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"},
+                                 {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}],
                          ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
-                              "rooted_parts"])
+                              "rooted_parts", "pair_off", "pair_all"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,

@@ -231,6 +231,11 @@ def test_node_tables_match_oracle(seed):
         p = nd.passive_child
         if not T.partition(t).node(p).is_leaf():
             want = np.stack([tabs[p][g.neighbors(v)].sum(axis=0) for v in range(n)])
+            # P'[v, T] is computed where T misses c(v) (the consumed columns)
+            sp = T.partition(t).node(p).size
+            ix = T.ColorIndexer(k)
+            has = np.array([[c in ix.set_of(S, sp) for c in range(k)] for S in range(ix.num_sets(sp))])
+            want[has[:, colors].T] = 0.0
             assert_close(c.node_table(p, 1), want)
     assert_close(pv, opv)
     assert rel_err([total], [ototal]) <= 1e-12 or rel_err([total], [ototal]) <= REL
