@@ -152,7 +152,7 @@ void release_schedule(PartSchedule& s) {
 // length (descending), pad with no-op segments; rows longer than one segment
 // get fp64 partial slots (summed in order by spmm_fixup).
 PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
-                            bool keep_empty, cudaStream_t stream) {
+                            bool keep_empty, cudaStream_t stream, bool by_len = true) {
   const int32_t n = static_cast<int32_t>(lo.size());
   std::vector<dev::Seg> segs;
   segs.reserve(static_cast<size_t>(n) + 16);
@@ -176,7 +176,10 @@ PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<in
   const int64_t padded = std::max<int64_t>((static_cast<int64_t>(segs.size()) + dev::kSegPad - 1) /
                                                dev::kSegPad * dev::kSegPad, dev::kSegPad);
   std::vector<dev::Seg> sorted(static_cast<size_t>(padded), dev::Seg{0, 0, dev::kSkip});
-  for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
+  if (by_len)
+    for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
+  else
+    std::copy(segs.begin(), segs.end(), sorted.begin());
   PartSchedule ps;
   ps.nseg_padded = padded;
   ps.d_segs = dupload(sorted, stream);
@@ -390,7 +393,8 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   max_slots_ = 0;
   {  // whole-row schedule: the rooted SpMM, the histogram, P = 1 panels
     std::vector<int64_t> lo(row_ptr, row_ptr + n_), hi(row_ptr + 1, row_ptr + n_ + 1);
-    sched_[1].push_back(build_schedule(lo, hi, true, stream_));
+    static const bool by_id = std::getenv("TCG_SEG_ID") && std::atoi(std::getenv("TCG_SEG_ID")) > 0;
+    sched_[1].push_back(build_schedule(lo, hi, true, stream_, !by_id));
     max_slots_ = sched_[1][0].nslots;
   }
   {  // rows by degree, descending (stable counting sort), for the per-coloring bucketing
@@ -475,6 +479,8 @@ void Engine::ensure_schedules(int P) {
 }
 
 // --------------------------------------------------------------- template
+static std::vector<int16_t> dummy_slots(const RootedLayout& L, int K);
+
 void Engine::set_template(int k, const int32_t* edges, int root) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   Template t = make_template(k, edges, root);
@@ -524,7 +530,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
       int fpad_max = 0;
       for (int g = 0; g < rl.groups; ++g)
         fpad_max = std::max(fpad_max, (g + 1 < rl.groups ? rl.fbase[g + 1] : rl.store_cols) - rl.fbase[g]);
-      const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * fpad_max * 4;
+      const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * (fpad_max + 4) * 4;
       // (rooted_compress stages at least one full row of M_p in smem)
       if (smem <= static_cast<size_t>(max_smem) - 4096 && 4 * dev::table_floats(e.Cp, 1) <= max_smem - 4096) {
         e.rooted = true;
@@ -535,7 +541,8 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
         e.rl_fsize = rl.fsize;
         e.rl_perm = rl.perm;
         e.rooted_smem = smem;
-        e.d_slot_acc = dupload(rl.slot_acc, stream_);
+        e.slot_K = k;
+        e.d_slot_acc = dupload(dummy_slots(rl, k), stream_);
         e.d_slot_col = dupload(rl.slot_col, stream_);
         e.d_pinv = dupload(rl.inv, stream_);
         for (auto& q : pr) q.y = rl.perm[q.y];
@@ -552,7 +559,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
           int fpad1 = 0;
           for (int g = 0; g < r1.groups; ++g)
             fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
-          const size_t smem1 = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * fpad1 * 4;
+          const size_t smem1 = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4;
           const int64_t wx = B(k - 1, e.sp - 1);
           const int64_t lines_old = static_cast<int64_t>(rl.groups) * rl.zw, lines_new = static_cast<int64_t>(r1.groups) * r1.zw;
           const int64_t copy_bytes = 4ll * k * lines_new;
@@ -700,6 +707,25 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   tables_valid_ = false;
 }
 
+// spmm_rooted's slot table: -1 (unused slot) -> the group's dummy
+// accumulator fpad_g, plus an all-dummy row K (the state before a row's first run)
+static std::vector<int16_t> dummy_slots(const RootedLayout& L, int K) {
+  const int slots = L.groups * L.zw;
+  std::vector<int16_t> out(static_cast<size_t>(K + 1) * slots);
+  for (int g = 0; g < L.groups; ++g) {
+    const int fpad = (g + 1 < L.groups ? L.fbase[g + 1] : L.store_cols) - L.fbase[g];
+    for (int t = 0; t < L.zw; ++t) {
+      const int i = g * L.zw + t;
+      for (int c = 0; c < K; ++c) {
+        const int16_t x = L.slot_acc[static_cast<size_t>(c) * slots + i];
+        out[static_cast<size_t>(c) * slots + i] = x >= 0 ? x : static_cast<int16_t>(fpad);
+      }
+      out[static_cast<size_t>(K) * slots + i] = static_cast<int16_t>(fpad);
+    }
+  }
+  return out;
+}
+
 // relabeled combinadic index of the set cs[0..h) minus color c (colors above
 // c shift down by one), over k-1 colors
 static int64_t relabeled_index(const int* cs, int h, int c) {
@@ -762,9 +788,10 @@ void Engine::setup_rooted_ema(int max_smem) {
     int fpad1 = 0;
     for (int g = 0; g < r1.groups; ++g)
       fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
-    e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * fpad1 * 4;
+    e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4;
     dfree(e.d_slot_acc);
-    e.d_slot_acc = dupload(r1.slot_acc, stream_);
+    e.slot_K = k - 1;
+    e.d_slot_acc = dupload(dummy_slots(r1, k - 1), stream_);
     // copy (cu, cv) slot -> RR column of the set relative to cu
     const int slots = r1.groups * r1.zw;
     std::vector<int16_t> xm(static_cast<size_t>(k) * k * slots, -1);
@@ -1456,7 +1483,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - gbase;
     const int fbase = out ? 0 : gbase;       // streamed: the group's columns at 0 of the scratch
     const int32_t Cst = out ? e.Ct : e.Cps;
-    const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * fpad * 4;
+    const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * (fpad + 4) * 4;
     const int16_t* sl = e.d_slot_acc + static_cast<int64_t>(g) * zw;
     int slot_stride = G * zw;
     for (int q = 0; q < rooted_parts_; ++q) {
@@ -1468,7 +1495,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
                       const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
                       const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
                       const_cast<int*>(&fpad), const_cast<int32_t*>(&Cst), &n_, &Pp, &d_partial_,
-                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride};
+                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride, const_cast<int*>(&e.slot_K)};
       TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {

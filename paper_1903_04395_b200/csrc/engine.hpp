@@ -57,7 +57,8 @@ struct NodeExec {
   int32_t Cps = 0;
   int rl_zw = 0, rl_groups = 0;
   std::vector<int32_t> rl_fbase, rl_fsize, rl_perm;
-  int16_t* d_slot_acc = nullptr;  // [k][groups * zw]
+  int16_t* d_slot_acc = nullptr;  // [K + 1][groups * zw], unused slots -> the group's dummy (spmm_rooted)
+  int slot_K = 0;                 // colors of the slot table: k, or k - 1 (pair layout)
   int32_t* d_slot_col = nullptr;  // [k][groups * zw]
   int32_t* d_pinv = nullptr;      // [Cps] storage column -> combinadic column (blocked eMA staging)
   int64_t ct_off = -1;            // arena offset of the compressed passive table (pair: its copies)

@@ -46,6 +46,12 @@ __device__ __forceinline__ int ld_stream_i32(const int32_t* p, uint64_t pol) {
                : "=r"(v) : "l"(p), "l"(pol));
   return v;
 }
+// base + idx * bytes as one IMAD.WIDE.U32 (row gathers: idx < 2^27)
+__device__ __forceinline__ const float* row_addr(const char* base, uint32_t idx, uint32_t bytes) {
+  uint64_t r;
+  asm("mad.wide.u32 %0, %1, %2, %3;" : "=l"(r) : "r"(idx), "r"(bytes), "l"(base));
+  return reinterpret_cast<const float*>(r);
+}
 __device__ __forceinline__ float4 ld_keep_f4(const float* p, uint64_t pol) {
   float4 v;
   asm("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
@@ -775,7 +781,10 @@ rooted_compress(const float* __restrict__ M, int C, const uint8_t* __restrict__ 
 // task's F_g accumulators (smem, fp32: each F_g column receives at most one
 // run per color of its set).  The next round's entries are fetched while the
 // current round's gathers are in flight (its start only depends on the
-// entries' colors).  slot_acc: [k][stride], this group's zw slots at offset 0.
+// entries' colors).  slot_acc: [K + 1][stride], this group's zw slots at
+// offset 0, unused slots (and the whole extra row K, the state before the
+// first run) pointing at the dummy accumulator fpad, so the run scatter is
+// branch-free; a lane group's accumulators are fpad + 4 floats apart.
 // PAIR (pair layout, host.hpp): the row's color cv picks the source copy
 // X + cv * xstride, whose slots are indexed by the neighbour color relabeled
 // past cv (slot_acc: [k-1][stride]); P' is stored relative to cv as well.
@@ -785,14 +794,14 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
             const int64_t* __restrict__ cuts, int nparts, int part, const int32_t* __restrict__ slot_row,
             const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
             int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
-            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride) {
+            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride, int kdummy) {
   constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
   extern __shared__ float racc_sm[];
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
   const int64_t task = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp;
   if (task >= ntasks) return;
   const Seg s = segs[task * SPW + g];
-  float* acc = racc_sm + static_cast<int64_t>(warp * SPW + g) * fpad;
+  float* acc = racc_sm + (warp * SPW + g) * (fpad + 4);
   for (int i = l; i < fpad; i += G) acc[i] = 0.f;
   const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
   // this part's color class of the segment's row: [cut_p, cut_p+1) ∩ segment
@@ -809,7 +818,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   const uint32_t* cp = colb + lo;
   const int len = static_cast<int>(hi - lo);
   double r0 = 0, r1 = 0, r2 = 0, r3 = 0;
-  int cur = -1;
+  int cur = kdummy;
   int pos = 0;  // first unconsumed entry of the segment
   auto fetch = [&](int at, uint32_t (&w)[NI]) {
 #pragma unroll
@@ -822,7 +831,16 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   uint32_t w[NI];
   fetch(0, w);
   __syncwarp();
-  const float* Xl = X + (PAIR ? static_cast<int64_t>(cv) * xstride : 0) + l * 4;
+  const char* Xl = reinterpret_cast<const char*>(X + (PAIR ? static_cast<int64_t>(cv) * xstride : 0) + l * 4);
+  const int16_t* sla = slot_acc + l * 4;
+  auto scatter = [&]() {  // the finished run into its slots' accumulators (dummy for unused slots)
+    const short4 sl = __ldg(reinterpret_cast<const short4*>(sla + cur * slot_stride));
+    acc[sl.x] += static_cast<float>(r0);
+    acc[sl.y] += static_cast<float>(r1);
+    acc[sl.z] += static_cast<float>(r2);
+    acc[sl.w] += static_cast<float>(r3);
+    r0 = r1 = r2 = r3 = 0;
+  };
   const unsigned gmask = (G == 32 ? 0xffffffffu : ((1u << G) - 1u)) << (g * G);
   for (;;) {
     // the round = the prefix of the next R entries sharing entry 0's color
@@ -846,17 +864,11 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       v[j] = make_float4(0, 0, 0, 0);
-      if (j < count) v[j] = ld_keep_f4(Xl + static_cast<int64_t>(pk[j] & kPackMask) * ZW, pkeep);
+      if (j < count)
+        v[j] = ld_keep_f4(row_addr(Xl, pk[j] & kPackMask, ZW * 4), pkeep);
     }
     if (count > 0 && static_cast<int>(c_slot) != cur) {
-      if (cur >= 0) {
-        const short4 sl = __ldg(reinterpret_cast<const short4*>(slot_acc + static_cast<int64_t>(cur) * slot_stride + l * 4));
-        if (sl.x >= 0) acc[sl.x] += static_cast<float>(r0);
-        if (sl.y >= 0) acc[sl.y] += static_cast<float>(r1);
-        if (sl.z >= 0) acc[sl.z] += static_cast<float>(r2);
-        if (sl.w >= 0) acc[sl.w] += static_cast<float>(r3);
-        r0 = r1 = r2 = r3 = 0;
-      }
+      scatter();
       cur = static_cast<int>(c_slot);
     }
 #pragma unroll
@@ -867,13 +879,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
       }
     r0 += v[0].x; r1 += v[0].y; r2 += v[0].z; r3 += v[0].w;
   }
-  if (cur >= 0) {
-    const short4 sl = __ldg(reinterpret_cast<const short4*>(slot_acc + static_cast<int64_t>(cur) * slot_stride + l * 4));
-    if (sl.x >= 0) acc[sl.x] += static_cast<float>(r0);
-    if (sl.y >= 0) acc[sl.y] += static_cast<float>(r1);
-    if (sl.z >= 0) acc[sl.z] += static_cast<float>(r2);
-    if (sl.w >= 0) acc[sl.w] += static_cast<float>(r3);
-  }
+  scatter();
   __syncwarp();
   if (s.dst == kSkip) return;
   if (s.dst >= 0) {
@@ -942,20 +948,25 @@ pair_expand(const float* __restrict__ M, int Wx, const uint8_t* __restrict__ col
     }
   }
   __syncthreads();
-  const int per = 32 * zw / 4;  // float4s of one copy's tile block
-  const int total = k * L * per;
-  for (int i = threadIdx.x; i < total; i += blockDim.x) {
-    const int q = i / per, f = i % per;
-    const int cv = q / L, l = q % L;
-    const int r = (f * 4) / zw, j = (f * 4) % zw;
-    const int64_t u = u0 + r;
-    const int cu = cu_s[r];
-    if (u >= n || cu == cv) continue;
-    const short4 m = __ldg(reinterpret_cast<const short4*>(xmap + ((static_cast<int64_t>(cu) * k + cv) * L + l) * zw + j));
-    const float* xr = xrow + r * pitch;
+  // copy q = cv * L + l of vertex u0 + r: xmap block (cu * k * L + q), output
+  // block q; thread = (r, float4 j) of a copy block, copies strided by qstep
+  const int per = 32 * zw / 4;  // float4s of one copy's tile block (64, 128 or 256)
+  const int qstep = blockDim.x / per;
+  const int f = threadIdx.x % per;
+  const int r = f / (zw / 4), j = (f % (zw / 4)) * 4;
+  const int64_t u = u0 + r;
+  if (u >= n) return;
+  const int cu = cu_s[r];
+  const float* xr = xrow + r * pitch;
+  const int QL = k * L;
+  const int16_t* xm = xmap + static_cast<int64_t>(cu) * QL * zw + j;
+  float* o = out + u * zw + j;
+  for (int q = threadIdx.x / per; q < QL; q += qstep) {
+    if (static_cast<unsigned>(q - cu * L) < static_cast<unsigned>(L)) continue;  // cv == cu: never read
+    const short4 m = __ldg(reinterpret_cast<const short4*>(xm + q * zw));
     const float4 val = make_float4(m.x >= 0 ? xr[m.x] : 0.f, m.y >= 0 ? xr[m.y] : 0.f, m.z >= 0 ? xr[m.z] : 0.f,
                                    m.w >= 0 ? xr[m.w] : 0.f);
-    __stcs(reinterpret_cast<float4*>(out + (static_cast<int64_t>(q) * n + u) * zw + j), val);
+    __stcs(reinterpret_cast<float4*>(o + static_cast<int64_t>(q) * n * zw), val);
   }
 }
 

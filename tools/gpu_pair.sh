@@ -1,4 +1,4 @@
 set -x
-mkdir -p gpurun_out
-timeout 1200 python -m pytest tests/test_gpu_modes.py -x -q 2>&1 | tail -15
-timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -4
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_modes.py tests/test_sharded.py -x -q 2>&1 | tail -3
+timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 --stats 2>&1 | tail -12
+timeout 300 python tools/prof_driver.py --config cfg2 --colorings 5 2>&1 | tail -1
