@@ -1611,7 +1611,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
         P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, L, out);
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
-    dev::ema_rt_blocked<<<grid, 256, e.rt_smem, stream_>>>(
+    dev::ema_rt_blocked<<<grid, dev::kRtBlockedThreads, e.rt_smem, stream_>>>(
         A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
         static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, out);
   } else {
