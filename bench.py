@@ -318,7 +318,7 @@ def run_b200(args, rank, world, local, dist):
                    "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
                    "l2": "inputs larger than L2 (CSR %.0f MB + count tables %.1f GB vs 126 MB L2)"
                          % ((g.csc_col_ptr.nbytes + g.csc_rows.nbytes) / 1e6, need / 1e9)},
-        "roofline": {"kernel": "spmm phase (rooted: bucket_rows + rooted_compress + spmm_rooted + rooted_fixup)",
+        "roofline": {"kernel": "spmm phase (bucket_rows + segment colour order + pair_expand + spmm_rooted + rooted_fixup)",
                      "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
                      "unit": "GB/s", "frac": spmm_gbs / hbm_peak if spmm_gbs else None,
                      "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
@@ -330,7 +330,8 @@ def run_b200(args, rank, world, local, dist):
                              "gathers are L2->SM bound, see l2_gather",
                      "l2_gather": {"achieved": gathered_gbs, "peak": L2_GATHER_PEAK_GBS, "unit": "GB/s",
                                    "frac": gathered_gbs / L2_GATHER_PEAK_GBS if gathered_gbs else None,
-                                   "bytes": "nnz * 4 B * gathered columns (compressed groups x zw, or full panels)"},
+                                   "bytes": "walked entries (nnz * (k-1)/k: own-colour neighbours are skipped) * 4 B * "
+                                            "gathered columns (pair / compressed groups x zw)"},
                      "ema": {"achieved_gbs": ema_gbs, "frac_hbm": ema_gbs / hbm_peak if ema_gbs else None,
                              "tflops": tm.ema_flops / (tm.ema_ms * 1e-3) / 1e12 if tm.ema_ms else None,
                              "ms_per_coloring": tm.ema_ms / args.steps}},

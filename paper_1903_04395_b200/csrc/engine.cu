@@ -237,15 +237,22 @@ Engine::~Engine() {
   cudaSetDevice(cfg_.device);
   release_template();
   release_graph();
+  free_graph_buffers();
   dfree(d_scalars_);
   dfree(d_seeds_);
   dfree(d_colors_);
   if (stream_) cudaStreamDestroy(stream_);
 }
 
-void Engine::release_graph() {
+void Engine::free_graph_buffers() {
   dfree(d_row_ptr_);
   dfree(d_col_);
+  dfree(d_est_acc_);
+  dfree(d_est_tot_);
+  row_ptr_cap_ = col_cap_ = est_acc_cap_ = est_tot_cap_ = 0;
+}
+
+void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the next graph)
   for (auto& kv : sched_)
     for (auto& s : kv.second) release_schedule(s);
   sched_.clear();
@@ -376,8 +383,18 @@ void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* co
 
 void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool validate) {
   host_row_ptr_.assign(row_ptr, row_ptr + n_ + 1);
-  TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (n_ + 1)));
-  TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
+  if (row_ptr_cap_ < n_ + 1) {
+    dfree(d_row_ptr_);
+    row_ptr_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (n_ + 1)));
+    row_ptr_cap_ = n_ + 1;
+  }
+  if (col_cap_ < std::max<int64_t>(nnz_, 1)) {
+    dfree(d_col_);
+    col_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
+    col_cap_ = std::max<int64_t>(nnz_, 1);
+  }
   TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyHostToDevice, stream_));
   if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice, stream_));
   if (validate && nnz_) {
@@ -1915,12 +1932,23 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
   ensure_arena();
   const int chunk = color_chunk(iterations, nglob_);
   ensure_colors(static_cast<int64_t>(chunk) * nglob_);
-  double* d_totals = nullptr;
+  if (est_tot_cap_ < iterations) {
+    dfree(d_est_tot_);
+    est_tot_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&d_est_tot_, sizeof(double) * iterations));
+    est_tot_cap_ = iterations;
+  }
+  double* d_totals = d_est_tot_;
   double* d_acc = nullptr;
-  TCG_CUDA(cudaMalloc(&d_totals, sizeof(double) * iterations));
-  try {
+  {
     if (per_vertex_est && !exec_.empty()) {
-      TCG_CUDA(cudaMalloc(&d_acc, sizeof(double) * std::max(n_, 1)));
+      if (est_acc_cap_ < std::max(n_, 1)) {
+        dfree(d_est_acc_);
+        est_acc_cap_ = 0;
+        TCG_CUDA(cudaMalloc(&d_est_acc_, sizeof(double) * std::max(n_, 1)));
+        est_acc_cap_ = std::max(n_, 1);
+      }
+      d_acc = d_est_acc_;
       TCG_CUDA(cudaMemsetAsync(d_acc, 0, sizeof(double) * std::max(n_, 1), stream_));
     }
     std::vector<uint64_t> seeds(chunk);
@@ -1962,13 +1990,7 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
     }
     for (int i = 0; i < iterations; ++i)
       if (!std::isfinite(totals[i])) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
-  } catch (...) {
-    dfree(d_totals);
-    dfree(d_acc);
-    throw;
   }
-  dfree(d_totals);
-  dfree(d_acc);
   tables_valid_ = false;
 }
 
@@ -2039,10 +2061,12 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
     if (!e.p_leaf && e.pp_dup_of < 0) {
       t.spmm_launches += count;
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
-      // columns actually gathered per neighbour
+      // columns actually gathered per neighbour; the rooted SpMMs never walk
+      // a row's own-color neighbours (expected 1/k of them)
       const int32_t gc = e.lspmm ? e.Cx : e.rooted ? e.rl_groups * e.rl_zw : e.Cp;
-      t.spmm_gathered_bytes += count * nnz * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
-                                                     dev::last_panel_width(gc));
+      const double walked = e.rooted ? nnz * (plan_.k - 1) / plan_.k : nnz;
+      t.spmm_gathered_bytes += count * walked * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
+                                                        dev::last_panel_width(gc));
     }
     t.ema_launches += count;
     t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));

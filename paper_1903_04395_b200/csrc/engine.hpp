@@ -215,6 +215,13 @@ class Engine {
   int64_t nnz_ = 0;
   int64_t* d_row_ptr_ = nullptr;
   int32_t* d_col_ = nullptr;
+  // graph buffers are kept across set_graph calls that fit them (e2e: a new
+  // CSR per call without cudaFree/cudaMalloc of ~1 GB); freed by ~Engine
+  int64_t row_ptr_cap_ = 0, col_cap_ = 0;
+  double* d_est_acc_ = nullptr;      // estimate(): per-vertex fp64 accumulator (n)
+  double* d_est_tot_ = nullptr;      // estimate(): totals (iterations)
+  int64_t est_acc_cap_ = 0, est_tot_cap_ = 0;
+  void free_graph_buffers();
   // part count -> that many part schedules; [1] holds whole rows (also the
   // one-hot histogram's schedule)
   std::map<int, std::vector<PartSchedule>> sched_;
