@@ -2,8 +2,13 @@
 #include "engine.hpp"
 #include "kernels.cuh"
 #include "kernels_rt.cuh"
+#include "kernels_graph.cuh"
+
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -141,6 +146,10 @@ void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
 }
 
 void release_schedule(PartSchedule& s) {
+  if (!s.owned) {
+    s = PartSchedule{};
+    return;
+  }
   dfree(s.d_segs);
   dfree(s.d_split_rows);
   dfree(s.d_slot_begin);
@@ -250,6 +259,10 @@ void Engine::free_graph_buffers() {
   dfree(d_est_acc_);
   dfree(d_est_tot_);
   row_ptr_cap_ = col_cap_ = est_acc_cap_ = est_tot_cap_ = 0;
+  dfree(gp_buf_);
+  gp_n_cap_ = gp_nnz_cap_ = -1;
+  dfree(gp_tmp_);
+  gp_tmp_cap_ = 0;
 }
 
 void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the next graph)
@@ -257,14 +270,14 @@ void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the n
     for (auto& s : kv.second) release_schedule(s);
   sched_.clear();
   dfree(d_tile_tot_);
-  dfree(d_row_order_);
+  d_row_order_ = nullptr;  // (graph-prep block)
   dfree(d_counter_);
   dfree(d_xfull_);
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
-  dfree(d_lchunks_);
-  dfree(d_lfirst_);
+  d_lchunks_ = nullptr;
+  d_lfirst_ = nullptr;
   nlchunks_ = 0;
   host_row_ptr_.clear();
   host_col_.clear();
@@ -382,7 +395,11 @@ void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* co
 }
 
 void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool validate) {
-  host_row_ptr_.assign(row_ptr, row_ptr + n_ + 1);
+  static const bool timing = std::getenv("TCG_TIMING") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+  const auto t0 = now();
+  host_row_ptr_.clear();  // (host copy made lazily by ensure_schedules)
   if (row_ptr_cap_ < n_ + 1) {
     dfree(d_row_ptr_);
     row_ptr_cap_ = 0;
@@ -402,50 +419,19 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
     dev::validate_csr<<<148 * 8, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, reinterpret_cast<int*>(d_scalars_ + 4));
     ++launches_;
   }
+  if (timing) TCG_CUDA(cudaStreamSynchronize(stream_));
+  const auto t1 = now();
   // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
   // sparse skewed graphs (cfg2, avg ~30) the hub rows stay L2-resident anyway
   // and extra parts only add output passes (measured: profiles/ DESIGN.md 3).
   if (!std::getenv("TCG_PART_MB") && !std::getenv("TCG_PART_KB"))
     part_bytes_ = (n_ > 0 && nnz_ / std::max(n_, 1) >= 64) ? (64ll << 20) : (128ll << 20);
   max_slots_ = 0;
-  {  // whole-row schedule: the rooted SpMM, the histogram, P = 1 panels
-    std::vector<int64_t> lo(row_ptr, row_ptr + n_), hi(row_ptr + 1, row_ptr + n_ + 1);
-    static const bool by_id = std::getenv("TCG_SEG_ID") && std::atoi(std::getenv("TCG_SEG_ID")) > 0;
-    sched_[1].push_back(build_schedule(lo, hi, true, stream_, !by_id));
-    max_slots_ = sched_[1][0].nslots;
-  }
-  {  // rows by degree, descending (stable counting sort), for the per-coloring bucketing
-    int64_t maxd = 0;
-    for (int32_t v = 0; v < n_; ++v) maxd = std::max(maxd, row_ptr[v + 1] - row_ptr[v]);
-    std::vector<int64_t> start(static_cast<size_t>(maxd) + 2, 0);
-    for (int32_t v = 0; v < n_; ++v) ++start[maxd - (row_ptr[v + 1] - row_ptr[v]) + 1];
-    for (size_t i = 1; i < start.size(); ++i) start[i] += start[i - 1];
-    std::vector<int32_t> order(static_cast<size_t>(n_));
-    for (int32_t v = 0; v < n_; ++v) order[start[maxd - (row_ptr[v + 1] - row_ptr[v])]++] = v;
-    d_row_order_ = dupload(order, stream_);
-    nlong_ = 0;
-    while (nlong_ < n_ && row_ptr[order[nlong_] + 1] - row_ptr[order[nlong_]] > dev::kBucketLong) ++nlong_;
-    {  // hub rows -> chunks of kLongChunk entries (offsets within the row)
-      std::vector<int4> ch;
-      std::vector<int32_t> first{0};
-      for (int32_t r = 0; r < nlong_; ++r) {
-        const int32_t v = order[r];
-        const int64_t d = row_ptr[v + 1] - row_ptr[v];
-        int32_t q = 0;
-        for (int64_t o = 0; o < d; o += dev::kLongChunk, ++q)
-          ch.push_back(make_int4(v, static_cast<int32_t>(o), static_cast<int32_t>(std::min<int64_t>(d, o + dev::kLongChunk)), q));
-        first.push_back(static_cast<int32_t>(ch.size()));
-      }
-      nlchunks_ = static_cast<int32_t>(ch.size());
-      if (nlchunks_) {
-        d_lchunks_ = dupload(ch, stream_);
-        d_lfirst_ = dupload(first, stream_);
-      }
-    }
-    nsmall_ = nlong_;  // rows of degree <= kBucketSmall: a thread each
-    while (nsmall_ < n_ && row_ptr[order[nsmall_] + 1] - row_ptr[order[nsmall_]] > dev::kBucketSmall) ++nsmall_;
-    TCG_CUDA(cudaMalloc(&d_counter_, 64));
-  }
+  const auto t2 = now();
+  prep_graph_device();  // whole-row schedule, degree order, hub chunks (kernels_graph.cuh)
+  max_slots_ = sched_[1][0].nslots;
+  TCG_CUDA(cudaMalloc(&d_counter_, 64));
+  const auto t3 = now();
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
   TCG_CUDA(cudaStreamSynchronize(stream_));
@@ -459,13 +445,156 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
       throw invalid_argument("CSR row not strictly ascending");
     }
   }
+  const auto t4 = now();
   if (have_template_) plan_arena();
+  if (timing)
+    std::fprintf(stderr, "[tcg timing] set_graph: h2d+validate %.1f, device prep %.1f, sync %.1f, plan %.1f ms\n",
+                 ms(t0, t1), ms(t2, t3), ms(t3, t4), ms(t4, now()));
   tables_valid_ = false;
+}
+
+// Whole-row segment schedule (sched_[1]), degree order and hub-row chunks of
+// the bucketing, built on the device from d_row_ptr_ (same result as the
+// host builders; kernels_graph.cuh).  Buffers are carved from one block kept
+// across graphs that fit it.
+void Engine::prep_graph_device() {
+  static_assert(dev::kSegMax == dev::kBucketLong, "split rows == hub rows");
+  const int64_t n = n_, nnz = nnz_;
+  const int64_t nseg_max = n + nnz / dev::kSegMax + 1;
+  const int64_t nsplit_max = nnz / (dev::kSegMax + 1) + 1;
+  const int64_t nslot_max = nnz / dev::kSegMax + nsplit_max + 1;
+  const int64_t nch_max = nnz / dev::kLongChunk + nsplit_max + 1;
+  const int64_t nseg_pad_max = (nseg_max + dev::kSegPad - 1) / dev::kSegPad * dev::kSegPad + dev::kSegPad;
+  struct Carve {
+    int64_t off = 0;
+    int64_t take(int64_t bytes) { const int64_t o = off; off += (bytes + 255) / 256 * 256; return o; }
+  } cv;
+  const int64_t o_nseg = cv.take(4 * (n + 1)), o_segoff = cv.take(4 * (n + 1));
+  const int64_t o_nslot = cv.take(4 * (n + 1)), o_slotoff = cv.take(4 * (n + 1));
+  const int64_t o_split = cv.take(4 * (n + 1)), o_splitoff = cv.take(4 * (n + 1));
+  const int64_t o_okey = cv.take(4 * n), o_okey2 = cv.take(4 * n), o_ids = cv.take(4 * n), o_order = cv.take(4 * n);
+  const int64_t o_segs = cv.take(16 * nseg_max), o_keys = cv.take(4 * nseg_max), o_keys2 = cv.take(4 * nseg_max);
+  const int64_t o_vals = cv.take(4 * nseg_max), o_perm = cv.take(4 * nseg_max);
+  const int64_t o_out = cv.take(16 * nseg_pad_max);
+  const int64_t o_srows = cv.take(4 * nsplit_max), o_sbegin = cv.take(4 * (nsplit_max + 1));
+  const int64_t o_srow = cv.take(4 * nslot_max);
+  const int64_t o_nch = cv.take(4 * (nsplit_max + 1)), o_first = cv.take(4 * (nsplit_max + 1));
+  const int64_t o_chunks = cv.take(16 * nch_max), o_small = cv.take(16);
+  if (n > gp_n_cap_ || nnz > gp_nnz_cap_) {
+    dfree(gp_buf_);
+    gp_n_cap_ = gp_nnz_cap_ = -1;
+    TCG_CUDA(cudaMalloc(&gp_buf_, cv.off));
+    gp_n_cap_ = n;
+    gp_nnz_cap_ = nnz;
+  }
+  auto at = [&](int64_t o) { return gp_buf_ + o; };
+  int32_t* nseg = reinterpret_cast<int32_t*>(at(o_nseg));
+  int32_t* segoff = reinterpret_cast<int32_t*>(at(o_segoff));
+  int32_t* nslot = reinterpret_cast<int32_t*>(at(o_nslot));
+  int32_t* slotoff = reinterpret_cast<int32_t*>(at(o_slotoff));
+  int32_t* split = reinterpret_cast<int32_t*>(at(o_split));
+  int32_t* splitoff = reinterpret_cast<int32_t*>(at(o_splitoff));
+  uint32_t* okey = reinterpret_cast<uint32_t*>(at(o_okey));
+  uint32_t* okey2 = reinterpret_cast<uint32_t*>(at(o_okey2));
+  int32_t* ids = reinterpret_cast<int32_t*>(at(o_ids));
+  int32_t* order = reinterpret_cast<int32_t*>(at(o_order));
+  dev::Seg* segs = reinterpret_cast<dev::Seg*>(at(o_segs));
+  uint32_t* keys = reinterpret_cast<uint32_t*>(at(o_keys));
+  uint32_t* keys2 = reinterpret_cast<uint32_t*>(at(o_keys2));
+  int32_t* vals = reinterpret_cast<int32_t*>(at(o_vals));
+  int32_t* perm = reinterpret_cast<int32_t*>(at(o_perm));
+  dev::Seg* out = reinterpret_cast<dev::Seg*>(at(o_out));
+  int32_t* srows = reinterpret_cast<int32_t*>(at(o_srows));
+  int32_t* sbegin = reinterpret_cast<int32_t*>(at(o_sbegin));
+  int32_t* srow = reinterpret_cast<int32_t*>(at(o_srow));
+  int32_t* nch = reinterpret_cast<int32_t*>(at(o_nch));
+  int32_t* first = reinterpret_cast<int32_t*>(at(o_first));
+  int4* chunks = reinterpret_cast<int4*>(at(o_chunks));
+  int32_t* nsmall = reinterpret_cast<int32_t*>(at(o_small));
+  auto tmp = [&](size_t need) {
+    if (need > gp_tmp_cap_) {
+      dfree(gp_tmp_);
+      gp_tmp_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&gp_tmp_, need));
+      gp_tmp_cap_ = need;
+    }
+    return gp_tmp_;
+  };
+  auto scan = [&](const int32_t* in, int32_t* o, int64_t items) {
+    size_t b = 0;
+    TCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, in, o, static_cast<int>(items), stream_));
+    void* t = tmp(b);
+    TCG_CUDA(cub::DeviceScan::ExclusiveSum(t, b, in, o, static_cast<int>(items), stream_));
+  };
+  auto sort = [&](const uint32_t* k, uint32_t* k2, const int32_t* v, int32_t* v2, int64_t items, int bits) {
+    size_t b = 0;
+    TCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, k, k2, v, v2, static_cast<int>(items), 0, bits, stream_));
+    void* t = tmp(b);
+    TCG_CUDA(cub::DeviceRadixSort::SortPairs(t, b, k, k2, v, v2, static_cast<int>(items), 0, bits, stream_));
+  };
+  const unsigned g1 = static_cast<unsigned>((n + 1 + 255) / 256);
+  TCG_CUDA(cudaMemsetAsync(nsmall, 0, sizeof(int32_t), stream_));
+  dev::graph_row_counts<<<g1, 256, 0, stream_>>>(d_row_ptr_, n_, nseg, nslot, split, okey, ids, nsmall);
+  scan(nseg, segoff, n + 1);
+  scan(nslot, slotoff, n + 1);
+  scan(split, splitoff, n + 1);
+  if (n) sort(okey, okey2, ids, order, n, 32);
+  int32_t tot[4];
+  TCG_CUDA(cudaMemcpyAsync(&tot[0], segoff + n, 4, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaMemcpyAsync(&tot[1], slotoff + n, 4, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaMemcpyAsync(&tot[2], splitoff + n, 4, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaMemcpyAsync(&tot[3], nsmall, 4, cudaMemcpyDeviceToHost, stream_));
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+  const int64_t nseg_tot = tot[0];
+  const int nslots = tot[1], nsplit = tot[2];
+  if (n) {
+    dev::graph_emit_segs<<<static_cast<unsigned>((n + 255) / 256), 256, 0, stream_>>>(d_row_ptr_, n_, segoff, slotoff, splitoff,
+                                                                                    segs, keys, vals, srows, sbegin, srow);
+    TCG_CUDA(cudaMemcpyAsync(sbegin + nsplit, &tot[1], 4, cudaMemcpyHostToDevice, stream_));
+    sort(keys, keys2, vals, perm, nseg_tot, 11);
+  }
+  const int64_t padded = std::max<int64_t>((nseg_tot + dev::kSegPad - 1) / dev::kSegPad * dev::kSegPad, dev::kSegPad);
+  dev::graph_gather_segs<<<static_cast<unsigned>((padded + 255) / 256), 256, 0, stream_>>>(segs, perm, nseg_tot, padded, out);
+  PartSchedule ps;
+  ps.owned = false;
+  ps.d_segs = out;
+  ps.nseg_padded = padded;
+  ps.nsplit_rows = nsplit;
+  ps.nslots = nslots;
+  if (nsplit) {
+    ps.d_split_rows = srows;
+    ps.d_slot_begin = sbegin;
+    ps.d_slot_row = srow;
+  }
+  sched_[1].push_back(ps);
+  d_row_order_ = order;
+  nlong_ = nsplit;
+  nsmall_ = tot[3];
+  nlchunks_ = 0;
+  d_lchunks_ = nullptr;
+  d_lfirst_ = nullptr;
+  if (nlong_) {
+    dev::graph_long_counts<<<static_cast<unsigned>((nlong_ + 1 + 255) / 256), 256, 0, stream_>>>(d_row_ptr_, order, nlong_, nch);
+    scan(nch, first, nlong_ + 1);
+    int32_t nc = 0;
+    TCG_CUDA(cudaMemcpyAsync(&nc, first + nlong_, 4, cudaMemcpyDeviceToHost, stream_));
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    nlchunks_ = nc;
+    dev::graph_long_chunks<<<static_cast<unsigned>((nlong_ + 255) / 256), 256, 0, stream_>>>(d_row_ptr_, order, nlong_, first, chunks);
+    d_lchunks_ = chunks;
+    d_lfirst_ = first;
+  }
+  launches_ += 0;  // (graph preparation: not part of a coloring)
+  TCG_CUDA(cudaGetLastError());
 }
 
 // Vertex-range part schedules for the full-table SpMM (P parts per panel).
 void Engine::ensure_schedules(int P) {
   if (sched_.count(P)) return;
+  if (host_row_ptr_.empty()) {
+    host_row_ptr_.resize(static_cast<size_t>(n_) + 1);
+    copy_sync(host_row_ptr_.data(), d_row_ptr_, sizeof(int64_t) * (n_ + 1), cudaMemcpyDeviceToHost);
+  }
   if (host_col_.empty() && nnz_) {
     host_col_.resize(static_cast<size_t>(nnz_));
     copy_sync(host_col_.data(), d_col_, sizeof(int32_t) * nnz_, cudaMemcpyDeviceToHost);

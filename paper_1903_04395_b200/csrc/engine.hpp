@@ -114,6 +114,7 @@ struct PartSchedule {
   int32_t* d_slot_begin = nullptr;
   int32_t* d_slot_row = nullptr;  // partial slot -> row
   int nsplit_rows = 0, nslots = 0;
+  bool owned = true;              // false: buffers live in the engine's graph-prep block
 };
 
 // All-gather of equal-size per-rank device buffers (SpMM panels, totals).
@@ -237,6 +238,13 @@ class Engine {
   int4* d_lchunks_ = nullptr;        // hub-row chunks {row, begin, end, index in row}
   int32_t* d_lfirst_ = nullptr;      // first chunk of each hub row (nlong_ + 1)
   int32_t nlchunks_ = 0;
+  // device-built whole-row schedule + degree order (kernels_graph.cuh): one
+  // block reused across set_graph calls of the same (or smaller) size
+  char* gp_buf_ = nullptr;
+  int64_t gp_n_cap_ = -1, gp_nnz_cap_ = -1;
+  void* gp_tmp_ = nullptr;
+  size_t gp_tmp_cap_ = 0;
+  void prep_graph_device();
   int64_t lcnt_off_ = -1;            // per-coloring chunk color counts [chunks][32]
   int* d_counter_ = nullptr;
 

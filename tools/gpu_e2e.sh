@@ -1,4 +1,5 @@
 set -x
-timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_sharded.py -x -q 2>&1 | tail -2
-python tools/e2e_probe.py cfg3
-python tools/e2e_probe.py cfg2
+timeout 1500 python -m pytest tests -x -q -m gpu 2>&1 | tail -3
+TCG_TIMING=1 python tools/e2e_probe.py cfg3
+TCG_TIMING=1 python tools/e2e_probe.py cfg2
+timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 2>&1 | tail -1
