@@ -263,15 +263,16 @@ void Engine::free_graph_buffers() {
   gp_n_cap_ = gp_nnz_cap_ = -1;
   dfree(gp_tmp_);
   gp_tmp_cap_ = 0;
+  dfree(d_tile_tot_);
+  tile_tot_cap_ = 0;
+  dfree(d_counter_);
 }
 
 void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the next graph)
   for (auto& kv : sched_)
     for (auto& s : kv.second) release_schedule(s);
   sched_.clear();
-  dfree(d_tile_tot_);
-  d_row_order_ = nullptr;  // (graph-prep block)
-  dfree(d_counter_);
+  d_row_order_ = nullptr;  // (graph-prep block; d_tile_tot_ / d_counter_ are kept)
   dfree(d_xfull_);
   dfree(d_colors_pad_);
   dfree(d_gather_);
@@ -430,10 +431,10 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   const auto t2 = now();
   prep_graph_device();  // whole-row schedule, degree order, hub chunks (kernels_graph.cuh)
   max_slots_ = sched_[1][0].nslots;
-  TCG_CUDA(cudaMalloc(&d_counter_, 64));
+  if (!d_counter_) TCG_CUDA(cudaMalloc(&d_counter_, 64));
   const auto t3 = now();
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
-  TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * std::max<int64_t>(ntiles, 1)));
+  ensure_tile_tot(ntiles);
   TCG_CUDA(cudaStreamSynchronize(stream_));
   if (validate && nnz_) {
     int bad = 0;
@@ -1137,13 +1138,23 @@ void Engine::setup_rooted_ema(int max_smem) {
 // per-group scatter: used when the plan with full P' tables does not fit the
 // device (or the memory budget).  TCG_PSTREAM: 0 never, 1 when needed
 // (default), 2 always (also with TCG_KEEP_TABLES; tests).
+void Engine::ensure_tile_tot(int64_t count) {
+  count = std::max<int64_t>(count, 1);
+  if (count <= tile_tot_cap_) return;
+  dfree(d_tile_tot_);
+  tile_tot_cap_ = 0;
+  TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * count));
+  tile_tot_cap_ = count;
+}
+
 void Engine::plan_arena() {
   static const int pstream_mode = [] {
     const char* s = std::getenv("TCG_PSTREAM");
     return s ? std::atoi(s) : 1;
   }();
   plan_arena_once(pstream_mode == 2);
-  if (pstream_mode == 1 && !(cfg_.flags & TCG_KEEP_TABLES)) {
+  // (an arena already allocated at this size needs no device-memory query)
+  if (pstream_mode == 1 && !(cfg_.flags & TCG_KEEP_TABLES) && !(arena_ && arena_bytes_ <= arena_alloc_)) {
     size_t fr = 0, tot = 0;
     TCG_CUDA(cudaMemGetInfo(&fr, &tot));
     int64_t limit = static_cast<int64_t>(fr) + (arena_ ? arena_alloc_ : 0) - partial_bytes_ - (3ll << 30);
@@ -1201,8 +1212,7 @@ void Engine::plan_arena_once(bool allow_stream) {
     vs_off_ = ap.alloc(4 * std::max<int64_t>(n_, 1));
     tiles_off_ = ap.alloc(16 * static_cast<int64_t>(max_tiles_));
     vcnt_off_ = ap.alloc(4 * static_cast<int64_t>((n_ + dev::kVsChunk - 1) / dev::kVsChunk + 1) * plan_.k);
-    dfree(d_tile_tot_);
-    TCG_CUDA(cudaMalloc(&d_tile_tot_, sizeof(double) * max_tiles_));
+    ensure_tile_tot(max_tiles_);
   }
   if (need_rooted_) {
     const int slots = sched_.at(1)[0].nslots;
@@ -1345,13 +1355,13 @@ void Engine::ensure_arena() {
   if (cfg_.memory_budget > 0 && arena_bytes_ > cfg_.memory_budget)
     throw resource_error("count tables need " + std::to_string(arena_bytes_) +
                          " bytes, over the budget of " + std::to_string(cfg_.memory_budget));
-  if (arena_alloc_ != arena_bytes_ || !arena_) {
+  if (arena_bytes_ > arena_alloc_ || !arena_) {  // (grow only: no free/malloc per graph)
     dfree(arena_);
     arena_alloc_ = 0;
     TCG_CUDA(cudaMalloc(&arena_, std::max<int64_t>(arena_bytes_, kAlign)));
     arena_alloc_ = arena_bytes_;
   }
-  if (partial_alloc_ != partial_bytes_) {
+  if (partial_bytes_ > partial_alloc_) {
     dfree(d_partial_);
     partial_alloc_ = 0;
     if (partial_bytes_) TCG_CUDA(cudaMalloc(&d_partial_, partial_bytes_));
@@ -2057,6 +2067,9 @@ static int color_chunk(int count, int32_t n) {
 void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est, double* se,
                       double* per_vertex_est) {
   if (iterations < 1) throw invalid_argument("iterations must be >= 1");
+  static const bool timing = std::getenv("TCG_TIMING") != nullptr;
+  const auto t0 = std::chrono::steady_clock::now();
+  auto since = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
   TCG_CUDA(cudaSetDevice(cfg_.device));
   ensure_arena();
   const int chunk = color_chunk(iterations, nglob_);
@@ -2087,6 +2100,11 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
       gen_colors(seeds.data(), c, d_colors_);
       for (int j = 0; j < c; ++j)
         run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, d_acc, nullptr);
+    }
+    if (timing) {
+      const double q = since();
+      TCG_CUDA(cudaStreamSynchronize(stream_));
+      std::fprintf(stderr, "[tcg timing] estimate: enqueue %.1f ms, device done %.1f ms\n", q, since());
     }
     TCG_CUDA(cudaMemcpyAsync(totals, d_totals, sizeof(double) * iterations, cudaMemcpyDeviceToHost, stream_));
     std::vector<double> acc;
@@ -2120,6 +2138,7 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
     for (int i = 0; i < iterations; ++i)
       if (!std::isfinite(totals[i])) throw nonfinite_error("rooted total is not finite (fp64 overflow)");
   }
+  if (timing) std::fprintf(stderr, "[tcg timing] estimate: total %.1f ms\n", since());
   tables_valid_ = false;
 }
 

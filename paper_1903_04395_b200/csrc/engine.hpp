@@ -282,6 +282,8 @@ class Engine {
   double* d_partial_ = nullptr;
   int64_t partial_bytes_ = 0, partial_alloc_ = 0;
   double* d_tile_tot_ = nullptr;
+  int64_t tile_tot_cap_ = 0;
+  void ensure_tile_tot(int64_t count);
   double* d_scalars_ = nullptr;      // [0] total of run_coloring
   uint8_t* d_colors_ = nullptr;      // color batch
   int64_t colors_cap_ = 0;

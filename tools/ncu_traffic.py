@@ -14,7 +14,7 @@ from collections import defaultdict
 
 
 def phase(name):
-    if name.startswith(("bucket_", "rooted_", "spmm_", "lspmm", "color_bucket")):
+    if name.startswith(("bucket_", "rooted_", "spmm_", "lspmm", "color_bucket", "pair_expand", "seg_")):
         return "spmm"
     if name.startswith(("ema_", "root_reduce")):
         return "ema"
