@@ -677,7 +677,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
       int fpad_max = 0;
       for (int g = 0; g < rl.groups; ++g)
         fpad_max = std::max(fpad_max, (g + 1 < rl.groups ? rl.fbase[g + 1] : rl.store_cols) - rl.fbase[g]);
-      const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * (fpad_max + 4) * 4;
+      const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * (fpad_max + 4) * 4 + 2 * (k + 1) * rl.zw;
       // (rooted_compress stages at least one full row of M_p in smem)
       if (smem <= static_cast<size_t>(max_smem) - 4096 && 4 * dev::table_floats(e.Cp, 1) <= max_smem - 4096) {
         e.rooted = true;
@@ -706,7 +706,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
           int fpad1 = 0;
           for (int g = 0; g < r1.groups; ++g)
             fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
-          const size_t smem1 = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4;
+          const size_t smem1 = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4 + 2 * k * r1.zw;
           const int64_t wx = B(k - 1, e.sp - 1);
           const int64_t lines_old = static_cast<int64_t>(rl.groups) * rl.zw, lines_new = static_cast<int64_t>(r1.groups) * r1.zw;
           const int64_t copy_bytes = 4ll * k * lines_new;
@@ -935,7 +935,7 @@ void Engine::setup_rooted_ema(int max_smem) {
     int fpad1 = 0;
     for (int g = 0; g < r1.groups; ++g)
       fpad1 = std::max(fpad1, (g + 1 < r1.groups ? r1.fbase[g + 1] : r1.store_cols) - r1.fbase[g]);
-    e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4;
+    e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / r1.zw) * (fpad1 + 4) * 4 + 2 * k * r1.zw;
     dfree(e.d_slot_acc);
     e.slot_K = k - 1;
     e.d_slot_acc = dupload(dummy_slots(r1, k - 1), stream_);
@@ -1192,7 +1192,7 @@ void Engine::plan_arena_once(bool allow_stream) {
   rcol_off_ = rcut_off_ = -1;
   int64_t rooted_partial = 0;
   if (need_rooted_) {
-    if (nsrc_ >= (1 << dev::kPackShift))
+    if (nsrc_ >= (1ll << (32 - dev::kColorBits)))
       throw invalid_argument("graph too large for the rooted-compressed SpMM (ids >= 2^27); set TCG_ROOTED=0");
     rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
     rcut_off_ = ap.alloc(8 * static_cast<int64_t>(n_) * (rooted_parts_ + 1));
@@ -1639,7 +1639,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const int fpad = (g + 1 < G ? e.rl_fbase[g + 1] : e.Cps) - gbase;
     const int fbase = out ? 0 : gbase;       // streamed: the group's columns at 0 of the scratch
     const int32_t Cst = out ? e.Ct : e.Cps;
-    const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * (fpad + 4) * 4;
+    const size_t smem = static_cast<size_t>(dev::kSpmmWarps) * spw * (fpad + 4) * 4 + 2 * (e.slot_K + 1) * zw;
     const int16_t* sl = e.d_slot_acc + static_cast<int64_t>(g) * zw;
     int slot_stride = G * zw;
     for (int q = 0; q < rooted_parts_; ++q) {

@@ -428,9 +428,13 @@ lspmm_combine(const float* __restrict__ Q, int64_t q_stride, int c0, int nc,
 // compressed panel slots mean the same parent columns, so the run is summed
 // in registers and scattered into the task's F_g accumulators (smem, fp64)
 // once per run.
+// packed entry = u << 5 | color (n < 2^27): within a round (one color c) the
+// row address X + u * ZW * 4 is (X - c * ZW / 8) + entry * ZW / 8, one
+// IMAD.WIDE per entry
 constexpr uint32_t kPackSentinel = 0xFFFFFFFFu;  // color 31: never a real color (k <= 20)
-constexpr int kPackShift = 27;
-constexpr uint32_t kPackMask = (1u << kPackShift) - 1u;
+constexpr int kColorBits = 5;
+constexpr uint32_t kColorMask = (1u << kColorBits) - 1u;
+__device__ __forceinline__ uint32_t pack_entry(uint32_t u, uint32_t color) { return u << kColorBits | color; }
 
 // Neighbour colors are sorted in the row's ROTATED order: key(c) = (c - cv - 1)
 // mod k for a row of color cv, so the run of the row's own color comes last
@@ -525,7 +529,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
         const int slot = key[q] >= 0 ? cnt[key[q]] + __popc(same & lt) : 0;
         __syncwarp();
         if (key[q] >= 0) {
-          out[b + slot] = static_cast<uint32_t>(u[q]) | (static_cast<uint32_t>(unrot_key(key[q], cv, k)) << kPackShift);
+          out[b + slot] = pack_entry(static_cast<uint32_t>(u[q]), static_cast<uint32_t>(unrot_key(key[q], cv, k)));
           if ((same & lt) == 0) cnt[key[q]] += __popc(same);
         }
         __syncwarp();
@@ -548,7 +552,7 @@ bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col
         const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
         __syncwarp();
         if (ok) {
-          out[b + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(unrot_key(key, cv, k)) << kPackShift);
+          out[b + slot] = pack_entry(static_cast<uint32_t>(u), static_cast<uint32_t>(unrot_key(key, cv, k)));
           if ((same & lt) == 0) cnt[key] += __popc(same);
         }
         __syncwarp();
@@ -597,7 +601,7 @@ bucket_small(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ co
       int uu = u[0];  // u[pos] with static register indices
 #pragma unroll
       for (int q = 1; q < kBucketSmall; ++q) uu = pos == q ? u[q] : uu;
-      out[b + j] = static_cast<uint32_t>(uu) | (static_cast<uint32_t>(unrot_key(static_cast<int>(key[j] >> 4), cv, k)) << kPackShift);
+      out[b + j] = pack_entry(static_cast<uint32_t>(uu), static_cast<uint32_t>(unrot_key(static_cast<int>(key[j] >> 4), cv, k)));
     }
   }
   auto below = [&](int c) {  // entries of color < c
@@ -731,7 +735,7 @@ bucket_long_scatter(const int4* __restrict__ chunks, const int64_t* __restrict__
     const int slot = ok ? cnt[key] + __popc(same & lt) : 0;
     __syncwarp();
     if (ok) {
-      out[rb + slot] = static_cast<uint32_t>(u) | (static_cast<uint32_t>(unrot_key(key, cv, k)) << kPackShift);
+      out[rb + slot] = pack_entry(static_cast<uint32_t>(u), static_cast<uint32_t>(unrot_key(key, cv, k)));
       if ((same & lt) == 0) cnt[key] += __popc(same);
     }
     __syncwarp();
@@ -798,6 +802,11 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
   extern __shared__ float racc_sm[];
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
+  // this group's slot table (K + 1 rows of ZW) after the accumulators
+  int16_t* slot_sm = reinterpret_cast<int16_t*>(racc_sm + kSpmmWarps * SPW * (fpad + 4));
+  for (int i = threadIdx.x; i < (kdummy + 1) * ZW; i += blockDim.x)
+    slot_sm[i] = slot_acc[static_cast<int64_t>(i / ZW) * slot_stride + i % ZW];
+  __syncthreads();
   const int64_t task = static_cast<int64_t>(blockIdx.x) * kSpmmWarps + warp;
   if (task >= ntasks) return;
   const Seg s = segs[task * SPW + g];
@@ -832,9 +841,9 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   fetch(0, w);
   __syncwarp();
   const char* Xl = reinterpret_cast<const char*>(X + (PAIR ? static_cast<int64_t>(cv) * xstride : 0) + l * 4);
-  const int16_t* sla = slot_acc + l * 4;
+  const int16_t* sla = slot_sm + l * 4;
   auto scatter = [&]() {  // the finished run into its slots' accumulators (dummy for unused slots)
-    const short4 sl = __ldg(reinterpret_cast<const short4*>(sla + cur * slot_stride));
+    const short4 sl = *reinterpret_cast<const short4*>(sla + cur * ZW);
     acc[sl.x] += static_cast<float>(r0);
     acc[sl.y] += static_cast<float>(r1);
     acc[sl.z] += static_cast<float>(r2);
@@ -845,27 +854,27 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
   for (;;) {
     // the round = the prefix of the next R entries sharing entry 0's color
     // (entry j sits in lane j % G, word j / G of the group)
-    const uint32_t c_round = __shfl_sync(0xffffffffu, w[0], g * G) >> kPackShift;
+    const uint32_t c_round = __shfl_sync(0xffffffffu, w[0], 0, G) & kColorMask;
     // the slot table's color index: relabeled past cv in the pair layout
     const uint32_t c_slot = PAIR ? c_round - (c_round > cv ? 1u : 0u) : c_round;
     int count = 0;
 #pragma unroll
     for (int i = 0; i < NI; ++i) {
-      const bool ok = w[i] != kPackSentinel && (w[i] >> kPackShift) == c_round;
+      const bool ok = w[i] != kPackSentinel && (w[i] & kColorMask) == c_round;
       count += __popc(__ballot_sync(0xffffffffu, ok) & gmask);
     }
     if (!__any_sync(0xffffffffu, count > 0)) break;
     uint32_t pk[R];
 #pragma unroll
-    for (int j = 0; j < R; ++j) pk[j] = __shfl_sync(0xffffffffu, w[j / G], g * G + (j % G));
+    for (int j = 0; j < R; ++j) pk[j] = __shfl_sync(0xffffffffu, w[j / G], j % G, G);
     pos += count;
     fetch(pos, w);  // next round's entries, overlapping this round's gathers
     float4 v[R];
+    const char* Xr = Xl - c_round * (ZW / 8);  // entry * ZW / 8 = u * ZW * 4 + c_round * ZW / 8
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       v[j] = make_float4(0, 0, 0, 0);
-      if (j < count)
-        v[j] = ld_keep_f4(row_addr(Xl, pk[j] & kPackMask, ZW * 4), pkeep);
+      if (j < count) v[j] = ld_keep_f4(row_addr(Xr, pk[j], ZW / 8), pkeep);
     }
     if (count > 0 && static_cast<int>(c_slot) != cur) {
       scatter();

@@ -32,7 +32,7 @@ def main():
     per = defaultdict(lambda: {"name": "", "read": 0.0, "write": 0.0, "time": 0.0})
     for r in rows[1:]:
         d = per[r[ii]]
-        d["name"] = r[ki].split("(")[0].strip().replace("void ", "")
+        d["name"] = r[ki].split("(")[0].strip().replace("void ", "").replace("tcg::dev::", "").replace("tcg::", "")
         val = float(r[vi].replace(",", "")) * scale.get(r[ui], 1)
         if r[mi] == "dram__bytes_read.sum":
             d["read"] = val
