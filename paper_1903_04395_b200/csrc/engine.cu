@@ -1225,6 +1225,24 @@ void Engine::plan_arena_once(bool allow_stream) {
     if (y.pair) feeds_pair[y.p] = 1;
   for (const auto& x : exec_)
     if (x.dup_of >= 0 && feeds_pair[x.id]) feeds_pair[exec_[x.dup_of].id] = 1;
+  // Virtual active-leaf tables: an active-leaf node read only as its parent's
+  // ACTIVE child is M_s[v, S] = P'[v, S minus c(v)], so the parent stages P'
+  // through this node's per-color P' map and the permuted copy is never
+  // written (TCG_VIRT=0 disables; inspection contexts materialize it).
+  static const int virt_mode = [] {
+    const char* s = std::getenv("TCG_VIRT");
+    return s ? std::atoi(s) : 1;
+  }();
+  {
+    std::vector<int> active_uses(plan_.num_nodes, 0), aliased(plan_.num_nodes, 0);
+    for (const auto& y : exec_) {
+      if (y.dup_of < 0 && !y.a_leaf) ++active_uses[y.a];
+      if (y.dup_of >= 0) aliased[exec_[y.dup_of].id] = 1;
+    }
+    for (auto& e : exec_)
+      e.virt = virt_mode && !keep && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.dup_of < 0 &&
+               !aliased[e.id] && active_uses[e.id] == 1 && !feeds_pair[e.id] && !e.skip_ema && !e.lspmm;
+  }
   for (auto& e : exec_) {
     if (e.dup_of >= 0) {  // alias the first occurrence; release this node's own children
       const NodeExec& x = exec_[e.dup_of];
@@ -1242,7 +1260,7 @@ void Engine::plan_arena_once(bool allow_stream) {
     }
     e.pstream = false;
     if (allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.d_emap && e.pp_dup_of < 0 &&
-        !feeds_pair[e.id]) {
+        !feeds_pair[e.id] && !e.virt) {
       bool shared = false;
       for (const auto& y : exec_) shared |= y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id;
       e.pstream = !shared;
@@ -1304,6 +1322,10 @@ void Engine::plan_arena_once(bool allow_stream) {
     if (!e.p_leaf && e.pp_dup_of < 0)
       for (const auto& y : exec_)  // one reference per node sharing this P'
         if (y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id) ap.retain(e.pp_off);
+    if (e.virt) {  // the table IS P' (released by the parent, which reads it as its active child)
+      table_off_[e.id] = e.out_off = e.pp_off;
+      continue;
+    }
     if (e.skip_ema) {                 // M of this node is never needed
       table_off_[e.id] = -1;
       e.out_off = -1;
@@ -1323,11 +1345,16 @@ void Engine::plan_arena_once(bool allow_stream) {
   // consumers of a packed (streamed, RR) active table stage it through its amap
   for (auto& e : exec_) {
     e.d_amap_in = nullptr;
+    e.Ca_in = e.Wa;
     if (e.a_leaf) continue;
     for (const auto& x : exec_)
       if (x.id == e.a) {
         const NodeExec& src = x.dup_of >= 0 ? exec_[x.dup_of] : x;
         if (src.pstream && src.omap.empty()) e.d_amap_in = src.d_amap;
+        if (src.virt) {  // stage the child's P' through its P' map
+          e.d_amap_in = src.d_pmap;
+          e.Ca_in = src.Cpt;
+        }
       }
   }
   arena_bytes_ = ap.peak;
@@ -1728,13 +1755,13 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     if (e.root) {
       double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
       attr(reinterpret_cast<const void*>(dev::ema_rtv_root));
-      dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
+      dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
       auto kern = e.rtv_h == 8 ? dev::ema_rtv_blocked<8> : e.rtv_h == 7 ? dev::ema_rtv_blocked<7> : dev::ema_rtv_blocked<6>;
       attr(reinterpret_cast<const void*>(kern));
       kern<<<vgrid, 256, e.rt_smem, stream_>>>(
-          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
           static_cast<const uint2*>(e.d_rtv_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V,
           e.rtv_sa, e.rtv_sp);
     }
@@ -1746,11 +1773,11 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     if (e.a_leaf) {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<true>));
       dev::ema_rt_root<true><<<grid, 64, e.rt_smem, stream_>>>(
-          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     } else {
       attr(reinterpret_cast<const void*>(dev::ema_rt_root<false>));
       dev::ema_rt_root<false><<<grid, rwarps * 32, e.rt_smem, stream_>>>(
-          A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
+          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_split, e.rt_pairs, n_, rout, d_root_acc, d_tile_tot_);
     }
     return;
   }
@@ -1768,12 +1795,12 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
     dev::ema_rt_blocked<<<grid, dev::kRtBlockedThreads, e.rt_smem, stream_>>>(
-        A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
+        A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
         static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, out);
   } else {
     attr(reinterpret_cast<const void*>(dev::ema_rt_node<false>));
     dev::ema_rt_node<false><<<grid, warps * 32, e.rt_smem, stream_>>>(
-        A, e.Wa, e.d_amap_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);
+        A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);
   }
 }
 
@@ -1908,7 +1935,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
       if (prof_) { prof_->spmm.emplace_back(p0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       P = table_ptr(e.pp_off);
     }
-    if (e.skip_ema) {
+    if (e.skip_ema || e.virt) {
       if (stats) { m.t1 = mark(); m.t2 = mark(); }
       marks.push_back(m);
       continue;
@@ -2216,6 +2243,7 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
       t.spmm_gathered_bytes += count * walked * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
                                                         dev::last_panel_width(gc));
     }
+    if (e.virt || e.skip_ema) continue;  // no eMA executed: no eMA work claimed
     t.ema_launches += count;
     t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));
     t.ema_flops += count * 2 * n * e.Cs * static_cast<double>(B(e.size, e.sa));

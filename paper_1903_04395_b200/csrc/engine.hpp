@@ -101,6 +101,9 @@ struct NodeExec {
   int32_t* d_emap = nullptr;      // [k][Cps] P' storage column -> output column (RS slot / packed q), or -1
   int32_t* d_amap = nullptr;      // packed RR output: [k][Ws] q -> RR column (for its consumer's staging)
   std::vector<int32_t> amap_host;
+  int32_t Ca_in = 0;              // storage columns of the active input (Wa, or the virtual child's P' width)
+  bool virt = false;              // active-leaf node read only as an active child: its table IS its P',
+                                  // staged by the parent through this node's d_pmap (no eMA launch)
   const int32_t* d_amap_in = nullptr;  // this node's ACTIVE input is packed: stage it through this map  // vertices per pass, their smem row strides
   int dup_of = -1;                // exec index of an identical earlier node (table aliased)
   int pp_dup_of = -1;             // exec index of an earlier node with the same P' (SpMM skipped)

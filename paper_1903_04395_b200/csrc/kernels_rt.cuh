@@ -197,7 +197,7 @@ __device__ __forceinline__ void rt_write8(float* __restrict__ out, int Ws, int C
 // computes chunks of 8 output columns for the tile's 32 vertices.
 template <bool ALEAF>
 __global__ void __launch_bounds__(kEmaWarps * 32)
-ema_rt_node(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, const float* __restrict__ Pm, int Cpt,
+ema_rt_node(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
             const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
             const int4* __restrict__ tiles, const uint32_t* __restrict__ packed, int pairs, int Ws,
             const int32_t* __restrict__ omap, const int32_t* __restrict__ imap, int Cout, int32_t n,
@@ -212,7 +212,7 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ am
   __syncthreads();
   float* sA = smem;
   float* sP = smem + (ALEAF ? 0 : Wa * kSpitch);
-  if (!ALEAF) stage_rows<1>(Am, Wa, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Wa : nullptr);
+  if (!ALEAF) stage_rows<1>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr);
   stage_rows<1>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
   __syncthreads();
   const int64_t v = vids[lane];
@@ -327,7 +327,7 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
 
 constexpr int kRtBlockedThreads = 384;  // 2 CTAs x 12 warps per SM (80 registers, 2 x 87 KB smem at k=12)
 __global__ void __launch_bounds__(kRtBlockedThreads, 2)
-ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, const float* __restrict__ Pm, int Cpt,
+ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
                const int4* __restrict__ tiles, const GroupDesc* __restrict__ groups, int ngroups,
                const BlockDesc* __restrict__ blocks, int Ws, const int32_t* __restrict__ omap, int Cout,
@@ -344,7 +344,7 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__
   __syncthreads();
   float* sA = smem;
   float* sP = smem + Wa * kSpitch;
-  stage_rows<8>(Am, Wa, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Wa : nullptr);
+  stage_rows<8>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr);
   stage_rows<8>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
   __syncthreads();
   const int64_t v = vids[lane];
@@ -389,7 +389,7 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__
 // root_out[v]; fixed-order per-tile totals (0 for unused tiles).
 template <bool ALEAF>
 __global__ void __launch_bounds__(kEmaWarps * 32)
-ema_rt_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, const float* __restrict__ Pm, int Cpt,
+ema_rt_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
             const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
             const int4* __restrict__ tiles, const int2* __restrict__ split, int pairs, int32_t n,
             double* __restrict__ root_out, double* __restrict__ root_acc, double* __restrict__ tile_tot) {
@@ -407,7 +407,7 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ am
   __syncthreads();
   float* sA = smem;
   float* sP = smem + (ALEAF ? 0 : Wa * kSpitch);
-  if (!ALEAF) stage_rows<1>(Am, Wa, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Wa : nullptr);
+  if (!ALEAF) stage_rows<1>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr);
   stage_rows<1>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
   __syncthreads();
   double acc = 0;
@@ -564,7 +564,7 @@ __device__ __forceinline__ void micro_block_h(const float* __restrict__ sa, cons
 // run's first block)}, one dispatch per run.
 template <int H>
 __global__ void __launch_bounds__(256, 2)
-ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, const float* __restrict__ Pm, int Cpt,
+ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                 const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
                 const GroupDesc* __restrict__ groups, int ngroups, const uint2* __restrict__ blocks, int Ws,
                 const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out, int V, int sa,
@@ -580,7 +580,7 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
     __syncthreads();
     if (threadIdx.x == 0) next_task = blockDim.x >> 5;
     for (int j = 0; j < V && v0 + j < n; ++j) {
-      if (amap) stage_row_pmap(Am, Wa, n, v0 + j, smem + j * sa, amap + static_cast<int64_t>(colors[v0 + j]) * Wa);
+      if (amap) stage_row_pmap(Am, Ca, n, v0 + j, smem + j * sa, amap + static_cast<int64_t>(colors[v0 + j]) * Ca);
       else stage_row(Am, Wa, n, v0 + j, smem + j * sa);
       stage_row_pmap(Pm, Cpt, n, v0 + j, sP0 + j * sp, pmap + static_cast<int64_t>(colors[v0 + j]) * Cpt);
     }
@@ -625,7 +625,7 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
 // Root, one vertex per CTA: fp64 dot product over the relabeled split pairs,
 // fixed-order block reduction -> root_out[v] (root_reduce then sums root_out).
 __global__ void __launch_bounds__(256)
-ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, const float* __restrict__ Pm, int Cpt,
+ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
              const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors, const int2* __restrict__ split,
              int pairs, int32_t n, double* __restrict__ root_out, double* __restrict__ root_acc) {
   extern __shared__ float smem[];
@@ -635,7 +635,7 @@ ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ a
   for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
     const int c = colors[v];
     __syncthreads();
-    if (amap) stage_row_pmap(Am, Wa, n, v, sA, amap + static_cast<int64_t>(c) * Wa);
+    if (amap) stage_row_pmap(Am, Ca, n, v, sA, amap + static_cast<int64_t>(c) * Ca);
     else stage_row(Am, Wa, n, v, sA);
     stage_row_pmap(Pm, Cpt, n, v, sP, pmap + static_cast<int64_t>(c) * Cpt);
     __syncthreads();
