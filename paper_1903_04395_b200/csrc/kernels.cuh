@@ -476,7 +476,7 @@ __device__ __forceinline__ void warp_exclusive_scan(int* cnt, int nkeys, int lan
 // passes cost one round of loads.  Longer rows: bucket_long.
 constexpr int kBucketCache = 16;
 constexpr int kBucketLong = 1024;  // rows above this go to bucket_long (CTA per row)
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(256, 4)  // 64 registers: 4 CTAs per SM (the row loads are latency-bound)
 bucket_rows(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
             const uint8_t* __restrict__ colors, const uint8_t* __restrict__ rowc, const int32_t* __restrict__ row_order,
             int32_t row0, int32_t n, int k, int nparts, uint32_t* __restrict__ out, int64_t* __restrict__ cuts,
