@@ -1240,7 +1240,8 @@ void Engine::plan_arena_once(bool allow_stream) {
       if (y.dup_of >= 0) aliased[exec_[y.dup_of].id] = 1;
     }
     for (auto& e : exec_)
-      e.virt = virt_mode && !keep && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.dup_of < 0 &&
+      // (a plan that streams active-leaf SpMMs to fit the device keeps streaming them)
+      e.virt = virt_mode && !keep && !allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.dup_of < 0 &&
                !aliased[e.id] && active_uses[e.id] == 1 && !feeds_pair[e.id] && !e.skip_ema && !e.lspmm;
   }
   for (auto& e : exec_) {

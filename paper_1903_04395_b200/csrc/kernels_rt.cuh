@@ -325,7 +325,7 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
     }                                                                                       \
     break;
 
-constexpr int kRtBlockedThreads = 384;  // 2 CTAs x 12 warps per SM (80 registers, 2 x 87 KB smem at k=12)
+constexpr int kRtBlockedThreads = 512;  // 2 CTAs x 16 warps per SM (64 registers, 2 x 87 KB smem at k=12)
 __global__ void __launch_bounds__(kRtBlockedThreads, 2)
 ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
