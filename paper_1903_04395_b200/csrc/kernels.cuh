@@ -1219,6 +1219,15 @@ __host__ __device__ constexpr int cbin(int a, int b) {
   for (int i = 1; i <= b; ++i) r = r * (a - b + i) / i;
   return r;
 }
+// C(H, s) for a runtime s: H + 1 selects of compile-time constants (no
+// integer division in the epilogues)
+template <int H>
+__device__ __forceinline__ int cbin_rt(int s) {
+  int r = 0;
+#pragma unroll
+  for (int t = 0; t <= H; ++t) r = s == t ? cbin(H, t) : r;
+  return r;
+}
 __host__ __device__ constexpr int cpop(unsigned m) {
   int c = 0;
   for (; m; m &= m - 1) ++c;
@@ -1319,7 +1328,7 @@ ema_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
       }
     }
     if (v < n) {
-      const int cnt = cbin(kH1, gd.s1);
+      const int cnt = cbin_rt<kH1>(gd.s1);
 #pragma unroll
       for (int x = 0; x < kMaxAcc; ++x)
         if (x < cnt) out[panel_offset(Cs, n, v, gd.out_off + x)] = acc[x];
@@ -1426,7 +1435,7 @@ ema_vtx_blocked(const float* __restrict__ Am, const float* __restrict__ Pm,
           default: break;
         }
       }
-      const int cnt = cbin(kH1, gd.s1);
+      const int cnt = cbin_rt<kH1>(gd.s1);
 #pragma unroll
       for (int x = 0; x < kMaxAcc; ++x)
         if (x < cnt) out[panel_offset(Cs, n, v, gd.out_off + x)] = acc[x];

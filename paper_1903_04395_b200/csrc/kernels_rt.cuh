@@ -370,7 +370,7 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__
       b += len;
     }
     if (v >= 0) {
-      const int cnt = cbin(kH1, gd.s1);
+      const int cnt = cbin_rt<kH1>(gd.s1);
 #pragma unroll
       for (int x = 0; x < kMaxAcc; ++x)
         if (x < cnt) {
@@ -606,7 +606,7 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
           b += len;
         }
         const int32_t* om = omap ? omap + static_cast<int64_t>(colors[v]) * Ws : nullptr;
-        const int cnt = cbin(H, gd.s1);
+        const int cnt = cbin_rt<H>(gd.s1);
 #pragma unroll
         for (int x = 0; x < kAcc; ++x)
           if (x < cnt) {
