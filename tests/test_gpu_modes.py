@@ -14,7 +14,8 @@ child process):
 * TCG_ROOTED_PARTS=1 with TCG_PART_KB=16 -- the rooted SpMM split into
   colour-class parts (P' accumulated across parts);
 * TCG_PAIR=0 -- no pair layout (every rooted SpMM over the k-color slot
-  layout); TCG_PAIR=2 -- the pair layout for every node whose copies fit.
+  layout); TCG_PAIR=2 -- the pair layout for every node whose copies fit;
+* TCG_VIRT=0 -- every active-leaf table materialized (no virtual tables).
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -76,9 +77,9 @@ print("OK")
 
 @pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"},
                                  {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"},
-                                 {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}],
+                                 {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}, {"TCG_VIRT": "0"}],
                          ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
-                              "rooted_parts", "pair_off", "pair_all"])
+                              "rooted_parts", "pair_off", "pair_all", "virt_off"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,

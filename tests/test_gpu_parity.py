@@ -283,6 +283,36 @@ def test_given_coloring_matches_seeded(cfg1_golden):
     assert a == b == float(gold["totals_seeds1_10"][3])
 
 
+def test_set_graph_buffer_reuse():
+    """One context, a sequence of host-CSR graphs that grow, shrink and grow
+    again (device graph buffers, the device-built schedules, the arena and the
+    estimate buffers are reused when they fit): every result equals the oracle."""
+    parents = [-1, 0, 1, 2, 0, 4, 4, 6, 0, 8]
+    k = len(parents)
+    plan = O.partition(k, parents_to_edges(parents), 0)
+    t = T.template_from_parents(parents, 0)
+    c = T.Context(0)
+    c.set_template(t)
+    rng = np.random.default_rng(11)
+    for i, (scale, ef) in enumerate([(9, 16), (12, 48), (8, 8), (12, 24), (11, 64)]):
+        g = T.generate_rmat(T.RmatSpec(scale, ef << scale, .45, .15, .15, .25, 1 + i))
+        rp = np.ascontiguousarray(g.csc_col_ptr, np.int64)
+        cl = np.ascontiguousarray(g.csc_rows, np.int32)
+        c.set_graph_csr(g.n, rp, cl)
+        seed = int(rng.integers(1, 1 << 30))
+        totals, est, se, pv = c.estimate(seed, 2, per_vertex=True)
+        want = []
+        opv = np.zeros(g.n)
+        for j in range(2):
+            colors = O.random_coloring(g.n, k, seed + j)
+            tot, vv, _ = O.run_iteration(g.n, g.csc_col_ptr, g.csc_rows, plan, colors)
+            want.append(tot)
+            opv += vv
+        assert rel_err(totals, want) <= REL, (i, totals, want)
+        scale_f = est / np.mean(totals) if np.mean(totals) else 1.0
+        assert_close(pv, opv / 2 * scale_f)
+
+
 # ------------------------------------------------------------ full-size cases
 def _load(name):
     p = os.path.join(GOLDEN, f"{name}.npz")
