@@ -262,7 +262,7 @@ def run_b200(args, rank, world, local, dist):
         ectx = T.Context(device=local)
         ectx.set_template(t)
         ectx.set_graph_csr(g.n, rp, cl)
-        ectx.estimate(1, 1)                                       # warm (allocations)
+        ectx.estimate(1, ncol, per_vertex=True)                   # warm (allocations; not timed)
         barrier(dist, local)
         e_steps = max(1, min(args.steps, 3))
         t0 = time.perf_counter()
