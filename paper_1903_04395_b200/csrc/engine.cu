@@ -1799,6 +1799,21 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
         A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
         static_cast<const dev::BlockDesc*>(e.d_rt_blocks), e.Ws, e.d_omap, e.Cout, n_, out);
   } else {
+    // narrow nodes: one warp per tile (8 tiles per CTA in flight) when a
+    // warp's slice of A, P (and the staged RS output) is small
+    static const int warp_mode = [] {
+      const char* s = std::getenv("TCG_RT_WARP");
+      return s ? std::atoi(s) : 1;
+    }();
+    const int slice = (e.Wa + e.Wp + (e.d_imap ? e.Ws : 0)) * dev::kSpitch;
+    const size_t wsmem = static_cast<size_t>(8) * slice * 4;
+    if (warp_mode && wsmem <= (100u << 10)) {
+      TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_node_w, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsmem)));
+      dev::ema_rt_node_w<<<static_cast<unsigned>((max_tiles_ + 7) / 8), 256, wsmem, stream_>>>(
+          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_, e.d_rt_packed, e.rt_pairs, e.Ws,
+          e.d_omap, e.d_imap, e.Cout, n_, slice, out);
+      return;
+    }
     attr(reinterpret_cast<const void*>(dev::ema_rt_node<false>));
     dev::ema_rt_node<false><<<grid, warps * 32, e.rt_smem, stream_>>>(
         A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, e.d_rt_packed, e.rt_pairs, e.Ws, e.d_omap, e.d_imap, e.Cout, n_, out);

@@ -131,18 +131,19 @@ vsort_scatter(const uint8_t* __restrict__ colors, int32_t n, int k, const int* _
 template <int kStageU>
 __device__ __forceinline__ void stage_rows(const float* __restrict__ T, int C, int32_t n,
                                            const int32_t* __restrict__ vids, float* dst,
-                                           const int32_t* __restrict__ map) {
+                                           const int32_t* __restrict__ map, int tid = threadIdx.x,
+                                           int nth = blockDim.x) {
   const int panels = num_panels(C);
   const int zl = last_panel_width(C);
   const int full4 = (panels - 1) * kTileV * (kZ / 4);
   const int total4 = full4 + kTileV * (zl / 4);
   const int lq_last = zl == 32 ? 3 : (zl == 16 ? 2 : 1);  // log2(float4s per row) of the last panel
-  for (int base = threadIdx.x; base < total4; base += blockDim.x * kStageU) {
+  for (int base = tid; base < total4; base += nth * kStageU) {
     float4 x[kStageU];
     int c0[kStageU], vv[kStageU];
 #pragma unroll
     for (int u = 0; u < kStageU; ++u) {
-      const int f = base + u * blockDim.x;
+      const int f = base + u * nth;
       int p, r, lq;
       if (f < full4) { p = f >> 8; r = f & 255; lq = 3; }  // kTileV * 8 float4s per full panel tile
       else { p = panels - 1; r = f - full4; lq = lq_last; }
@@ -308,6 +309,82 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
         const int col = p * kZ + t;
         const int src = col < Cout ? __ldg(cm + col) : -1;
         out[static_cast<int64_t>(p) * n * kZ + u * zp + t] = src >= 0 ? crow[r * rf + src] : 0.f;
+      }
+    }
+  }
+}
+
+// ema_rt_node with one WARP per tile (narrow nodes): every warp stages its
+// own tile's rows into its smem slice and computes all of the tile's output
+// chunks, so 8 tiles per CTA (and 2-4 CTAs per SM) are in flight instead of
+// one -- the narrow nodes are latency-bound on the staging round trips.
+// Slice layout: A [Wa][kSpitch], P [Wp][kSpitch], RS output tile [Ws][kSpitch].
+__global__ void __launch_bounds__(256)
+ema_rt_node_w(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm,
+              int Cpt, const int32_t* __restrict__ pmap, int Wp, const int32_t* __restrict__ vsorted,
+              const int4* __restrict__ tiles, int ntiles, const uint32_t* __restrict__ packed, int pairs, int Ws,
+              const int32_t* __restrict__ omap, const int32_t* __restrict__ imap, int Cout, int32_t n, int slice,
+              float* __restrict__ out) {
+  extern __shared__ float smem[];
+  __shared__ int32_t vids_all[8][32];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int t = blockIdx.x * (blockDim.x >> 5) + warp;
+  if (t >= ntiles) return;
+  const int4 tile = tiles[t];
+  if (tile.x < 0) return;
+  const int c = tile.x;
+  int32_t* vids = vids_all[warp];
+  vids[lane] = lane < tile.z ? vsorted[tile.y + lane] : -1;
+  __syncwarp();
+  float* sA = smem + static_cast<int64_t>(warp) * slice;
+  float* sP = sA + Wa * kSpitch;
+  float* sO = sP + Wp * kSpitch;
+  stage_rows<4>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr, lane, 32);
+  stage_rows<4>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt, lane, 32);
+  __syncwarp();
+  const int64_t v = vids[lane];
+  const int32_t* om = omap ? omap + static_cast<int64_t>(c) * Ws : nullptr;
+  const int nchunks = (Ws + 7) / 8;
+  for (int q = 0; q < nchunks; ++q) {
+    float r[8];
+    const int nv = min(8, Ws - q * 8);
+    const uint32_t* sp = packed + static_cast<int64_t>(q) * 8 * pairs;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = 0.f;
+    for (int pb = 0; pb < pairs; pb += 32) {
+      uint32_t w[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) w[j] = (j < nv && pb + lane < pairs) ? __ldg(sp + j * pairs + pb + lane) : 0u;
+      const int cnt = min(32, pairs - pb);
+      for (int pp = 0; pp < cnt; ++pp) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const uint32_t s = __shfl_sync(0xffffffffu, w[j], pp);
+          r[j] = fmaf(sA[(s & 0xFFFFu) * kSpitch + lane], sP[(s >> 16) * kSpitch + lane], r[j]);
+        }
+      }
+    }
+    if (om && imap) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (q * 8 + j < Ws) sO[(q * 8 + j) * kSpitch + lane] = r[j];
+    } else if (v >= 0) {
+      rt_write8(out, Ws, Cout, om, n, v, q * 8, r);
+    }
+  }
+  if (om && imap) {
+    __syncwarp();
+    const int32_t* im = imap + static_cast<int64_t>(c) * Cout;
+    const int pout = num_panels(Cout), zout = last_panel_width(Cout);
+    for (int rr = 0; rr < 32; ++rr) {
+      const int64_t u = vids[rr];
+      if (u < 0) continue;
+      for (int p = 0; p < pout; ++p) {
+        const int zp = p == pout - 1 ? zout : kZ;
+        if (lane < zp) {
+          const int j = p * kZ + lane < Cout ? __ldg(im + p * kZ + lane) : -1;
+          out[static_cast<int64_t>(p) * n * kZ + u * zp + lane] = j >= 0 ? sO[j * kSpitch + rr] : 0.f;
+        }
       }
     }
   }

@@ -1,0 +1,5 @@
+set -x
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_modes.py -x -q 2>&1 | tail -2
+timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 --stats 2>&1 | head -12
+TCG_RT_WARP=0 timeout 300 python tools/prof_driver.py --config cfg3 --colorings 3 2>&1 | head -1
+timeout 300 python tools/prof_driver.py --config cfg2 --colorings 5 2>&1 | tail -1
