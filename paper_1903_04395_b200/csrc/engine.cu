@@ -298,6 +298,7 @@ void Engine::release_template() {
     dfree(e.d_slot_col);
     dfree(e.d_pinv);
     dfree(e.d_xmap);
+    dfree(e.d_xmap_v);
     dfree(e.d_pmap);
     dfree(e.d_cmap);
     dfree(e.d_imap);
@@ -956,6 +957,7 @@ void Engine::setup_rooted_ema(int max_smem) {
       }
     dfree(e.d_xmap);
     e.d_xmap = dupload(xm, stream_);
+    e.xmap_host = std::move(xm);
   }
   std::vector<int> parent(plan_.num_nodes, -1);
   for (size_t i = 0; i < exec_.size(); ++i) {
@@ -1033,6 +1035,7 @@ void Engine::setup_rooted_ema(int max_smem) {
           if (i >= 0) cm[static_cast<size_t>(c) * e.Cout + i] = src;
         }
       e.d_cmap = dupload(cm, stream_);
+      e.cmap_host = cm;
       if (!e.p_leaf && !e.pair) {
         // streamed SpMM epilogue (pstream_copy): P' storage column -> output
         // column.  RS outputs: the slot.  RR outputs are stored PACKED in P'
@@ -1130,6 +1133,25 @@ void Engine::setup_rooted_ema(int max_smem) {
       e.rt_smem += out_tile;
     else
       dfree(e.d_imap);  // scattered RS writes instead
+  }
+  // pair SpMMs over an active-leaf passive child: the composed map lets the
+  // expansion read the child's P' directly (plan_arena_once decides virt_px)
+  for (auto& par : exec_) {
+    dfree(par.d_xmap_v);
+    if (!par.pair) continue;
+    const NodeExec* ch = nullptr;
+    for (const auto& x : exec_)
+      if (x.id == par.p) ch = &x;
+    if (!ch || !ch->a_leaf || ch->root || !ch->rooted || ch->p_leaf || ch->cmap_host.empty() || !ch->omap.empty()) continue;
+    std::vector<int16_t> xv(par.xmap_host.size(), -1);
+    const int slots = par.rl_groups * par.rl_zw;
+    for (int cu = 0; cu < k; ++cu)
+      for (size_t i = 0; i < static_cast<size_t>(k) * slots; ++i) {
+        const size_t at = static_cast<size_t>(cu) * k * slots + i;
+        const int16_t j = par.xmap_host[at];
+        if (j >= 0) xv[at] = static_cast<int16_t>(ch->cmap_host[static_cast<size_t>(cu) * ch->Cout + j]);
+      }
+    par.d_xmap_v = dupload(xv, stream_);
   }
   rooted_ema_ = true;
 }
@@ -1239,10 +1261,18 @@ void Engine::plan_arena_once(bool allow_stream) {
       if (y.dup_of < 0 && !y.a_leaf) ++active_uses[y.a];
       if (y.dup_of >= 0) aliased[exec_[y.dup_of].id] = 1;
     }
-    for (auto& e : exec_)
+    std::vector<char> pair_virt_ok(plan_.num_nodes, 0);  // a pair parent has the composed map
+    for (const auto& y : exec_)
+      if (y.pair && y.d_xmap_v && y.dup_of < 0) pair_virt_ok[y.p] = 1;
+    for (auto& e : exec_) {
       // (a plan that streams active-leaf SpMMs to fit the device keeps streaming them)
-      e.virt = virt_mode && !keep && !allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted && !e.p_leaf && e.dup_of < 0 &&
-               !aliased[e.id] && active_uses[e.id] == 1 && !feeds_pair[e.id] && !e.skip_ema && !e.lspmm;
+      const bool base = virt_mode && !keep && !allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted &&
+                        !e.p_leaf && e.dup_of < 0 && !aliased[e.id] && !e.skip_ema && !e.lspmm;
+      // read only as an active child (staged through its P' map), or only by a
+      // pair expansion (through the composed map)
+      e.virt_px = base && feeds_pair[e.id] && pair_virt_ok[e.id] && active_uses[e.id] == 0;
+      e.virt = (base && active_uses[e.id] == 1 && !feeds_pair[e.id]) || e.virt_px;
+    }
   }
   for (auto& e : exec_) {
     if (e.dup_of >= 0) {  // alias the first occurrence; release this node's own children
@@ -1618,10 +1648,16 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
   if (e.pair) {
     if (sharded()) throw logic_error("pair-layout SpMM on a sharded context");
     float* cp = table_ptr(e.ct_off);
-    const size_t smem = static_cast<size_t>(4) * 32 * (e.Wx + 1);
+    // a virtual active-leaf child: its P' (storage columns) through the composed map
+    const NodeExec* ch = nullptr;
+    for (const auto& x : exec_)
+      if (x.id == e.p) ch = &x;
+    const bool vpx = ch && ch->virt_px;
+    const int wx = vpx ? ch->Cpt : e.Wx;
+    const size_t smem = static_cast<size_t>(4) * 32 * (wx + 1);
     TCG_CUDA(cudaFuncSetAttribute(dev::pair_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    dev::pair_expand<<<static_cast<unsigned>((n_ + 31) / 32), 256, smem, stream_>>>(M, e.Wx, d_colors, e.d_xmap, plan_.k, G, zw,
-                                                                                      n_, cp);
+    dev::pair_expand<<<static_cast<unsigned>((n_ + 31) / 32), 256, smem, stream_>>>(M, wx, d_colors, vpx ? e.d_xmap_v : e.d_xmap,
+                                                                                      plan_.k, G, zw, n_, cp);
     ++launches_;
     X = cp;
     xstride = static_cast<int64_t>(G) * n_ * zw;

@@ -71,6 +71,13 @@ struct NodeExec {
   RootedLayout pr;                // the (k-1)-color layout (candidates)
   int32_t Wx = 0;                 // RR columns of the passive table, C(k-1, sp-1)
   int16_t* d_xmap = nullptr;      // [k][k][groups * zw] copy slot -> RR column, or -1
+  std::vector<int16_t> xmap_host;
+  // the passive child is an active-leaf node whose table is never written
+  // (virt_px): the expansion reads the child's P' through xmap composed with
+  // the child's output map (copy slot -> P' storage column)
+  int16_t* d_xmap_v = nullptr;
+  std::vector<int32_t> cmap_host; // active leaf: [k][Cout] output column -> P' storage column
+  bool virt_px = false;
   // rooted eMA (kernels_rt.cuh): same-color vertex tiles of the (k-1)-color
   // problem (s-1, a-1, p); tables stored rooted (RR) or in the parent SpMM's
   // slot layout (RS, passive children)
