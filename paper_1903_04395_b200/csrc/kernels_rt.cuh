@@ -484,8 +484,8 @@ ema_rt_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ am
   __syncthreads();
   float* sA = smem;
   float* sP = smem + (ALEAF ? 0 : Wa * kSpitch);
-  if (!ALEAF) stage_rows<1>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr);
-  stage_rows<1>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
+  if (!ALEAF) stage_rows<4>(Am, Ca, n, vids, sA, amap ? amap + static_cast<int64_t>(c) * Ca : nullptr);
+  stage_rows<4>(Pm, Cpt, n, vids, sP, pmap + static_cast<int64_t>(c) * Cpt);
   __syncthreads();
   double acc = 0;
   if (ALEAF) {
