@@ -82,11 +82,27 @@ __device__ __forceinline__ void st_stream_f4(float* p, float4 v, uint64_t pol) {
 // draw, or forced by the test hook) takes an exact block-scan path.
 constexpr int kMtThreads = 160;
 
+// Two generations per barrier: thread t also produces word t of generation
+// g+1 from its own word t of g and word t+1 of g-1; only word 155 needs a
+// word of g it does not own (word 0), which thread 155 recomputes from g-1
+// and g-2.  Four ring slots: a round reads one pair, writes the other.
+__device__ __forceinline__ uint64_t mt_twist(uint64_t c, uint64_t a, uint64_t b) {
+  constexpr uint64_t U = 0xFFFFFFFF80000000ULL, L = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
+  const uint64_t y = (a & U) | (b & L);
+  return c ^ (y >> 1) ^ ((y & 1) ? A : 0);
+}
+__device__ __forceinline__ uint64_t mt_temper(uint64_t z) {
+  z ^= (z >> 29) & 0x5555555555555555ULL;
+  z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
+  z ^= (z << 37) & 0xFFF7EEE000000000ULL;
+  return z ^ (z >> 43);
+}
+
 __global__ void __launch_bounds__(kMtThreads)
 mt_coloring(const uint64_t* __restrict__ seeds, int32_t n, int k, uint64_t limit, uint64_t magic,
             uint8_t* __restrict__ out, int64_t out_stride) {
-  __shared__ uint64_t ring[3][156];
-  __shared__ int wcnt[kMtThreads / 32];
+  __shared__ uint64_t ring[4][156];
+  __shared__ int wcnt[2][kMtThreads / 32];
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
   uint8_t* colors = out + blockIdx.x * out_stride;
   if (k == 1) {  // count_table.hpp:97: no draws
@@ -102,46 +118,56 @@ mt_coloring(const uint64_t* __restrict__ seeds, int32_t n, int k, uint64_t limit
     }
   }
   __syncthreads();
-  constexpr uint64_t U = 0xFFFFFFFF80000000ULL, L = 0x7FFFFFFFULL, A = 0xB5026F5AA96619E9ULL;
   const bool act = t < 156;
   const uint64_t kk = static_cast<uint64_t>(k);
-  int64_t base = 0;
-  for (int g = 2; base < n; ++g) {
-    const int s2 = g % 3, s1 = (g + 2) % 3, s0 = (g + 1) % 3;  // slots of g, g-1, g-2
-    uint64_t z = 0;
-    if (act) {
-      const uint64_t a = ring[s0][t];
-      const uint64_t b = t < 155 ? ring[s0][t + 1] : ring[s1][0];
-      const uint64_t c = ring[s1][t];
-      const uint64_t y = (a & U) | (b & L);
-      const uint64_t w = c ^ (y >> 1) ^ ((y & 1) ? A : 0);
-      ring[s2][t] = w;
-      z = w;
-      z ^= (z >> 29) & 0x5555555555555555ULL;
-      z ^= (z << 17) & 0x71D67FFFEDA60000ULL;
-      z ^= (z << 37) & 0xFFF7EEE000000000ULL;
-      z ^= (z >> 43);
-    }
-    const bool rej = act && z >= limit;
-    uint64_t q = __umul64hi(z, magic);
+  auto reduce = [&](uint64_t z) {
+    const uint64_t q = __umul64hi(z, magic);
     uint64_t r = z - q * kk;
     if (r >= kk) r -= kk;
-    if (!__syncthreads_or(rej)) {
-      const int64_t v = base + t;
-      if (act && v < n) colors[v] = static_cast<uint8_t>(r);
-      base += 156;
-    } else {
-      const unsigned bal = __ballot_sync(0xffffffffu, rej);
-      if (lane == 0) wcnt[warp] = __popc(bal);
-      __syncthreads();
-      int pre = __popc(bal & ((1u << lane) - 1u)), tot = 0;
-      for (int w = 0; w < kMtThreads / 32; ++w) {
-        if (w < warp) pre += wcnt[w];
-        tot += wcnt[w];
+    return static_cast<uint8_t>(r);
+  };
+  int64_t base = 0;
+  for (int rd = 0; base < n; ++rd) {
+    const uint64_t* P2 = ring[(rd & 1) * 2];      // generation g-2
+    const uint64_t* P1 = ring[(rd & 1) * 2 + 1];  // generation g-1
+    uint64_t* O0 = ring[((rd + 1) & 1) * 2];      // g
+    uint64_t* O1 = ring[((rd + 1) & 1) * 2 + 1];  // g+1
+    uint64_t z0 = 0, z1 = 0;
+    if (act) {
+      const uint64_t w0 = mt_twist(P1[t], P2[t], t < 155 ? P2[t + 1] : P1[0]);
+      const uint64_t g0w0 = t < 155 ? 0 : mt_twist(P1[0], P2[0], P2[1]);  // word 0 of g (thread 155)
+      const uint64_t w1 = mt_twist(w0, P1[t], t < 155 ? P1[t + 1] : g0w0);
+      O0[t] = w0;
+      O1[t] = w1;
+      z0 = mt_temper(w0);
+      z1 = mt_temper(w1);
+    }
+    const bool rej0 = act && z0 >= limit, rej1 = act && z1 >= limit;
+    const uint8_t c0 = reduce(z0), c1 = reduce(z1);
+    if (!__syncthreads_or(rej0 || rej1)) {
+      if (act) {
+        if (base + t < n) colors[base + t] = c0;
+        if (base + 156 + t < n) colors[base + 156 + t] = c1;
       }
-      const int64_t v = base + t - pre;
-      if (act && !rej && v < n) colors[v] = static_cast<uint8_t>(r);
-      base += 156 - tot;
+      base += 312;
+    } else {  // exact compaction of the accepted words of both generations, in order
+      const unsigned b0 = __ballot_sync(0xffffffffu, rej0), b1 = __ballot_sync(0xffffffffu, rej1);
+      if (lane == 0) {
+        wcnt[0][warp] = __popc(b0);
+        wcnt[1][warp] = __popc(b1);
+      }
+      __syncthreads();
+      int pre0 = __popc(b0 & ((1u << lane) - 1u)), pre1 = __popc(b1 & ((1u << lane) - 1u)), tot0 = 0, tot1 = 0;
+      for (int w = 0; w < kMtThreads / 32; ++w) {
+        if (w < warp) { pre0 += wcnt[0][w]; pre1 += wcnt[1][w]; }
+        tot0 += wcnt[0][w];
+        tot1 += wcnt[1][w];
+      }
+      const int64_t v0 = base + t - pre0;
+      const int64_t v1 = base + (156 - tot0) + t - pre1;
+      if (act && !rej0 && v0 < n) colors[v0] = c0;
+      if (act && !rej1 && v1 < n) colors[v1] = c1;
+      base += 312 - tot0 - tot1;
       __syncthreads();
     }
   }
