@@ -1822,7 +1822,8 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   const int warps = std::max(2, std::min(dev::kEmaWarps, (e.Ws + 7) / 8));
   if (e.a_leaf) {
     const int rf = static_cast<int>(dev::table_floats(e.Cpt, 1));
-    const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (48 << 10) / (4 * rf))));
+    // (narrow rows: up to 128 vertices per CTA, so a CTA moves >= 16 KB)
+    const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(128, (48 << 10) / (4 * rf))));
     const size_t smem = static_cast<size_t>(vpb) * rf * 4;
     TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     int L = 1;  // lanes per row: enough for the row's float4s and the output panel's slots
