@@ -327,6 +327,14 @@ void Engine::set_shard(int rank, int world, std::unique_ptr<Transport> t) {
   rank_ = rank;
   world_ = world;
   tr_ = std::move(t);
+  if (have_template_) {  // layouts depend on sharding (no pair layout): re-plan the template
+    std::vector<int32_t> edges;
+    for (const auto& pr : tpl_.edges) {
+      edges.push_back(pr.first);
+      edges.push_back(pr.second);
+    }
+    set_template(tpl_.k, edges.data(), tpl_.root);
+  }
 }
 
 void Engine::set_graph(const Csr& gin) {

@@ -108,6 +108,22 @@ def test_sharded_world1_host():
     assert totals[0] == total
 
 
+@pytest.mark.gpu
+def test_shard_after_template_replans():
+    """set_template before set_shard_*: the template is re-planned for the
+    sharded context (no pair layout), so a pair-eligible k=12 template runs."""
+    g = T.generate_rmat(T.RmatSpec(11, 48 << 11, .45, .15, .15, .25, 3))
+    parents = CFG_TEMPLATES["cfg3"]
+    c = T.Context(0)
+    c.set_template(T.template_from_parents(parents, 0))
+    c.set_shard_host(0, 1, lambda a: a)
+    c.set_graph(g)
+    total, pv, _ = c.run_coloring(2, per_vertex=True)
+    ot, opv, _ = _ref(g, parents, 2)
+    assert abs(total - ot) <= 1e-4 * ot
+    assert np.max(np.abs(pv - opv) / np.maximum(opv, 1)) <= 1e-4
+
+
 def _worker(rank, world, port, name, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     import torch
