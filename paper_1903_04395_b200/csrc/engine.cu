@@ -161,7 +161,7 @@ void release_schedule(PartSchedule& s) {
 // length (descending), pad with no-op segments; rows longer than one segment
 // get fp64 partial slots (summed in order by spmm_fixup).
 PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<int64_t>& hi,
-                            bool keep_empty, cudaStream_t stream, bool by_len = true) {
+                            bool keep_empty, cudaStream_t stream) {
   const int32_t n = static_cast<int32_t>(lo.size());
   std::vector<dev::Seg> segs;
   segs.reserve(static_cast<size_t>(n) + 16);
@@ -185,10 +185,7 @@ PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<in
   const int64_t padded = std::max<int64_t>((static_cast<int64_t>(segs.size()) + dev::kSegPad - 1) /
                                                dev::kSegPad * dev::kSegPad, dev::kSegPad);
   std::vector<dev::Seg> sorted(static_cast<size_t>(padded), dev::Seg{0, 0, dev::kSkip});
-  if (by_len)
-    for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
-  else
-    std::copy(segs.begin(), segs.end(), sorted.begin());
+  for (auto& s : segs) sorted[pos[dev::kSegMax - s.len]++] = s;
   PartSchedule ps;
   ps.nseg_padded = padded;
   ps.d_segs = dupload(sorted, stream);
