@@ -305,6 +305,7 @@ void Engine::release_template() {
     dfree(e.d_rt_groups);
     dfree(e.d_rt_blocks);
     dfree(e.d_rtv_blocks);
+    dfree(e.d_rtv_drop);
     dfree(e.d_emap);
     dfree(e.d_amap);
   }
@@ -1115,6 +1116,29 @@ void Engine::setup_rooted_ema(int max_smem) {
         }
       }
     }
+    e.rtv_pleaf = false;
+    dfree(e.d_rtv_drop);
+    static const int pleaf_mode = [] {
+      const char* s = std::getenv("TCG_RTV_PLEAF");
+      return s ? std::atoi(s) : 1;
+    }();
+    if (e.rt_vtx && e.p_leaf && !e.root && !e.a_leaf && pleaf_mode && e.Wa < 65536) {
+      // out'[S'] = sum over d in S' of A'[S' minus d] * H[d]: the drop table
+      const int K = k - 1, sp1 = e.size - 1;
+      std::vector<uint32_t> dr(static_cast<size_t>(e.Ws) * sp1);
+      int t2[kMaxK];
+      for (int32_t j = 0; j < e.Ws; ++j) {
+        set_of(K, j, sp1, cs);
+        for (int i = 0; i < sp1; ++i) {
+          int m = 0;
+          for (int q = 0; q < sp1; ++q)
+            if (q != i) t2[m++] = cs[q];
+          dr[static_cast<size_t>(j) * sp1 + i] = static_cast<uint32_t>(index_of(t2, m)) | (static_cast<uint32_t>(cs[i]) << 16);
+        }
+      }
+      e.d_rtv_drop = dupload(dr, stream_);
+      e.rtv_pleaf = true;
+    }
     if (e.rt_vtx) {
       if (e.root) {
         e.rt_smem = static_cast<size_t>(4 * (row_floats(e.Wa) + e.Wp));
@@ -1791,6 +1815,19 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   auto attr = [&](const void* f) {
     TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_smem)));
   };
+  if (e.rtv_pleaf) {  // vertex-per-warp over a leaf passive child
+    const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
+    const int cst = e.omap.empty() ? e.Ws : e.Cout;
+    const int oslice = (cst + 31) / 32 * 32 + 1;
+    const size_t smem = static_cast<size_t>(dev::kPleafV) * (slice + oslice) * 4;
+    TCG_CUDA(cudaFuncSetAttribute(dev::ema_rtv_pleaf, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(
+        1, std::min<int64_t>((n_ + dev::kPleafV - 1) / dev::kPleafV, 148 * 16)));
+    dev::ema_rtv_pleaf<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_,
+                                                      e.d_rtv_drop, e.size - 1, e.Ws, e.d_omap, e.Cout, n_, slice,
+                                                      oslice, table_ptr(e.out_off));
+    return;
+  }
   if (e.rt_vtx) {
     const unsigned vgrid = static_cast<unsigned>(std::max<int64_t>(
         1, std::min<int64_t>((n_ + e.rtv_V - 1) / e.rtv_V, e.root ? 148 * 16 : 148 * 2 * 8)));

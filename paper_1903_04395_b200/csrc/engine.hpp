@@ -100,6 +100,8 @@ struct NodeExec {
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
   void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)
+  bool rtv_pleaf = false;         // vertex-per-warp eMA over a leaf passive child (ema_rtv_pleaf)
+  uint32_t* d_rtv_drop = nullptr; // [Ws][s-1] {A index of S' minus d | d << 16}
   // active-leaf node with an unshared rooted SpMM: P' is never materialized --
   // each group's columns go to an n x Ct scratch table and are scattered into
   // the output (RR or RS) right after the group's last part (pstream_copy)

@@ -390,6 +390,101 @@ ema_rt_node_w(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
   }
 }
 
+// Wide nodes over a LEAF passive child (p = 1) whose 32-vertex tile does not
+// fit (cfg4's (7,6,1)): out'[S'] = sum over d in S' of A'[S' minus d] *
+// H[v, d] (relabeled past c(v)) -- s' terms per output, so the register-blocked
+// micro-patterns of ema_rtv_blocked are all overhead here.  A CTA stages the A
+// rows and histograms of kPleafV vertices; a thread takes output columns and,
+// per drop-table entry {A index | d << 16} (s' per output, read once),
+// accumulates all kPleafV vertices into the vertices' output rows staged in
+// smem (storage order: RR columns, or the RS slots of the parent's SpMM),
+// which warps then write as whole 128 B panel rows.
+constexpr int kPleafV = 4;
+__global__ void __launch_bounds__(256)
+ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
+              const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap,
+              const uint8_t* __restrict__ colors, const uint32_t* __restrict__ drop, int sp, int Ws,
+              const int32_t* __restrict__ omap, int Cout, int32_t n, int slice, int oslice, float* __restrict__ out) {
+  extern __shared__ float smem[];
+  __shared__ int cvs[kPleafV];
+  float* sO = smem + kPleafV * slice;  // [kPleafV][oslice]: output rows in storage order
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const int pa = num_panels(Ca), za = last_panel_width(Ca);
+  const int tot4 = ((pa - 1) * kZ + za) / 4;
+  for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * kPleafV; v0 < n; v0 += static_cast<int64_t>(gridDim.x) * kPleafV) {
+    __syncthreads();
+    if (threadIdx.x < kPleafV) cvs[threadIdx.x] = v0 + threadIdx.x < n ? colors[v0 + threadIdx.x] : 0;
+    // warp w stages vertices w, w + nw, ...: its A row (through amap when the
+    // table is packed or virtual) and its relabeled histogram
+    for (int vv = warp; vv < kPleafV; vv += nw) {
+      const int64_t v = v0 + vv;
+      float* sA = smem + static_cast<int64_t>(vv) * slice;
+      float* sH = sA + slice - 32;
+      if (v >= n) {
+        for (int f = lane; f < slice; f += 32) sA[f] = 0.f;
+        continue;
+      }
+      const int c = colors[v];
+      const int32_t* am = amap ? amap + static_cast<int64_t>(c) * Ca : nullptr;
+      for (int f = lane; f < tot4; f += 32) {
+        const int c0 = f * 4, p = c0 / kZ, z4 = c0 % kZ;
+        const int zw = p == pa - 1 ? za : kZ;
+        const float4 x = __ldg(reinterpret_cast<const float4*>(Am + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
+        if (!am) {
+          if (c0 < Wa) sA[c0] = x.x;
+          if (c0 + 1 < Wa) sA[c0 + 1] = x.y;
+          if (c0 + 2 < Wa) sA[c0 + 2] = x.z;
+          if (c0 + 3 < Wa) sA[c0 + 3] = x.w;
+        } else {
+          const int m0 = c0 < Ca ? __ldg(am + c0) : -1, m1 = c0 + 1 < Ca ? __ldg(am + c0 + 1) : -1;
+          const int m2 = c0 + 2 < Ca ? __ldg(am + c0 + 2) : -1, m3 = c0 + 3 < Ca ? __ldg(am + c0 + 3) : -1;
+          if (m0 >= 0) sA[m0] = x.x;
+          if (m1 >= 0) sA[m1] = x.y;
+          if (m2 >= 0) sA[m2] = x.z;
+          if (m3 >= 0) sA[m3] = x.w;
+        }
+      }
+      if (lane < Cpt) {  // pmap: storage column -> d' (or -1 for c(v))
+        const int d = __ldg(pmap + static_cast<int64_t>(c) * Cpt + lane);
+        if (d >= 0) sH[d] = __ldg(Pm + v * panel_width(Cpt, 0) + lane);
+      }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < Ws; j += blockDim.x) {
+      float acc[kPleafV];
+#pragma unroll
+      for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = 0.f;
+      const uint32_t* dr = drop + static_cast<int64_t>(j) * sp;
+      for (int i = 0; i < sp; ++i) {
+        const uint32_t e = __ldg(dr + i);
+        const int ia = static_cast<int>(e & 0xFFFFu), ih = static_cast<int>(e >> 16) + slice - 32;
+#pragma unroll
+        for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], smem[vv * slice + ih], acc[vv]);
+      }
+#pragma unroll
+      for (int vv = 0; vv < kPleafV; ++vv) {
+        const int32_t* om = omap ? omap + static_cast<int64_t>(cvs[vv]) * Ws : nullptr;
+        const int slot = om ? __ldg(om + j) : j;
+        if (slot >= 0) sO[vv * oslice + slot] = acc[vv];
+      }
+    }
+    __syncthreads();
+    // whole panel rows: warp w writes (vertex, panel) rows w, w + nw, ...
+    const int Cst = omap ? Cout : Ws;
+    const int po = num_panels(Cst), zo = last_panel_width(Cst);
+    for (int r = warp; r < kPleafV * po; r += nw) {
+      const int vv = r / po, p = r % po;
+      const int64_t v = v0 + vv;
+      if (v >= n) continue;
+      const int zp = p == po - 1 ? zo : kZ;
+      if (lane < zp) {
+        const int col = p * kZ + lane;
+        out[static_cast<int64_t>(p) * n * kZ + v * zp + lane] = col < Cst ? sO[vv * oslice + col] : 0.f;
+      }
+    }
+  }
+}
+
 // Register-blocked eMA (see ema_blocked) on a same-color tile of the (k-1)
 // problem; descriptors from build_blocked(k-1, s-1, a-1).
 // blocks of a group are sorted by pattern; BlockDesc.pad of a run's first
