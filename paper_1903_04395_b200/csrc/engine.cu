@@ -1819,11 +1819,15 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
     const int cst = e.omap.empty() ? e.Ws : e.Cout;
     const int oslice = (cst + 31) / 32 * 32 + 1;
-    const size_t smem = static_cast<size_t>(dev::kPleafV) * (slice + oslice) * 4;
-    TCG_CUDA(cudaFuncSetAttribute(dev::ema_rtv_pleaf, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(
-        1, std::min<int64_t>((n_ + dev::kPleafV - 1) / dev::kPleafV, 148 * 16)));
-    dev::ema_rtv_pleaf<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_,
+    static const int pv = [] {  // vertices per CTA pass (1, 2 or 4; measured cfg4 node 4: 104.6 / 107.6 / 138.7 ms)
+      const char* s = std::getenv("TCG_PLEAF_V");
+      return s ? std::atoi(s) : 1;
+    }();
+    const size_t smem = static_cast<size_t>(pv) * (slice + oslice) * 4;
+    auto kern = pv == 1 ? dev::ema_rtv_pleaf<1> : pv == 4 ? dev::ema_rtv_pleaf<4> : dev::ema_rtv_pleaf<2>;
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n_ + pv - 1) / pv, 148 * 16)));
+    kern<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_,
                                                       e.d_rtv_drop, e.size - 1, e.Ws, e.d_omap, e.Cout, n_, slice,
                                                       oslice, table_ptr(e.out_off));
     return;

@@ -399,7 +399,7 @@ ema_rt_node_w(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
 // accumulates all kPleafV vertices into the vertices' output rows staged in
 // smem (storage order: RR columns, or the RS slots of the parent's SpMM),
 // which warps then write as whole 128 B panel rows.
-constexpr int kPleafV = 4;
+template <int kPleafV>
 __global__ void __launch_bounds__(256)
 ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
               const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap,
