@@ -1136,6 +1136,16 @@ void Engine::setup_rooted_ema(int max_smem) {
           dr[static_cast<size_t>(j) * sp1 + i] = static_cast<uint32_t>(index_of(t2, m)) | (static_cast<uint32_t>(cs[i]) << 16);
         }
       }
+      if (sp1 <= 6 && K <= 16) {  // packed: uint4 per output (6 x 16-bit A index, 6 x 4-bit colour)
+        std::vector<uint32_t> pk(static_cast<size_t>(e.Ws) * 4, 0u);
+        for (int32_t j = 0; j < e.Ws; ++j)
+          for (int i = 0; i < sp1; ++i) {
+            const uint32_t x = dr[static_cast<size_t>(j) * sp1 + i];
+            pk[static_cast<size_t>(j) * 4 + (i >> 1)] |= (x & 0xFFFFu) << ((i & 1) * 16);
+            pk[static_cast<size_t>(j) * 4 + 3] |= (x >> 16) << (4 * i);
+          }
+        dr.swap(pk);
+      }
       e.d_rtv_drop = dupload(dr, stream_);
       e.rtv_pleaf = true;
     }

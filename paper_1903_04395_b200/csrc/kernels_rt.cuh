@@ -454,12 +454,25 @@ ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
       float acc[kPleafV];
 #pragma unroll
       for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = 0.f;
-      const uint32_t* dr = drop + static_cast<int64_t>(j) * sp;
-      for (int i = 0; i < sp; ++i) {
-        const uint32_t e = __ldg(dr + i);
-        const int ia = static_cast<int>(e & 0xFFFFu), ih = static_cast<int>(e >> 16) + slice - 32;
+      if (sp <= 6) {  // packed row: six 16-bit A indices + six 4-bit colours in one 16 B load
+        const uint4 q = __ldg(reinterpret_cast<const uint4*>(drop) + j);
+        const uint32_t w[3] = {q.x, q.y, q.z};
 #pragma unroll
-        for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], smem[vv * slice + ih], acc[vv]);
+        for (int i = 0; i < 6; ++i) {
+          if (i >= sp) break;
+          const int ia = static_cast<int>((w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
+          const int ih = static_cast<int>((q.w >> (4 * i)) & 0xFu) + slice - 32;
+#pragma unroll
+          for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], smem[vv * slice + ih], acc[vv]);
+        }
+      } else {
+        const uint32_t* dr = drop + static_cast<int64_t>(j) * sp;
+        for (int i = 0; i < sp; ++i) {
+          const uint32_t e = __ldg(dr + i);
+          const int ia = static_cast<int>(e & 0xFFFFu), ih = static_cast<int>(e >> 16) + slice - 32;
+#pragma unroll
+          for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], smem[vv * slice + ih], acc[vv]);
+        }
       }
 #pragma unroll
       for (int vv = 0; vv < kPleafV; ++vv) {
