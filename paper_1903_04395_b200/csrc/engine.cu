@@ -1122,7 +1122,9 @@ void Engine::setup_rooted_ema(int max_smem) {
       const char* s = std::getenv("TCG_RTV_PLEAF");
       return s ? std::atoi(s) : 1;
     }();
-    if (e.rt_vtx && e.p_leaf && !e.root && !e.a_leaf && pleaf_mode && e.Wa < 65536) {
+    // (also for wide tiled nodes: a leaf passive child makes the blocked
+    // micro-patterns and the 8-column tile chunks mostly overhead)
+    if ((e.rt_vtx || e.Ws >= 512) && e.p_leaf && !e.root && !e.a_leaf && pleaf_mode && e.Wa < 65536) {
       // out'[S'] = sum over d in S' of A'[S' minus d] * H[d]: the drop table
       const int K = k - 1, sp1 = e.size - 1;
       std::vector<uint32_t> dr(static_cast<size_t>(e.Ws) * sp1);
