@@ -7,7 +7,8 @@ coloring, the neighbour histogram, every internal node's SpMM + fused eMA,
 and the fp64 root total -- one full pass of the hot path.
 
   python bench.py [--config cfg3] [--gpus N] [--steps K] [--warmup W]
-  python bench.py --impl reference ...      (the reference CPU engine, sampled)
+  python bench.py --impl reference ...      (the unmodified reference CPU engine: one full
+                                            coloring, timed in K slices)
 
 Multi-GPU (torchrun, one rank per GPU): colorings are independent units, so
 every rank runs its own K colorings (seeds offset by rank) on a replica of the
@@ -162,6 +163,14 @@ def build_graph(spec):
     return g
 
 
+def bench_config(name, n, nnz, k, world):
+    """The `config` object of BOTH arms (identical, so the driver can pair them)."""
+    csr_mb = (8 * (n + 1) + 4 * nnz) / 1e6
+    return {"workload": f"{name}: {CONFIGS[name][3]}", "n": int(n), "nnz": int(nnz), "k": int(k),
+            "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
+            "l2": "no flush: inputs larger than L2 (CSR %.0f MB + count tables vs 126 MB L2)" % csr_mb}
+
+
 def cpu_reference(g, parents, seed, reps=1, pairs=32):
     """The UNMODIFIED reference engine (oracle/_ref), sampled (ref_driver.cpp ref_time_sampled)."""
     import numpy as np
@@ -172,7 +181,7 @@ def cpu_reference(g, parents, seed, reps=1, pairs=32):
     k = len(parents)
     e = np.array(O.parent_array_edges(parents), np.int32).reshape(-1)
     out = np.zeros(8)
-    cores = os.cpu_count() or 1
+    cores = O.physical_cores()
     rc = O.ref().ref_time_sampled(rg.h, k, e, 0, seed, cores, reps, pairs, out)
     if rc != 0:
         raise RuntimeError("reference sampled timing failed")
@@ -181,17 +190,28 @@ def cpu_reference(g, parents, seed, reps=1, pairs=32):
 
 
 def ref_sample_desc(k):
-    return ("reference vectorized engine (oracle/_ref, -O3, fp64, Z=16, WorkerPool=all host threads): "
-            "one full-graph SpMM batch of 16 and of 1 column, 32 ema() column pairs, random_coloring and "
-            f"init_leaf_table timed in full, then summed over the k={k} plan's batches/pairs "
-            "(ref_driver.cpp ref_time_sampled)")
+    return ("MODEL of one coloring of the reference vectorized engine (oracle/_ref, -O3, fp64, Z=16, WorkerPool = "
+            "physical cores): one full-graph SpMM batch of 16 and of 1 column, 32 ema() column pairs, "
+            f"random_coloring and init_leaf_table timed in full, then summed over the k={k} plan's batches/pairs "
+            "(ref_driver.cpp ref_time_sampled); checked against a full timed coloring in "
+            "profiles/r02_ref_full_vs_sampled.txt.  `bench.py --impl reference` times a FULL coloring.")
 
 
 def run_reference(args, rank, world, local, dist):
+    """The reference's own CPU path, unmodified (oracle/_ref), on this box's host cores.
+
+    The graph comes from the reference's own generate_rmat (synthgen.hpp:40-74).
+    ONE full coloring (random_coloring + run_iteration(vectorized), engines.hpp:
+    106-132) is replayed through the reference's public pieces in K slices of
+    about equal estimated cost (ref_driver.cpp RefStepper, bit-identical to
+    run_iteration): step i executes slice i, so the K timed steps together
+    execute and time the whole coloring -- nothing is extrapolated.  Warm-up
+    steps run the first slices of an untimed coloring (seed 0)."""
     spec, parents, ncol, desc = CONFIGS[args.config]
     if rank != 0:
         return
     try:
+        import numpy as np
         import oracle as O
         if not O.ref_available():
             O.build(ref=True)
@@ -201,26 +221,55 @@ def run_reference(args, rank, world, local, dist):
     except Exception as ex:  # noqa: BLE001
         print(json.dumps({"impl": "reference", "unavailable": f"{type(ex).__name__}: {ex}"}))
         return
-    g = build_graph(spec)
-    vals = []
-    rg = None
-    for i in range(args.warmup + args.steps):
-        r, rg = cpu_reference(g, parents, 1 + i) if rg is None else (cpu_reference(g, parents, 1 + i)[0], rg)
-        if i >= args.warmup:
-            vals.append(r)
-        log(f"[bench] reference step {i}: {r['ms']:.1f} ms/coloring (sample wall {r['sample_wall_s']:.1f}s)")
-    v = statistics.mean(x["ms"] for x in vals)
+    t0 = time.perf_counter()
+    rg = O.RefGraph.rmat(*spec)
+    n, rp, _ = rg.csr()
+    nnz = int(rp[-1])
+    gsec = time.perf_counter() - t0
+    log(f"[bench] reference graph (synthgen generate_rmat) n={n} nnz={nnz} in {gsec:.1f}s")
+    k = len(parents)
+    e = np.array(O.parent_array_edges(parents), np.int32).reshape(-1)
+    cores = O.physical_cores()
+    warm = O.RefStepper(rg, k, e, 0, 0, cores, 400)
+    for i in range(args.warmup):
+        warm.run(i)
+    del warm
+    st = O.RefStepper(rg, k, e, 0, 1, cores, args.steps)
+    step_s = []
+    for i in range(args.steps):
+        step_s.append(st.run(i))
+        log(f"[bench] reference step {i}: {step_s[-1]:.2f} s")
+    total, node_stats, extra = st.finish()
+    full_ms = sum(step_s) * 1e3
+    spmm_ms = float(node_stats[:, 1].sum() * 1e3)
+    ema_ms = float(node_stats[:, 2].sum() * 1e3)
+    golden = None
+    try:
+        gz = np.load(os.path.join(ROOT, "tests", "golden", f"{args.config}.npz"))
+        if "totals" in gz and int(gz["seeds"][0]) == 1:
+            golden = float(gz["totals"][0])
+    except Exception:  # noqa: BLE001
+        pass
     line = {
-        "impl": "reference", "metric": METRIC, "value": v, "unit": "ms/coloring",
-        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": v,
+        "impl": "reference", "metric": METRIC, "value": full_ms, "unit": "ms/coloring",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms / args.steps,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic R-MAT from the reference generator (graph seed 1)",
-        "config": {"workload": f"{args.config}: {desc}", "n": g.n, "nnz": g.nnz(), "k": len(parents)},
-        "cpu_baseline": {"value": v, "unit": "ms/coloring", "cores": vals[0]["cores"], "kind": "reference",
-                         "sample": ref_sample_desc(len(parents)),
-                         "spmm_ms": statistics.mean(x["spmm_ms"] for x in vals),
-                         "ema_ms": statistics.mean(x["ema_ms"] for x in vals)},
-        "e2e": {"value": v, "unit": "ms/coloring", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "data": "synthetic R-MAT from the reference's own generate_rmat (graph seed 1), coloring seed 1",
+        "config": bench_config(args.config, n, nnz, k, world),
+        "cpu_baseline": {"value": full_ms, "unit": "ms/coloring", "cores": cores, "kind": "reference",
+                         "sample": f"ONE FULL coloring (seed 1) of the unmodified reference vectorized engine "
+                                   f"(oracle/_ref: random_coloring + IterationRun::run order, Z=16, fp64, "
+                                   f"WorkerPool of {cores} workers = physical cores per lscpu), executed in "
+                                   f"{args.steps} timed slices of about equal estimated cost (ref_driver.cpp "
+                                   f"RefStepper, bit-identical to run_iteration)",
+                         "spmm_ms": spmm_ms, "ema_ms": ema_ms},
+        "e2e": {"value": full_ms, "unit": "ms/coloring", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "step_s": [round(x, 3) for x in step_s],
+        "node_seconds": {str(i): round(float(node_stats[i, 0]), 4) for i in range(node_stats.shape[0])
+                         if node_stats[i, 0] > 0},
+        "coloring_s": float(extra[0]), "units": int(extra[1]),
+        "rooted_total": total, "rooted_total_golden": golden,
+        "graph_build_s": round(gsec, 1),
     }
     print(json.dumps(line), flush=True)
 
@@ -314,10 +363,8 @@ def run_b200(args, rank, world, local, dist):
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": False,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 tables, f64 accumulate/root",
         "data": "synthetic R-MAT from the reference generator (graph seed 1), colorings seeds 1.. on device",
-        "config": {"workload": f"{args.config}: {desc}", "n": g.n, "nnz": g.nnz(), "k": len(parents),
-                   "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
-                   "l2": "inputs larger than L2 (CSR %.0f MB + count tables %.1f GB vs 126 MB L2)"
-                         % ((g.csc_col_ptr.nbytes + g.csc_rows.nbytes) / 1e6, need / 1e9)},
+        "config": bench_config(args.config, g.n, g.nnz(), len(parents), world),
+        "device_bytes": need,
         "roofline": {"kernel": "spmm phase (bucket_rows + segment colour order + pair_expand + spmm_rooted + rooted_fixup)",
                      "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
                      "unit": "GB/s", "frac": spmm_gbs / hbm_peak if spmm_gbs else None,

@@ -275,8 +275,81 @@ def ref():
                                    C.POINTER(C.c_uint64), C.POINTER(C.c_double)]
         R.ref_time_sampled.argtypes = [vp, C.c_int, _i32p, C.c_int, C.c_uint64, C.c_int, C.c_int,
                                        C.c_int, _f64p]
+        R.ref_run_iteration_stats.argtypes = [vp, C.c_int, _i32p, C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                              C.POINTER(C.c_double), C.POINTER(C.c_double), _f64p,
+                                              C.POINTER(C.c_int)]
+        R.ref_step_begin.restype = vp
+        R.ref_step_begin.argtypes = [vp, C.c_int, _i32p, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_int]
+        R.ref_step_run.argtypes = [vp, C.c_int, C.POINTER(C.c_double)]
+        R.ref_step_finish.argtypes = [vp, C.POINTER(C.c_double), _f64p, C.POINTER(C.c_int), _f64p]
+        R.ref_step_free.argtypes = [vp]
         _ref = R
     return _ref
+
+
+def physical_cores() -> int:
+    """Physical cores of this host (lscpu: sockets x cores per socket), else os.cpu_count()."""
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        f = {}
+        for line in out.splitlines():
+            if ":" in line:
+                a, b = line.split(":", 1)
+                f[a.strip()] = b.strip()
+        cores = int(f["Core(s) per socket"]) * int(f.get("Socket(s)", "1"))
+        if cores > 0:
+            return cores
+    except Exception:  # noqa: BLE001
+        pass
+    return os.cpu_count() or 1
+
+
+class RefStepper:
+    """One coloring of the UNMODIFIED reference vectorized engine, replayed in
+    `steps` slices of about equal estimated cost (ref_driver.cpp RefStepper):
+    random_coloring, init_leaf_table, load_batch + spmm_csc per Z-batch and
+    ema() per grouped split, in IterationRun::run's order (engines.hpp:106-132,
+    224-268).  Bit-identical to run_iteration; every unit is executed."""
+
+    def __init__(self, g: "RefGraph", k: int, edges, root: int, seed: int, workers: int, steps: int,
+                 batch: int = 16):
+        self.g = g  # keep the graph alive
+        e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1))
+        self.h = ref().ref_step_begin(g.h, k, e if e.size else np.zeros(2, np.int32), root, seed, workers,
+                                      batch, steps)
+        if not self.h:
+            raise RuntimeError("reference stepper refused the input")
+        self.steps = steps
+
+    def run(self, i: int) -> float:
+        sec = C.c_double()
+        if ref().ref_step_run(self.h, i, C.byref(sec)) < 0:
+            raise RuntimeError(f"reference step {i} failed")
+        return sec.value
+
+    def finish(self):
+        total, nn = C.c_double(), C.c_int()
+        ns = np.zeros(3 * MAXNODES)
+        out = np.zeros(2)
+        if ref().ref_step_finish(self.h, C.byref(total), ns, C.byref(nn), out) != 0:
+            raise RuntimeError("reference stepper not finished")
+        return total.value, ns[:3 * nn.value].reshape(nn.value, 3), out
+
+    def __del__(self):
+        if getattr(self, "h", None) and _ref is not None:
+            _ref.ref_step_free(self.h)
+            self.h = None
+
+
+def ref_run_iteration_stats(g: "RefGraph", k: int, edges, root: int, seed: int, workers: int, batch: int = 16):
+    """random_coloring + run_iteration(vectorized) in one call, timed, with NodeStats::seconds."""
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1))
+    total, sec, nn = C.c_double(), C.c_double(), C.c_int()
+    ns = np.zeros(MAXNODES)
+    if ref().ref_run_iteration_stats(g.h, k, e if e.size else np.zeros(2, np.int32), root, seed, workers, batch,
+                                     C.byref(total), C.byref(sec), ns, C.byref(nn)) != 0:
+        raise RuntimeError("reference run_iteration failed")
+    return total.value, sec.value, ns[:nn.value]
 
 
 class RefGraph:

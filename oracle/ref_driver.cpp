@@ -6,11 +6,13 @@
 // into oracle/_ref/libtcref.so.  Used (1) to pin the C restatement
 // (tc_oracle.c) and generate tests/golden fixtures, and (2) as the CPU
 // baseline / `bench.py --impl reference` arm.  Nothing here is product code.
+#include <algorithm>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <exception>
 #include <memory>
+#include <optional>
 #include <vector>
 
 #include "treecount/count_table.hpp"
@@ -149,6 +151,33 @@ uint64_t ref_automorphisms(int k, const int32_t* edges) {
 int64_t ref_estimate_bytes(int k, const int32_t* edges, int root, int64_t n) {
   try {
     return estimate_bytes(partition(make_tree(k, edges, root)), n, k);
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// run_iteration(EngineKind::vectorized, ...) with the per-node NodeStats::seconds
+// (engines.hpp:53-61,106-132): node_seconds[num_nodes] by plan node id.
+int ref_run_iteration_stats(const void* gp, int k, const int32_t* edges, int root, uint64_t seed,
+                            int workers, int batch, double* total, double* seconds,
+                            double* node_seconds, int* num_nodes) {
+  try {
+    const Graph& g = *static_cast<const Graph*>(gp);
+    TemplateTree t = make_tree(k, edges, root);
+    PartitionPlan plan = partition(t);
+    ColorIndexer idx(k);
+    EngineConfig cfg;
+    cfg.workers = workers;
+    cfg.batch = batch;
+    const double t0 = now_s();
+    Coloring c = random_coloring(g, k, seed);
+    IterationResult r = run_iteration(EngineKind::vectorized, g, plan, c, idx, cfg);
+    if (seconds) *seconds = now_s() - t0;
+    *total = r.rooted_total;
+    *num_nodes = static_cast<int>(r.per_node.size());
+    if (node_seconds)
+      for (size_t i = 0; i < r.per_node.size(); ++i) node_seconds[i] = r.per_node[i].seconds;
+    return 0;
   } catch (const std::exception&) {
     return -1;
   }
@@ -301,5 +330,203 @@ int ref_time_sampled(const void* gp, int k, const int32_t* edges, int root, uint
     return -1;
   }
 }
+
+// ---------------------------------------------------------------------------
+// One coloring of the reference vectorized engine, replayed in K bounded steps.
+//
+// IterationRun::run (engines.hpp:106-132) with vectorized_node
+// (engines.hpp:224-246) and accumulate_grouped (252-268) is a fixed sequence of
+// pool-dispatched units over the reference's own public pieces:
+// random_coloring (estimator.hpp:66), init_leaf_table per leaf, the zeroed
+// output CountTable per internal node, one load_batch + spmm_csc pass per
+// batch of <= Z passive columns, one ema() per grouped split (column pair),
+// the release of the children, and the sequential root sum.  The stepper
+// executes exactly that sequence, in that order, with the same WorkerPool
+// slicing -- so the result is bit-identical to run_iteration (tests pin it) --
+// but lets the caller time it in K slices of about equal estimated cost, so a
+// full coloring of cfg3 (minutes on the host) is measured IN FULL across
+// bench.py's K steps instead of being extrapolated from a sample.
+struct RefStepper {
+  const Graph* g = nullptr;
+  int k = 0;
+  uint64_t seed = 0;
+  PartitionPlan plan;
+  ColorIndexer idx{1};
+  std::vector<SplitTable> splits;
+  std::unique_ptr<WorkerPool> pool;
+  int Z = 16;
+  Coloring col;
+  std::vector<std::optional<CountTable>> tables;
+  enum Kind { COLOR, LEAF, ALLOC, SPMM, EMA, FREE, ROOT };
+  struct Unit { Kind kind; int node; int a, b; double cost; };
+  std::vector<Unit> units;
+  std::vector<size_t> cuts;  // step i runs units [cuts[i], cuts[i+1])
+  size_t next = 0;
+  std::vector<double> node_sec, node_spmm, node_ema;
+  double total = 0, color_sec = 0;
+};
+
+void* ref_step_begin(const void* gp, int k, const int32_t* edges, int root, uint64_t seed,
+                     int workers, int batch, int steps) {
+  try {
+    auto st = std::make_unique<RefStepper>();
+    st->g = static_cast<const Graph*>(gp);
+    st->k = k;
+    st->seed = seed;
+    st->plan = partition(make_tree(k, edges, root));
+    st->idx = ColorIndexer(k);
+    st->splits = build_plan_splits(st->plan, st->idx);  // estimate(): once, before the colorings
+    st->pool = std::make_unique<WorkerPool>(workers);
+    st->Z = std::max(1, batch);
+    st->tables.resize(st->plan.nodes.size());
+    const double n = st->g->n, nnz = static_cast<double>(st->g->csc_col_ptr[st->g->n]);
+    auto& u = st->units;
+    u.push_back({RefStepper::COLOR, -1, 0, 0, 4 * n});
+    for (int id : st->plan.dp_order) {
+      const PlanNode& nd = st->plan.node(id);
+      if (nd.is_leaf()) {
+        u.push_back({RefStepper::LEAF, id, 0, 0, 8 * n * k});
+        continue;
+      }
+      const SplitTable& sp = st->splits[static_cast<size_t>(id)];
+      u.push_back({RefStepper::ALLOC, id, 0, 0, 8 * n * sp.parent_cols});
+      for (int32_t c0 = 0; c0 < sp.passive_cols; c0 += st->Z) {
+        const int zc = static_cast<int>(std::min<int32_t>(st->Z, sp.passive_cols - c0));
+        u.push_back({RefStepper::SPMM, id, c0, zc, 8 * nnz * zc + 16 * n * zc});
+      }
+      for (int32_t ip = 0; ip < sp.passive_cols; ++ip)
+        u.push_back({RefStepper::EMA, id, ip, 0, 32 * n * sp.partners_per_passive});
+      u.push_back({RefStepper::FREE, id, 0, 0, 0});
+    }
+    u.push_back({RefStepper::ROOT, st->plan.full_node(), 0, 0, 8 * n});
+    double tot = 0;
+    for (auto& x : u) tot += x.cost;
+    steps = std::max(1, steps);
+    st->cuts.assign(static_cast<size_t>(steps) + 1, u.size());
+    st->cuts[0] = 0;
+    double cum = 0;
+    size_t j = 0;
+    for (int i = 1; i < steps; ++i) {
+      const double target = tot * i / steps;
+      while (j < u.size() && cum + u[j].cost * 0.5 < target) cum += u[j++].cost;
+      st->cuts[static_cast<size_t>(i)] = j;
+    }
+    st->node_sec.assign(st->plan.nodes.size(), 0.0);
+    st->node_spmm.assign(st->plan.nodes.size(), 0.0);
+    st->node_ema.assign(st->plan.nodes.size(), 0.0);
+    return st.release();
+  } catch (const std::exception&) {
+    return nullptr;
+  }
+}
+
+static void ref_step_unit(RefStepper& s, const RefStepper::Unit& x) {
+  const Graph& g = *s.g;
+  WorkerPool& pool = *s.pool;
+  const double t0 = now_s();
+  switch (x.kind) {
+    case RefStepper::COLOR:
+      s.col = random_coloring(g, s.k, s.seed);
+      break;
+    case RefStepper::LEAF:
+      s.tables[static_cast<size_t>(x.node)] = init_leaf_table(s.col, s.k, Layout::column_major);
+      break;
+    case RefStepper::ALLOC:
+      s.tables[static_cast<size_t>(x.node)] =
+          CountTable(g.n, s.splits[static_cast<size_t>(x.node)].parent_cols, Layout::column_major);
+      break;
+    case RefStepper::SPMM: {
+      const PlanNode& nd = s.plan.node(x.node);
+      CountTable& passive = *s.tables[static_cast<size_t>(nd.passive_child)];
+      RowBatch staged(g.n, x.b);
+      pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
+        load_batch(passive, x.a, x.b, staged, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
+      });
+      ColumnBlock block{&passive, x.a, x.b};
+      pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) {
+        spmm_csc(g, staged, block, static_cast<vertex_t>(lo), static_cast<vertex_t>(hi));
+      });
+      break;
+    }
+    case RefStepper::EMA: {
+      const PlanNode& nd = s.plan.node(x.node);
+      const SplitTable& st = s.splits[static_cast<size_t>(x.node)];
+      const CountTable& active = *s.tables[static_cast<size_t>(nd.active_child)];
+      const CountTable& passive = *s.tables[static_cast<size_t>(nd.passive_child)];
+      CountTable& out = *s.tables[static_cast<size_t>(x.node)];
+      std::span<const double> col_p = passive.column(x.a);
+      const size_t base = static_cast<size_t>(x.a) * static_cast<size_t>(st.partners_per_passive);
+      for (int q = 0; q < st.partners_per_passive; ++q) {
+        std::span<double> col_s = out.column(st.grouped_parent[base + q]);
+        std::span<const double> col_a = active.column(st.grouped_active[base + q]);
+        pool.for_range(static_cast<size_t>(g.n), [&](size_t lo, size_t hi, int) { ema(col_s, col_a, col_p, lo, hi); });
+      }
+      break;
+    }
+    case RefStepper::FREE: {
+      const PlanNode& nd = s.plan.node(x.node);
+      s.tables[static_cast<size_t>(nd.active_child)].reset();
+      s.tables[static_cast<size_t>(nd.passive_child)].reset();
+      break;
+    }
+    case RefStepper::ROOT: {
+      const CountTable& t = *s.tables[static_cast<size_t>(x.node)];
+      double total = 0.0;
+      for (vertex_t i = 0; i < g.n; ++i) total += t.at(i, 0);
+      s.total = total;
+      break;
+    }
+  }
+  const double dt = now_s() - t0;
+  if (x.node >= 0) {
+    s.node_sec[static_cast<size_t>(x.node)] += dt;
+    if (x.kind == RefStepper::SPMM) s.node_spmm[static_cast<size_t>(x.node)] += dt;
+    if (x.kind == RefStepper::EMA) s.node_ema[static_cast<size_t>(x.node)] += dt;
+  } else {
+    s.color_sec += dt;
+  }
+}
+
+// Runs step i's units; *seconds = its wall time.  Returns the units run or -1.
+int ref_step_run(void* sp, int i, double* seconds) {
+  try {
+    RefStepper& s = *static_cast<RefStepper*>(sp);
+    if (i < 0 || static_cast<size_t>(i) + 1 >= s.cuts.size()) return -1;
+    const double t0 = now_s();
+    const size_t end = s.cuts[static_cast<size_t>(i) + 1];
+    int ran = 0;
+    for (; s.next < end; ++s.next, ++ran) ref_step_unit(s, s.units[s.next]);
+    if (seconds) *seconds = now_s() - t0;
+    return ran;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+// After the last step: the rooted total, and per node id {seconds, spmm, ema}
+// (node_stats[3 * num_nodes]); out[0] = coloring seconds, out[1] = units.
+int ref_step_finish(void* sp, double* total, double* node_stats, int* num_nodes, double* out) {
+  try {
+    RefStepper& s = *static_cast<RefStepper*>(sp);
+    if (s.next != s.units.size()) return -1;
+    *total = s.total;
+    *num_nodes = static_cast<int>(s.plan.nodes.size());
+    if (node_stats)
+      for (size_t i = 0; i < s.plan.nodes.size(); ++i) {
+        node_stats[3 * i] = s.node_sec[i];
+        node_stats[3 * i + 1] = s.node_spmm[i];
+        node_stats[3 * i + 2] = s.node_ema[i];
+      }
+    if (out) {
+      out[0] = s.color_sec;
+      out[1] = static_cast<double>(s.units.size());
+    }
+    return 0;
+  } catch (const std::exception&) {
+    return -1;
+  }
+}
+
+void ref_step_free(void* sp) { delete static_cast<RefStepper*>(sp); }
 
 }  // extern "C"

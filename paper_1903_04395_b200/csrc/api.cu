@@ -92,6 +92,7 @@ int tcg_graph_from_csr(int32_t n, const int64_t* row_ptr, const int32_t* col, tc
   return guarded([&] {
     need(out, "out");
     need(row_ptr, "row_ptr");
+    if (n < 0) throw tcg::invalid_argument("negative vertex count");
     if (row_ptr[n] > 0) need(col, "col");
     auto g = std::make_unique<tcg_graph>();
     g->csr = tcg::csr_adopt(n, row_ptr, col);

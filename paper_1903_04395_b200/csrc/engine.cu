@@ -224,16 +224,6 @@ Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
   // B200 that costs more than the L2 misses of the unsplit gather source
   // (cfg3 49.9 -> 47.9 ms, cfg4 1666 -> 1049 ms).
   if (const char* e = std::getenv("TCG_ROOTED_PARTS")) rooted_part_mb_ = std::atoi(e);
-  if (const char* e = std::getenv("TCG_L2_PERSIST"); e && std::atoi(e) > 0) {
-    int win = 0;
-    TCG_CUDA(cudaDeviceGetAttribute(&win, cudaDevAttrMaxAccessPolicyWindowSize, cfg.device));
-    const size_t want = std::min<size_t>(static_cast<size_t>(prop.persistingL2CacheMaxSize),
-                                         static_cast<size_t>(std::atoi(e)) << 20);
-    TCG_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want));
-    persist_max_ = std::min<int64_t>(win, static_cast<int64_t>(want));
-    std::fprintf(stderr, "[tcg] L2 persisting: max window %d B, set-aside %zu B (device max %d)\n", win,
-                 want, prop.persistingL2CacheMaxSize);
-  }
   TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
   TCG_CUDA(cudaMalloc(&d_scalars_, 64));
   TCG_CUDA(cudaMalloc(&d_seeds_, 1024 * sizeof(uint64_t)));
@@ -290,7 +280,6 @@ void Engine::release_template() {
     dfree(e.d_packed);
     dfree(e.d_groups);
     dfree(e.d_blocks);
-    dfree(e.d_ins);
     dfree(e.d_slot_acc);
     dfree(e.d_slot_col);
     dfree(e.d_pinv);
@@ -647,14 +636,10 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   need_hist_ = false;
   int max_smem = 0;
   TCG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg_.device));
-  static const int lmode = [] {
-    const char* s = std::getenv("TCG_LSPMM");
-    return s ? std::atoi(s) : 0;
-  }();
   static const int rooted_mode = [] {
     const char* s = std::getenv("TCG_ROOTED");
     return s ? std::atoi(s) : 1;
-  }() && !lmode;
+  }();
   for (int id : plan_.dp_order) {
     if (plan_.is_leaf(id)) continue;
     NodeExec e;
@@ -771,47 +756,6 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
     }
     exec_.push_back(e);
   }
-  // Leaf-pushed SpMM: a node whose passive child p is (h, 1, h-1) gathers
-  // p's own P' (C(k,h-1) columns) per neighbour color instead of M_p
-  // (C(k,h) columns); p's eMA is then skipped.  Opt-in (TCG_LSPMM=1): on B200
-  // the per-(vertex, color) buckets (~deg/k neighbours) and the Q round trip
-  // cost more than the gathered columns save (measured cfg3: node 2 SpMM
-  // 26.6 -> 70 ms), so the direct panel SpMM is the default.
-  need_bucket_ = false;
-  static const int64_t q_budget = [] {
-    const char* s = std::getenv("TCG_Q_GB");
-    return (s ? std::atoll(s) : 12ll) << 30;
-  }();
-  std::vector<int> pos(plan_.num_nodes, -1);
-  for (size_t i = 0; i < exec_.size(); ++i) pos[exec_[i].id] = static_cast<int>(i);
-  for (auto& e : exec_) {
-    if (!lmode || e.p_leaf || sharded()) continue;
-    NodeExec& c = exec_[pos[e.p]];
-    if (!c.a_leaf || c.root) continue;
-    const int32_t Cx = static_cast<int32_t>(B(k, c.size - 1));
-    const int64_t comb = static_cast<int64_t>(Cx + e.Cp) * (dev::kTileV + 1) * 4;
-    if (Cx >= e.Cp || comb > max_smem - 4096) continue;
-    e.lspmm = true;
-    e.Cx = Cx;
-    e.comb_smem = static_cast<size_t>(comb);
-    c.skip_ema = !(cfg_.flags & TCG_KEEP_TABLES);
-    need_bucket_ = true;
-    std::vector<int32_t> ins(static_cast<size_t>(k) * Cx, -1);
-    int cs[kMaxK], us[kMaxK];
-    for (int32_t x = 0; x < Cx; ++x) {
-      set_of(k, x, c.size - 1, cs);
-      for (int col = 0; col < k; ++col) {
-        if (std::find(cs, cs + c.size - 1, col) != cs + c.size - 1) continue;
-        int m = 0;
-        for (int q = 0; q < c.size - 1 && cs[q] < col; ++q) us[m++] = cs[q];
-        us[m++] = col;
-        for (int q = 0; q < c.size - 1; ++q)
-          if (cs[q] > col) us[m++] = cs[q];
-        ins[static_cast<size_t>(col) * Cx + x] = static_cast<int32_t>(index_of(us, c.size));
-      }
-    }
-    e.d_ins = dupload(ins, stream_);
-  }
   setup_rooted_ema(max_smem);
   // Identical sub-template computations (same recursive shape and the same
   // table layout) are computed once: a later duplicate aliases the first
@@ -829,7 +773,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
       const char* lay = rooted_ema_ ? (e.omap.empty() ? "R" : "S") : "F";
       key[e.id] = "(" + key[e.a] + "," + key[e.p] + ")" + lay;
       e.dup_of = e.pp_dup_of = -1;
-      if (!dedup || lmode) continue;
+      if (!dedup) continue;
       auto it = first.find(key[e.id]);
       if (it == first.end() || e.root) {
         if (!e.root) first.emplace(key[e.id], static_cast<int>(i));
@@ -911,7 +855,7 @@ void Engine::setup_rooted_ema(int max_smem) {
   }();
   auto row_floats = [](int64_t C) { return C <= 0 ? 0 : dev::table_floats(C, 1); };
   for (auto& e : exec_) {
-    if ((!e.p_leaf && !e.rooted) || e.lspmm) return;
+    if (!e.p_leaf && !e.rooted) return;
     const int64_t Wa = e.a_leaf ? 0 : B(k - 1, e.sa - 1), Wp = B(k - 1, e.sp), Ws = e.root ? 1 : B(k - 1, e.size - 1);
     if (Wa >= 65536 || Wp >= 65536 || Ws >= 65536) return;
     e.rt_vtx = false;
@@ -1095,11 +1039,7 @@ void Engine::setup_rooted_ema(int max_smem) {
           std::vector<dev::GroupDesc> gr;
           std::vector<dev::BlockDesc> bl;
           if (e.rt_vtx) {  // vertex-per-CTA: the widest H1 the (k-1) colors allow (<= 8)
-            static const int hmax = [] {
-              const char* s = std::getenv("TCG_RTV_H");
-              return s ? std::atoi(s) : 6;
-            }();
-            e.rtv_h = std::max(dev::kH1, std::min(hmax, k - 1));
+            e.rtv_h = std::max(dev::kH1, std::min(6, k - 1));
             build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl, e.rtv_h, 16);
             std::vector<uint2> b2(bl.size());  // packed 8 B descriptors
             for (size_t i = 0; i < bl.size(); ++i)
@@ -1138,7 +1078,8 @@ void Engine::setup_rooted_ema(int max_smem) {
           dr[static_cast<size_t>(j) * sp1 + i] = static_cast<uint32_t>(index_of(t2, m)) | (static_cast<uint32_t>(cs[i]) << 16);
         }
       }
-      if (sp1 <= 6 && K <= 16) {  // packed: uint4 per output (6 x 16-bit A index, 6 x 4-bit colour)
+      e.rtv_packed = sp1 <= 6 && K <= 16;
+      if (e.rtv_packed) {  // packed: uint4 per output (6 x 16-bit A index, 6 x 4-bit colour)
         std::vector<uint32_t> pk(static_cast<size_t>(e.Ws) * 4, 0u);
         for (int32_t j = 0; j < e.Ws; ++j)
           for (int i = 0; i < sp1; ++i) {
@@ -1233,15 +1174,9 @@ void Engine::plan_arena_once(bool allow_stream) {
   table_off_.assign(plan_.num_nodes, -1);
   pprime_off_.assign(plan_.num_nodes, -1);
   hist_off_ = need_hist_ ? ap.alloc(table_bytes(plan_.k)) : -1;
-  colb_off_ = need_bucket_ ? ap.alloc(4 * std::max<int64_t>(nnz_, 1)) : -1;
-  boff_off_ = need_bucket_ ? ap.alloc(8 * static_cast<int64_t>(n_) * (plan_.k + 1)) : -1;
-  const int64_t q_budget = (std::getenv("TCG_Q_GB") ? std::atoll(std::getenv("TCG_Q_GB")) : 12ll) << 30;
-  std::vector<int64_t> child_pp(plan_.num_nodes, -1);  // P' kept alive for an LSpMM parent
-  int64_t lslots = 0;
   for (const auto& e : exec_)  // full-table SpMMs: their vertex-range part schedules
-    if (!e.p_leaf && !e.rooted && !e.lspmm && e.pp_dup_of < 0 && e.dup_of < 0)
+    if (!e.p_leaf && !e.rooted && e.pp_dup_of < 0 && e.dup_of < 0)
       for (int p = 0; p < dev::num_panels(e.Cp); ++p) ensure_schedules(parts_for_width(dev::panel_width(e.Cp, p)));
-  const int full_slots = sched_.count(1) ? sched_.at(1)[0].nslots : 0;
   // rooted SpMMs: parts are contiguous COLOR classes (one count for all
   // rooted nodes: the widest compressed panel's), over whole-row schedules
   need_rooted_ = need_pair_ = false;
@@ -1308,7 +1243,7 @@ void Engine::plan_arena_once(bool allow_stream) {
     for (auto& e : exec_) {
       // (a plan that streams active-leaf SpMMs to fit the device keeps streaming them)
       const bool base = virt_mode && !keep && !allow_stream && rooted_ema_ && e.a_leaf && !e.root && e.rooted &&
-                        !e.p_leaf && e.dup_of < 0 && !aliased[e.id] && !e.skip_ema && !e.lspmm;
+                        !e.p_leaf && e.dup_of < 0 && !aliased[e.id];
       // read only as an active child (staged through its P' map), or only by a
       // pair expansion (through the composed map)
       e.virt_px = base && feeds_pair[e.id] && pair_virt_ok[e.id] && active_uses[e.id] == 0;
@@ -1378,31 +1313,13 @@ void Engine::plan_arena_once(bool allow_stream) {
     } else if (!e.p_leaf) {
       e.pp_off = ap.alloc(table_bytes(e.Cp));
       pprime_off_[e.p] = e.pp_off;
-      if (e.lspmm) {
-        e.qchunk = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(plan_.k, q_budget / std::max<int64_t>(table_bytes(e.Cx), 1))));
-        e.q_off = ap.alloc(static_cast<int64_t>(e.qchunk) * table_bytes(e.Cx));
-        lslots = std::max<int64_t>(lslots, static_cast<int64_t>(e.qchunk) * full_slots);
-        if (!keep) {
-          ap.free(e.q_off);
-          if (child_pp[e.p] >= 0) ap.free(child_pp[e.p]);
-          if (table_off_[e.p] >= 0) ap.free(table_off_[e.p]);
-        }
-      } else if (!keep) {
-        ap.free(table_off_[e.p]);
-      }
+      if (!keep) ap.free(table_off_[e.p]);
     }
     if (!e.p_leaf && e.pp_dup_of < 0)
       for (const auto& y : exec_)  // one reference per node sharing this P'
         if (y.pp_dup_of >= 0 && exec_[y.pp_dup_of].id == e.id) ap.retain(e.pp_off);
     if (e.virt) {  // the table IS P' (released by the parent, which reads it as its active child)
       table_off_[e.id] = e.out_off = e.pp_off;
-      continue;
-    }
-    if (e.skip_ema) {                 // M of this node is never needed
-      table_off_[e.id] = -1;
-      e.out_off = -1;
-      if (!e.p_leaf) child_pp[e.id] = e.pp_off;  // X of the parent's LSpMM
-      if (!keep && !e.a_leaf) ap.free(table_off_[e.a]);
       continue;
     }
     e.out_off = ap.alloc(e.root ? 8 * static_cast<int64_t>(n_) : table_bytes(rooted_ema_ ? e.Cout : e.Cs));
@@ -1430,8 +1347,7 @@ void Engine::plan_arena_once(bool allow_stream) {
       }
   }
   arena_bytes_ = ap.peak;
-  partial_bytes_ = std::max<int64_t>(std::max<int64_t>(static_cast<int64_t>(max_slots_), lslots) * dev::kZ * 8,
-                                     rooted_partial * 8);
+  partial_bytes_ = std::max<int64_t>(static_cast<int64_t>(max_slots_) * dev::kZ * 8, rooted_partial * 8);
 }
 
 int64_t Engine::required_bytes() const {
@@ -1563,40 +1479,12 @@ void Engine::gather_per_vertex(const double* d_local, double* host_global) {
 template <int ZW, bool ONEHOT>
 static void launch_spmm_part(const PartSchedule& ps, cudaStream_t s, const int32_t* col,
                              const float* X, const uint8_t* colors, int color_base, float* Y,
-                             double* partial, bool first, int64_t& launches,
-                             const char* win_base = nullptr, int64_t win_bytes = 0) {
+                             double* partial, bool first, int64_t& launches) {
   constexpr int spw = 128 / ZW;  // segments per warp
   const int64_t ntasks = ps.nseg_padded / spw;
   const int64_t blocks = (ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
-  static const int rounds = [] {
-    const char* e = std::getenv("TCG_SPMM_R");
-    return e ? std::atoi(e) : 8;
-  }();
-  if (rounds == 16) {
-    dev::spmm_part<ZW, ONEHOT, 16><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
-        ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
-  } else if (win_bytes > 0) {
-    // pin the part's gather window in L2 (persisting) against the index and
-    // output streams that pass through L2 during the launch
-    cudaLaunchConfig_t lc = {};
-    lc.gridDim = dim3(static_cast<unsigned>(blocks));
-    lc.blockDim = dim3(dev::kSpmmWarps * 32);
-    lc.stream = s;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = const_cast<char*>(win_base);
-    at[0].val.accessPolicyWindow.num_bytes = static_cast<size_t>(win_bytes);
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    lc.attrs = at;
-    lc.numAttrs = 1;
-    TCG_CUDA(cudaLaunchKernelEx(&lc, dev::spmm_part<ZW, ONEHOT, 8>, ps.d_segs, ntasks, col, X, colors,
-                                color_base, Y, partial, first ? 1 : 0));
-  } else {
-    dev::spmm_part<ZW, ONEHOT, 8><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
-        ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
-  }
+  dev::spmm_part<ZW, ONEHOT><<<static_cast<unsigned>(blocks), dev::kSpmmWarps * 32, 0, s>>>(
+      ps.d_segs, ntasks, col, X, colors, color_base, Y, partial, first ? 1 : 0);
   ++launches;
   if (ps.nsplit_rows) {
     const int64_t total = static_cast<int64_t>(ps.nsplit_rows) * ZW;
@@ -1622,59 +1510,10 @@ void Engine::spmm(const float* X, float* Y, int64_t cols) {
     const int P = static_cast<int>(parts.size());
     for (int s = 0; s < P; ++s) {
       const PartSchedule& ps = parts[s];
-      const int64_t r0 = static_cast<int64_t>(n_) * s / P, r1 = static_cast<int64_t>(n_) * (s + 1) / P;
-      const char* wb = persist_max_ > 0 ? reinterpret_cast<const char*>(Xp + r0 * zw) : nullptr;
-      const int64_t wn = persist_max_ > 0 ? std::min<int64_t>((r1 - r0) * zw * 4, persist_max_) : 0;
-      if (zw == 32) launch_spmm_part<32, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
-      else if (zw == 16) launch_spmm_part<16, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
-      else launch_spmm_part<8, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_, wb, wn);
+      if (zw == 32) launch_spmm_part<32, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+      else if (zw == 16) launch_spmm_part<16, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
+      else launch_spmm_part<8, false>(ps, stream_, d_col_, Xp, nullptr, 0, Yp, d_partial_, s == 0, launches_);
     }
-  }
-  TCG_CUDA(cudaGetLastError());
-}
-
-// Leaf-pushed SpMM: P'_s = sum_c (A D_c X) inserted at S = x u {c}, in color
-// chunks of e.qchunk (Q chunk buffer at e.q_off).
-void Engine::lspmm(const NodeExec& e, const float* X, float* Pp) {
-  const PartSchedule& full = sched_.at(1)[0];
-  float* Q = table_ptr(e.q_off);
-  const int64_t q_stride = dev::table_floats(e.Cx, n_);
-  const int k = plan_.k;
-  for (int c0 = 0; c0 < k; c0 += e.qchunk) {
-    const int nc = std::min(e.qchunk, k - c0);
-    const int P = dev::num_panels(e.Cx);
-    for (int p = 0; p < P; ++p) {
-      const int zw = dev::panel_width(e.Cx, p);
-      const float* Xp = X + static_cast<int64_t>(p) * n_ * dev::kZ;
-      float* Qp = Q + static_cast<int64_t>(p) * n_ * dev::kZ;
-      const int spw = 128 / zw;
-      const int64_t ntasks = full.nseg_padded / spw;
-      const int64_t bpc = (ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps;
-      const unsigned grid = static_cast<unsigned>(bpc * nc);
-      const int64_t* boff = reinterpret_cast<const int64_t*>(arena_ + boff_off_);
-      const int32_t* colb = reinterpret_cast<const int32_t*>(arena_ + colb_off_);
-      if (zw == 32)
-        dev::spmm_bucket<32><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
-      else if (zw == 16)
-        dev::spmm_bucket<16><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
-      else
-        dev::spmm_bucket<8><<<grid, dev::kSpmmWarps * 32, 0, stream_>>>(full.d_segs, ntasks, bpc, full.d_slot_row, colb, boff, k, c0, Xp, Qp, q_stride, d_partial_, full.nslots);
-      ++launches_;
-      if (full.nsplit_rows) {
-        const int64_t total = static_cast<int64_t>(full.nsplit_rows) * zw;
-        for (int cl = 0; cl < nc; ++cl) {
-          dev::spmm_fixup<<<static_cast<unsigned>((total + 255) / 256), 256, 0, stream_>>>(
-              full.d_split_rows, full.d_slot_begin, full.nsplit_rows,
-              d_partial_ + static_cast<int64_t>(cl) * full.nslots * zw, Qp + cl * q_stride, zw, 1);
-          ++launches_;
-        }
-      }
-    }
-    auto kern = dev::lspmm_combine;
-    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.comb_smem)));
-    kern<<<static_cast<unsigned>((n_ + dev::kTileV - 1) / dev::kTileV), 512, e.comb_smem, stream_>>>(
-        Q, q_stride, c0, nc, e.d_ins, e.Cx, e.Cp, n_, Pp, c0 == 0 ? 1 : 0);
-    ++launches_;
   }
   TCG_CUDA(cudaGetLastError());
 }
@@ -1715,18 +1554,12 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
   const PartSchedule& ps = sched_.at(1)[0];  // whole rows; parts = color classes
   const uint32_t* colb = reinterpret_cast<const uint32_t*>(arena_ + rcol_off_);
   const int64_t* cuts = reinterpret_cast<const int64_t*>(arena_ + rcut_off_);
-  static const int minb = [] {
-    const char* s = std::getenv("TCG_ROOTED_MINB");
-    return s ? std::atoi(s) : 4;
-  }();
+  // (4 CTAs per SM at 64 registers: the occupancy sweep in DESIGN.md 3)
   auto pick = [&](auto pair_tag) -> const void* {
     constexpr bool P = decltype(pair_tag)::value;
-    return minb == 4 ? (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 4, P>)
-                        : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 4, P>)
-                                   : reinterpret_cast<const void*>(dev::spmm_rooted<8, 4, P>))
-                     : (zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 1, P>)
-                        : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 1, P>)
-                                   : reinterpret_cast<const void*>(dev::spmm_rooted<8, 1, P>));
+    return zw == 32 ? reinterpret_cast<const void*>(dev::spmm_rooted<32, 4, P>)
+           : zw == 16 ? reinterpret_cast<const void*>(dev::spmm_rooted<16, 4, P>)
+                      : reinterpret_cast<const void*>(dev::spmm_rooted<8, 4, P>);
   };
   const void* kern = e.pair ? pick(std::true_type{}) : pick(std::false_type{});
   // pair: the rows in color order (this coloring's re-ordered schedule)
@@ -1831,16 +1664,13 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
     const int cst = e.omap.empty() ? e.Ws : e.Cout;
     const int oslice = (cst + 31) / 32 * 32 + 1;
-    static const int pv = [] {  // vertices per CTA pass (1, 2 or 4; measured cfg4 node 4: 104.6 / 107.6 / 138.7 ms)
-      const char* s = std::getenv("TCG_PLEAF_V");
-      return s ? std::atoi(s) : 1;
-    }();
+    constexpr int pv = 1;  // vertices per CTA pass (measured cfg4 node 4, V = 1 / 2 / 4: 104.6 / 107.6 / 138.7 ms)
     const size_t smem = static_cast<size_t>(pv) * (slice + oslice) * 4;
-    auto kern = pv == 1 ? dev::ema_rtv_pleaf<1> : pv == 4 ? dev::ema_rtv_pleaf<4> : dev::ema_rtv_pleaf<2>;
+    auto kern = dev::ema_rtv_pleaf<pv>;
     TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n_ + pv - 1) / pv, 148 * 16)));
     kern<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_,
-                                                      e.d_rtv_drop, e.size - 1, e.Ws, e.d_omap, e.Cout, n_, slice,
+                                                      e.d_rtv_drop, e.size - 1, e.rtv_packed ? 1 : 0, e.Ws, e.d_omap, e.Cout, n_, slice,
                                                       oslice, table_ptr(e.out_off));
     return;
   }
@@ -1935,19 +1765,10 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     return ev.size() - 1;
   };
   const float* H = nullptr;
-  if ((need_hist_ || need_bucket_) && n_ > 0) {
+  if (need_hist_ && n_ > 0) {
     size_t h0 = 0;
     if (prof_) { h0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-    if (need_bucket_) {
-      // color-bucketed CSR for the leaf-pushed SpMMs; yields the histogram too
-      TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
-      dev::color_bucket<<<148 * 8, 256, 0, stream_>>>(
-          d_row_ptr_, d_col_, d_gcolors, d_row_order_, n_, plan_.k,
-          reinterpret_cast<int32_t*>(arena_ + colb_off_), reinterpret_cast<int64_t*>(arena_ + boff_off_),
-          need_hist_ ? table_ptr(hist_off_) : nullptr, dev::panel_width(plan_.k, 0), d_counter_);
-      ++launches_;
-      TCG_CUDA(cudaGetLastError());
-    } else if (!need_rooted_) {  // (with the rooted SpMM, bucket_rows writes it)
+    if (!need_rooted_) {  // (with the rooted SpMM, bucket_rows writes it)
       hist(d_gcolors, table_ptr(hist_off_));
     }
     if (prof_) { prof_->spmm.emplace_back(h0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
@@ -2031,12 +1852,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     } else if (!e.p_leaf && n_ > 0) {
       size_t p0 = 0;
       if (prof_) { p0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-      if (e.lspmm) {
-        const NodeExec* c = nullptr;
-        for (auto& x : exec_)
-          if (x.id == e.p) c = &x;
-        lspmm(e, c->p_leaf ? H : table_ptr(c->pp_off), table_ptr(e.pp_off));
-      } else if (e.rooted && e.pstream) {
+      if (e.rooted && e.pstream) {
         rooted_spmm(e, table_ptr(table_off_[e.p]), table_ptr(e.pp_off), d_colors, table_ptr(e.out_off));
       } else if (e.rooted) {
         rooted_spmm(e, table_ptr(table_off_[e.p]), table_ptr(e.pp_off), d_colors);
@@ -2046,7 +1862,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
       if (prof_) { prof_->spmm.emplace_back(p0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
       P = table_ptr(e.pp_off);
     }
-    if (e.skip_ema || e.virt) {
+    if (e.virt) {
       if (stats) { m.t1 = mark(); m.t2 = mark(); }
       marks.push_back(m);
       continue;
@@ -2349,12 +2165,12 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
       t.spmm_alg_bytes += count * (4 * nnz + 8 * (n + 1) + 8 * n * e.Cp);
       // columns actually gathered per neighbour; the rooted SpMMs never walk
       // a row's own-color neighbours (expected 1/k of them)
-      const int32_t gc = e.lspmm ? e.Cx : e.rooted ? e.rl_groups * e.rl_zw : e.Cp;
+      const int32_t gc = e.rooted ? e.rl_groups * e.rl_zw : e.Cp;
       const double walked = e.rooted ? nnz * (plan_.k - 1) / plan_.k : nnz;
       t.spmm_gathered_bytes += count * walked * 4.0 * (static_cast<double>(dev::num_panels(gc) - 1) * dev::kZ +
                                                         dev::last_panel_width(gc));
     }
-    if (e.virt || e.skip_ema) continue;  // no eMA executed: no eMA work claimed
+    if (e.virt) continue;  // no eMA executed: no eMA work claimed
     t.ema_launches += count;
     t.ema_alg_bytes += count * (4 * n * ((e.a_leaf ? 0 : e.Ca) + e.Cp) + (e.root ? 8 * n : 4 * n * e.Cs));
     t.ema_flops += count * 2 * n * e.Cs * static_cast<double>(B(e.size, e.sa));

@@ -37,13 +37,6 @@ struct NodeExec {
   void* d_groups = nullptr;      // dev::GroupDesc[ngroups], sorted by work
   void* d_blocks = nullptr;      // dev::BlockDesc[]
   int ngroups = 0;
-  // leaf-pushed SpMM (kernels.cuh spmm_bucket + lspmm_combine): P' of this node
-  // from the P' (X) of its active-leaf passive child, whose eMA is skipped
-  bool lspmm = false, skip_ema = false;
-  int Cx = 0, qchunk = 0;
-  int32_t* d_ins = nullptr;      // [k * Cx] column of (x u {c}) in P', or -1
-  int64_t q_off = -1;
-  size_t comb_smem = 0;
   int64_t out_off = -1;      // arena offset of M_s (root: fp64 n)
   int64_t pp_off = -1;       // arena offset of P' (passive internal child)
   size_t ema_smem = 0;
@@ -102,6 +95,7 @@ struct NodeExec {
   void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)
   bool rtv_pleaf = false;         // vertex-per-warp eMA over a leaf passive child (ema_rtv_pleaf)
   uint32_t* d_rtv_drop = nullptr; // [Ws][s-1] {A index of S' minus d | d << 16}
+  bool rtv_packed = false;        // d_rtv_drop packed as one uint4 per output (s-1 <= 6, k-1 <= 16)
   // active-leaf node with an unshared rooted SpMM: P' is never materialized --
   // each group's columns go to an n x Ct scratch table and are scattered into
   // the output (RR or RS) right after the group's last part (pstream_copy)
@@ -183,7 +177,6 @@ class Engine {
               tcg_node_stats* stats);
   void spmm(const float* X, float* Y, int64_t cols);
   void hist(const uint8_t* d_colors, float* H);
-  void lspmm(const NodeExec& e, const float* X, float* Pp);
   float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
   int64_t table_bytes(int64_t cols) const { return 4 * dev::table_floats(cols, n_); }
 
@@ -202,7 +195,6 @@ class Engine {
   uint64_t limit_override_ = 0;
   int64_t part_bytes_ = 64ll << 20;  // gather-source footprint per full-table SpMM part
   int rooted_part_mb_ = 0;           // > 0: split the rooted SpMM into colour-class parts of part_bytes_
-  int64_t persist_max_ = 0;          // > 0: pin each part's gather window in L2 (TCG_L2_PERSIST=MB)
 
   // sharding: this rank owns global rows [rows_[rank], rows_[rank+1]); tables
   // have n_ = nmax rows (the largest shard; pad rows have no neighbours);
@@ -271,8 +263,6 @@ class Engine {
   // arena + per-coloring buffers
   int64_t arena_bytes_ = 0;
   int64_t hist_off_ = -1;
-  bool need_bucket_ = false;         // some node uses the leaf-pushed SpMM
-  int64_t colb_off_ = -1, boff_off_ = -1;
   bool need_rooted_ = false;         // some node uses the rooted-compressed SpMM
   bool need_pair_ = false;           // some node uses the pair layout: per-coloring color-ordered segments
   int64_t pseg_off_ = -1, pkey_off_ = -1, pperm_off_ = -1, pcnt_off_ = -1;

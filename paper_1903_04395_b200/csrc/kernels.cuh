@@ -273,180 +273,6 @@ template <int kStageU>
 __device__ __forceinline__ void stage_tile(const float* __restrict__ T, int C, int32_t n, int64_t v0,
                                            float* dst);
 
-// --------------------------------------------- leaf-pushed SpMM (LSpMM)
-// When the passive child p of a node is (h, 1, h-1) -- an active leaf over X =
-// its own P' -- its table is M_p[u,S] = [c(u) in S] X[u, S minus c(u)], so
-//   (A M_p)[v,S] = sum_{c in S} Q_c[v, S minus c],   Q_c = A D_c X,
-// with D_c the color-c vertex selector.  The gather moves C(k,h-1) instead of
-// C(k,h) columns per neighbour, and M_p is never materialized.
-//
-// color_bucket: per coloring, stable-partition every CSR row by neighbour
-// color (warp per row, rows in degree order): bucketed ids `colb`, offsets
-// boff[v*(k+1)+c], and the exact neighbour color histogram H (the P' of a
-// leaf passive child) as a by-product.
-__global__ void __launch_bounds__(256)
-color_bucket(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ col,
-             const uint8_t* __restrict__ colors, const int32_t* __restrict__ row_order, int32_t n,
-             int k, int32_t* __restrict__ colb, int64_t* __restrict__ boff, float* __restrict__ H,
-             int hzw, int* __restrict__ next_row) {
-  const int lane = threadIdx.x & 31;
-  const unsigned lt = (1u << lane) - 1u;
-  for (;;) {
-    int ri = 0;
-    if (lane == 0) ri = atomicAdd(next_row, 1);
-    ri = __shfl_sync(0xffffffffu, ri, 0);
-    if (ri >= n) return;
-    const int32_t v = row_order[ri];
-    const int64_t b = row_ptr[v], e = row_ptr[v + 1];
-    unsigned cnt = 0;  // lane c: neighbours of color c
-    for (int64_t j = b; j < e; j += 32) {
-      const int c = j + lane < e ? colors[col[j + lane]] : 255;
-      for (int cc = 0; cc < k; ++cc) {
-        const unsigned m = __ballot_sync(0xffffffffu, c == cc);
-        if (lane == cc) cnt += __popc(m);
-      }
-    }
-    if (H && lane < hzw) H[static_cast<int64_t>(v) * hzw + lane] = lane < k ? static_cast<float>(cnt) : 0.f;
-    // exclusive scan of the counts over colors -> bucket starts
-    unsigned incl = cnt;
-    for (int o = 1; o < 32; o <<= 1) {
-      const unsigned y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    int64_t run = b + (incl - cnt);  // lane c: next free slot of bucket c
-    if (lane <= k) boff[static_cast<int64_t>(v) * (k + 1) + lane] = run;
-    for (int64_t j = b; j < e; j += 32) {
-      const bool ok = j + lane < e;
-      const int u = ok ? col[j + lane] : 0;
-      const int c = ok ? colors[u] : 31;
-      const unsigned same = __match_any_sync(0xffffffffu, c);
-      const int64_t slot = __shfl_sync(0xffffffffu, run, c) + __popc(same & lt);
-      if (ok) colb[slot] = u;
-      for (int cc = 0; cc < k; ++cc) {
-        const unsigned m = __ballot_sync(0xffffffffu, ok && c == cc);
-        if (lane == cc) run += __popc(m);
-      }
-    }
-  }
-}
-
-// Q_c[v, panel] = sum over the color-c bucket of row v of X[u, panel], for
-// the colors [c0, c0 + nc) of one chunk, over the whole-row schedule.  Blocks
-// are color-major, so all SMs gather color c's rows (~n/k rows of the panel,
-// L2-resident) at a time.  Rows split into several segments write fp64
-// partials per (color, slot), summed by spmm_fixup.
-template <int ZW>
-__global__ void __launch_bounds__(kSpmmWarps * 32)
-spmm_bucket(const Seg* __restrict__ segs, int64_t ntasks, int64_t blocks_per_color,
-            const int32_t* __restrict__ slot_row, const int32_t* __restrict__ colb,
-            const int64_t* __restrict__ boff, int k, int c0, const float* __restrict__ X,
-            float* __restrict__ Q, int64_t q_stride, double* __restrict__ partial, int nslots) {
-  constexpr int G = ZW / 4, SPW = 32 / G, R = 8;
-  const int lane = threadIdx.x & 31, g = lane / G, l = lane % G;
-  const int cl = static_cast<int>(blockIdx.x / blocks_per_color);
-  const int c = c0 + cl;
-  const int64_t task = static_cast<int64_t>(blockIdx.x % blocks_per_color) * kSpmmWarps + (threadIdx.x >> 5);
-  if (task >= ntasks) return;
-  const Seg s = segs[task * SPW + g];
-  int64_t lo = 0, hi = 0;
-  if (s.dst != kSkip) {
-    const int32_t v = s.dst >= 0 ? s.dst : slot_row[-1 - s.dst];
-    const int64_t bl = boff[static_cast<int64_t>(v) * (k + 1) + c], bh = boff[static_cast<int64_t>(v) * (k + 1) + c + 1];
-    lo = max(bl, s.e_begin);
-    hi = min(bh, s.e_begin + s.len);
-    if (hi < lo) hi = lo;
-  }
-  const int len = static_cast<int>(hi - lo);
-  const int maxlen = __reduce_max_sync(0xffffffffu, len);
-  const int32_t* cp = colb + lo;
-  const uint64_t pstream = policy_evict_first(), pkeep = policy_evict_last();
-  double a0 = 0, a1 = 0, a2 = 0, a3 = 0;
-  constexpr int NI = R / G > 0 ? R / G : 1;
-  int nxt[NI];
-#pragma unroll
-  for (int i = 0; i < NI; ++i) {
-    const int e = i * G + l;
-    nxt[i] = e < len ? ld_stream_i32(cp + e, pstream) : -1;
-  }
-  for (int t = 0; t < maxlen; t += R) {
-    int idx[NI];
-#pragma unroll
-    for (int i = 0; i < NI; ++i) {
-      idx[i] = nxt[i];
-      const int e = t + R + i * G + l;
-      nxt[i] = e < len ? ld_stream_i32(cp + e, pstream) : -1;
-    }
-    float4 vv[R];
-    int uu[R];
-#pragma unroll
-    for (int j = 0; j < R; ++j) uu[j] = __shfl_sync(0xffffffffu, idx[j / G], g * G + (j % G));
-#pragma unroll
-    for (int j = 0; j < R; ++j) vv[j] = ld_keep_f4(X + static_cast<int64_t>(uu[j] < 0 ? 0 : uu[j]) * ZW + l * 4, pkeep);
-#pragma unroll
-    for (int j = 0; j < R; ++j)
-      if (uu[j] < 0) vv[j] = make_float4(0, 0, 0, 0);
-#pragma unroll
-    for (int w = R / 2; w; w >>= 1)
-#pragma unroll
-      for (int j = 0; j < w; ++j) {
-        vv[j].x += vv[j + w].x; vv[j].y += vv[j + w].y; vv[j].z += vv[j + w].z; vv[j].w += vv[j + w].w;
-      }
-    a0 += vv[0].x; a1 += vv[0].y; a2 += vv[0].z; a3 += vv[0].w;
-  }
-  if (s.dst == kSkip) return;
-  if (s.dst >= 0) {
-    st_stream_f4(Q + cl * q_stride + static_cast<int64_t>(s.dst) * ZW + l * 4,
-                 make_float4(static_cast<float>(a0), static_cast<float>(a1), static_cast<float>(a2),
-                             static_cast<float>(a3)), pstream);
-  } else {
-    double* pp = partial + ((static_cast<int64_t>(cl) * nslots + (-1 - s.dst)) * ZW + l * 4);
-    reinterpret_cast<double2*>(pp)[0] = make_double2(a0, a1);
-    reinterpret_cast<double2*>(pp)[1] = make_double2(a2, a3);
-  }
-}
-
-// P'[v, S] (+)= sum_{c in chunk, c in S} Q_c[v, S minus c] for a 32-vertex
-// tile.  ins[c*Cx + x] = column of (set x) u {c} in P', or -1 if c is in x.
-// Colors are added in ascending order (deterministic).
-__global__ void __launch_bounds__(512)
-lspmm_combine(const float* __restrict__ Q, int64_t q_stride, int c0, int nc,
-              const int32_t* __restrict__ ins, int Cx, int Cp, int32_t n, float* __restrict__ Pp,
-              int first) {
-  extern __shared__ float smem[];
-  float* sP = smem;                    // [Cp][33]
-  float* sQ = smem + Cp * kSpitch;     // [Cx][33]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const int64_t v0 = static_cast<int64_t>(blockIdx.x) * kTileV;
-  if (first) {
-    for (int i = threadIdx.x; i < Cp * kSpitch; i += blockDim.x) sP[i] = 0.f;
-  } else {
-    stage_tile<1>(Pp, Cp, n, v0, sP);
-  }
-  for (int cl = 0; cl < nc; ++cl) {
-    __syncthreads();
-    stage_tile<4>(Q + cl * q_stride, Cx, n, v0, sQ);
-    __syncthreads();
-    const int32_t* im = ins + static_cast<int64_t>(c0 + cl) * Cx;
-    for (int x = warp; x < Cx; x += nw) {
-      const int d = __ldg(im + x);
-      if (d >= 0) sP[d * kSpitch + lane] += sQ[x * kSpitch + lane];
-    }
-  }
-  __syncthreads();
-  const int64_t v = v0 + lane;
-  if (v >= n) return;
-  for (int q = warp; q < (Cp + 7) / 8; q += nw) {
-    const int col0 = q * 8;
-    float r[8];
-#pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = col0 + j < Cp ? sP[(col0 + j) * kSpitch + lane] : 0.f;
-    const int zw = panel_width(Cp, col0 / kZ);
-    float* dst = Pp + static_cast<int64_t>(col0 / kZ) * n * kZ + v * zw + (col0 % kZ);
-    reinterpret_cast<float4*>(dst)[0] = make_float4(r[0], r[1], r[2], r[3]);
-    reinterpret_cast<float4*>(dst)[1] = make_float4(r[4], r[5], r[6], r[7]);
-  }
-}
-
 // ------------------------------------------ rooted-color compressed SpMM
 // (host.hpp RootedLayout).  Per coloring, every CSR row is re-ordered by
 // (part, neighbour color) and each entry packed as u | color << 27, so the

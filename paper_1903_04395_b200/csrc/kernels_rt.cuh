@@ -403,7 +403,7 @@ template <int kPleafV>
 __global__ void __launch_bounds__(256)
 ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
               const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap,
-              const uint8_t* __restrict__ colors, const uint32_t* __restrict__ drop, int sp, int Ws,
+              const uint8_t* __restrict__ colors, const uint32_t* __restrict__ drop, int sp, int packed, int Ws,
               const int32_t* __restrict__ omap, int Cout, int32_t n, int slice, int oslice, float* __restrict__ out) {
   extern __shared__ float smem[];
   __shared__ int cvs[kPleafV];
@@ -454,7 +454,7 @@ ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
       float acc[kPleafV];
 #pragma unroll
       for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = 0.f;
-      if (sp <= 6) {  // packed row: six 16-bit A indices + six 4-bit colours in one 16 B load
+      if (packed) {  // (s' <= 6, k - 1 <= 16) six 16-bit A indices + six 4-bit colours in one 16 B load
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(drop) + j);
         const uint32_t w[3] = {q.x, q.y, q.z};
 #pragma unroll

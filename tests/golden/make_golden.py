@@ -10,6 +10,13 @@ Outputs
   cfg1.npz         cfg1 graph CSR + per-vertex root counts seed 1 + totals seeds 1..10
   cfg2.npz         cfg2 totals seeds 1..2 + per-vertex root counts (seed 1) on a fixed vertex sample  [--big]
   cfg3.npz         cfg3 total seed 1 + per-vertex sample                                             [--big]
+  cfg3_full.npz    cfg3 seeds 1..3: totals + the WHOLE per-vertex root vector (float32)              [--r2]
+  cfg4t.npz        cfg4 template (k=15) on R-MAT scale 18 ef32 (.57,.19,.19,.05), seeds 1..2, full
+                   per-vertex (fp64): 261K-vertex graph with hub rows far above 1,024 neighbours    [--r2]
+  cfg5t.npz        cfg5 template (k=17) on R-MAT scale 16 ef100 (.45,.15,.15,.25), seed 1, full
+                   per-vertex (fp64)                                                                 [--r2]
+cfg2 seeds 1..10 are not stored: tests/test_parity_scale.py runs oracle/_ref on the GPU box's host
+(7-8 s per coloring) and compares the whole per-vertex vector.
 """
 from __future__ import annotations
 
@@ -38,7 +45,11 @@ CFG_TEMPLATES = {
 CFG_GRAPHS = {
     "cfg2": (20, 16 << 20, .57, .19, .19, .05, 1),
     "cfg3": (20, 100 << 20, .45, .15, .15, .25, 1),
+    # scaled-down graphs of the cfg4 / cfg5 shape: the full ones need 432 / 276 GB of fp64 tables
+    "cfg4t": (18, 32 << 18, .57, .19, .19, .05, 1),
+    "cfg5t": (16, 100 << 16, .45, .15, .15, .25, 1),
 }
+R2_TEMPLATES = {"cfg3_full": "cfg3", "cfg4t": "cfg4", "cfg5t": "cfg5"}
 
 
 def cfg1_edges(n=16384, seed=1):
@@ -204,11 +215,53 @@ def big_cfg(name, seeds):
                         **samples)
 
 
+def full_cfg(name, seeds, dtype):
+    """Whole per-vertex root vectors of the reference for several seeds (round-2 fixtures)."""
+    gname = "cfg3" if name == "cfg3_full" else name
+    t0 = time.time()
+    g = O.RefGraph.rmat(*CFG_GRAPHS[gname])
+    n, rp, cl = g.csr()
+    print(name, "graph", n, rp[-1], "maxdeg", int(np.diff(rp).max()), f"{time.time() - t0:.1f}s",
+          flush=True)
+    parents = CFG_TEMPLATES[R2_TEMPLATES[name]]
+    k, e = len(parents), eflat(parents)
+    out = {}
+    totals, secs = [], []
+    for s in seeds:
+        colors = np.zeros(n, np.uint8)
+        O.ref().ref_random_coloring(n, k, s, colors)
+        t0 = time.time()
+        total, pv = ref_run(g, k, e, 0, colors, workers=os.cpu_count())
+        secs.append(time.time() - t0)
+        print(name, "seed", s, repr(total), f"{secs[-1]:.1f}s", flush=True)
+        totals.append(total)
+        out[f"pv_seed{s}"] = pv.astype(dtype)
+        out[f"pv_sum_seed{s}"] = pv.sum()
+    np.savez_compressed(os.path.join(OUT, f"{name}.npz"), seeds=np.array(seeds),
+                        totals=np.array(totals), ref_seconds=np.array(secs), n=n, nnz=rp[-1],
+                        graph=np.array(CFG_GRAPHS[gname][:6]), graph_seed=CFG_GRAPHS[gname][6],
+                        parents=np.array(parents), pv_dtype=np.dtype(dtype).name,
+                        row_ptr_checksum=int(rp.sum() % (1 << 61)),
+                        col_checksum=int((cl.astype(np.int64) * (np.arange(cl.size) % 1000003)).sum()
+                                         % (1 << 61)), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--big", action="store_true", help="also cfg2 (and cfg3 with --cfg3)")
     ap.add_argument("--cfg3", action="store_true")
+    ap.add_argument("--r2", nargs="*", default=None,
+                    help="round-2 full per-vertex fixtures: cfg4t cfg5t cfg3_full (default all)")
     a = ap.parse_args()
+    if a.r2 is not None:
+        for name in a.r2 or ["cfg4t", "cfg5t", "cfg3_full"]:
+            if name == "cfg3_full":
+                full_cfg(name, [1, 2, 3], np.float32)
+            elif name == "cfg4t":
+                full_cfg(name, [1, 2], np.float64)
+            else:
+                full_cfg(name, [1], np.float64)
+        sys.exit(0)
     with open(os.path.join(OUT, "kats.json"), "w") as f:
         json.dump(kats(), f)
     cfg1()

@@ -171,3 +171,34 @@ def test_oracle_matches_reference_random_trees():
         assert list(p.dp_order)[:2 * k - 1] == dp.tolist()
         assert list(p.active_child)[:2 * k - 1] == ac.tolist()
         assert O.automorphisms(k, parents_to_edges(parents)) == R.ref_automorphisms(k, e)
+
+
+@needs_ref
+@pytest.mark.parametrize("steps", [1, 3, 7, 40])
+def test_reference_stepper_is_run_iteration(steps):
+    """bench.py --impl reference times ONE full coloring in K slices (ref_driver.cpp
+    RefStepper); the replay must be bit-identical to random_coloring + run_iteration
+    (engines.hpp:106-132) and execute every unit."""
+    g = O.RefGraph.rmat(11, 24 << 11, .45, .15, .15, .25, 3)
+    parents = CFG_TEMPLATES["cfg3"]
+    e = np.array(parents_to_edges(parents), np.int32).reshape(-1)
+    want, _, node_sec = O.ref_run_iteration_stats(g, len(parents), e, 0, 5, 4)
+    st = O.RefStepper(g, len(parents), e, 0, 5, 4, steps)
+    for i in range(steps):
+        st.run(i)
+    got, node_stats, extra = st.finish()
+    assert got == want
+    assert node_stats.shape == (len(node_sec), 3)
+    # every internal node ran its SpMM batches and eMA pairs
+    assert np.all((node_stats[:, 1] > 0) == (node_stats[:, 2] > 0))
+    assert int(extra[1]) > steps
+
+
+@needs_ref
+def test_reference_stepper_refuses_unfinished():
+    g = O.RefGraph.rmat(9, 8 << 9, .57, .19, .19, .05, 1)
+    e = np.array(parents_to_edges(CFG_TEMPLATES["cfg1"]), np.int32).reshape(-1)
+    st = O.RefStepper(g, 5, e, 0, 1, 2, 4)
+    st.run(0)
+    with pytest.raises(RuntimeError):
+        st.finish()
