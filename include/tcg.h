@@ -176,6 +176,15 @@ int tcg_node_table(tcg_ctx* ctx, int node_id, int which, double* out);
 /* Kernel-level hook: Y = A X for a vertex-major fp32 n x C host matrix,
  * through the production SpMM kernel (la_kernels.hpp:83-102 semantics). */
 int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y);
+/* Kernel-level hook of the PRODUCTION rooted SpMM of one DP node (the
+ * la_kernels.hpp:83-102 SpMM as every coloring runs it): x = a passive table
+ * M, vertex-major fp32 n x C(k,s), rooted (M[u,S] = 0 unless colors[u] is in
+ * S); it goes through the per-coloring colour bucketing, the k-colour slot
+ * layout (pair = 0) or the pair layout (pair = 1: per-row-colour copies), the
+ * spmm_rooted kernel and the split-row fixup.  y (n x C(k,s)) receives
+ * Y[v,T] = sum over u in N(v) of M[u,T] wherever T misses colors[v] -- the
+ * columns a consumer reads -- and 0 elsewhere.  2 <= k <= 20, 1 <= s < k. */
+int tcg_spmm_rooted(tcg_ctx* ctx, int k, int s, int pair, const uint8_t* colors, const float* x, float* y);
 /* Test hook: override the rejection threshold (UINT64_MAX/k)*k of
  * Rng::below (rng.hpp:21-27); 0 restores the reference value. */
 int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit);

@@ -89,6 +89,7 @@ _SIGS = {
     "tcg_estimate": (C.c_int, [vp, u64, C.c_int, vp, P(dbl), P(dbl), vp]),
     "tcg_node_table": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "tcg_spmm": (C.c_int, [vp, vp, C.c_int, vp]),
+    "tcg_spmm_rooted": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
     "tcg_set_rejection_limit": (C.c_int, [vp, u64]),
     "tcg_time_colorings": (C.c_int, [vp, u64, C.c_int, C.c_int, vp, P(TcgTiming)]),
     "tcg_kernel_launches": (i64, [vp]),

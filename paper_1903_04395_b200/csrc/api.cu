@@ -324,6 +324,16 @@ int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y) {
   });
 }
 
+int tcg_spmm_rooted(tcg_ctx* ctx, int k, int s, int pair, const uint8_t* colors, const float* x, float* y) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(colors, "colors");
+    need(x, "x");
+    need(y, "y");
+    ctx->eng->spmm_rooted_host(k, s, pair != 0, colors, x, y);
+  });
+}
+
 int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit) {
   return guarded([&] {
     need(ctx, "ctx");

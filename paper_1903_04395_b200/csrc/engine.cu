@@ -6,6 +6,7 @@
 
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
+#include <cub/device/device_segmented_sort.cuh>
 
 #include <algorithm>
 #include <chrono>
@@ -204,7 +205,7 @@ PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<in
 }
 }  // namespace
 
-Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
+Engine::Engine(const tcg_config& cfg, cudaStream_t shared_stream) : cfg_(cfg) {
   int ndev = 0;
   TCG_CUDA(cudaGetDeviceCount(&ndev));
   if (cfg.device < 0 || cfg.device >= ndev)
@@ -224,7 +225,13 @@ Engine::Engine(const tcg_config& cfg) : cfg_(cfg) {
   // B200 that costs more than the L2 misses of the unsplit gather source
   // (cfg3 49.9 -> 47.9 ms, cfg4 1666 -> 1049 ms).
   if (const char* e = std::getenv("TCG_ROOTED_PARTS")) rooted_part_mb_ = std::atoi(e);
-  TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  if (const char* e = std::getenv("TCG_HOT_MB")) hot_mb_ = std::atoi(e);
+  if (shared_stream) {
+    stream_ = shared_stream;
+    own_stream_ = false;
+  } else {
+    TCG_CUDA(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking));
+  }
   TCG_CUDA(cudaMalloc(&d_scalars_, 64));
   TCG_CUDA(cudaMalloc(&d_seeds_, 1024 * sizeof(uint64_t)));
 }
@@ -237,7 +244,8 @@ Engine::~Engine() {
   dfree(d_scalars_);
   dfree(d_seeds_);
   dfree(d_colors_);
-  if (stream_) cudaStreamDestroy(stream_);
+  batch_.reset();
+  if (stream_ && own_stream_) cudaStreamDestroy(stream_);
 }
 
 void Engine::free_graph_buffers() {
@@ -253,6 +261,18 @@ void Engine::free_graph_buffers() {
   dfree(d_tile_tot_);
   tile_tot_cap_ = 0;
   dfree(d_counter_);
+  dfree(d_perm_);
+  dfree(d_inv_);
+  perm_cap_ = inv_cap_ = 0;
+  dfree(d_rp2_);
+  dfree(d_col2_);
+  rp2_cap_ = col2_cap_ = 0;
+  dfree(rl_buf_);
+  rl_cap_ = -1;
+  dfree(d_colors_rl_);
+  colors_rl_cap_ = 0;
+  dfree(d_pv_out_);
+  pv_out_cap_ = 0;
 }
 
 void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the next graph)
@@ -270,6 +290,8 @@ void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the n
   host_row_ptr_.clear();
   host_col_.clear();
   host_col_.shrink_to_fit();
+  relabeled_ = false;
+  rows_sorted_ = true;
   n_ = -1;
 }
 
@@ -409,13 +431,30 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
     TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
     col_cap_ = std::max<int64_t>(nnz_, 1);
   }
-  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyHostToDevice, stream_));
-  if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyHostToDevice, stream_));
+  // (cudaMemcpyDefault: host buffers from the caller, device buffers from a batch union)
+  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyDefault, stream_));
+  if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyDefault, stream_));
   if (validate && nnz_) {
     TCG_CUDA(cudaMemsetAsync(reinterpret_cast<int*>(d_scalars_ + 4), 0, sizeof(int), stream_));
     dev::validate_csr<<<148 * 8, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, reinterpret_cast<int*>(d_scalars_ + 4));
     ++launches_;
   }
+  if (validate && nnz_) {  // (before the relabeling reads the ids)
+    int bad = 0;
+    copy_sync(&bad, reinterpret_cast<int*>(d_scalars_ + 4), sizeof(int), cudaMemcpyDeviceToHost);
+    if (bad) {
+      const int32_t n = n_;
+      release_graph();
+      if (bad == 1) throw invalid_argument("CSR column out of range [0, " + std::to_string(n) + ") or self-loop");
+      throw invalid_argument("CSR row not strictly ascending");
+    }
+  }
+  static const int relabel_mode = [] {
+    const char* s = std::getenv("TCG_RELABEL");
+    return s ? std::atoi(s) : 1;
+  }();
+  if (relabel_mode && !no_relabel_ && !sharded() && n_ > 0) relabel_device();
+  ++graph_gen_;
   if (timing) TCG_CUDA(cudaStreamSynchronize(stream_));
   const auto t1 = now();
   // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
@@ -432,22 +471,125 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
   ensure_tile_tot(ntiles);
   TCG_CUDA(cudaStreamSynchronize(stream_));
-  if (validate && nnz_) {
-    int bad = 0;
-    copy_sync(&bad, reinterpret_cast<int*>(d_scalars_ + 4), sizeof(int), cudaMemcpyDeviceToHost);
-    if (bad) {
-      const int32_t n = n_;
-      release_graph();
-      if (bad == 1) throw invalid_argument("CSR column out of range [0, " + std::to_string(n) + ") or self-loop");
-      throw invalid_argument("CSR row not strictly ascending");
-    }
-  }
   const auto t4 = now();
   if (have_template_) plan_arena();
   if (timing)
     std::fprintf(stderr, "[tcg timing] set_graph: h2d+validate %.1f, device prep %.1f, sync %.1f, plan %.1f ms\n",
                  ms(t0, t1), ms(t2, t3), ms(t3, t4), ms(t4, now()));
   tables_valid_ = false;
+}
+
+void* Engine::cub_tmp(size_t need) {
+  if (need > gp_tmp_cap_) {
+    dfree(gp_tmp_);
+    gp_tmp_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&gp_tmp_, need));
+    gp_tmp_cap_ = need;
+  }
+  return gp_tmp_;
+}
+
+// Degree-aware relabeling with isolated-vertex compaction, on the device
+// (kernels_graph.cuh relabel_*): the CSR in d_row_ptr_ / d_col_ is replaced
+// by the CSR of the live vertices in descending-degree order, each row's new
+// ids sorted ascending (a segmented sort), so the graph invariants hold for
+// the schedules built next.  Counts of the caller's vertex v are those of
+// internal row inv[v]; isolated vertices count 0 for every k >= 2.
+void Engine::relabel_device() {
+  const int64_t n = n_, nnz = nnz_;
+  auto grow = [&](auto*& p, int64_t& cap, int64_t need, size_t elem) {
+    if (cap >= need) return;
+    dfree(p);
+    cap = 0;
+    TCG_CUDA(cudaMalloc(&p, elem * static_cast<size_t>(std::max<int64_t>(need, 1))));
+    cap = need;
+  };
+  grow(d_perm_, perm_cap_, n, sizeof(int32_t));
+  grow(d_inv_, inv_cap_, n, sizeof(int32_t));
+  grow(d_rp2_, rp2_cap_, n + 1, sizeof(int64_t));
+  grow(d_col2_, col2_cap_, nnz, sizeof(int32_t));
+  const int64_t o_key = 0, o_key2 = (4 * n + 255) / 256 * 256, o_ids = 2 * o_key2, o_deg = 3 * o_key2,
+                o_cnt = o_deg + (8 * (n + 1) + 255) / 256 * 256, need = o_cnt + 256;
+  if (need > rl_cap_) {
+    dfree(rl_buf_);
+    rl_cap_ = -1;
+    TCG_CUDA(cudaMalloc(&rl_buf_, need));
+    rl_cap_ = need;
+  }
+  uint32_t* key = reinterpret_cast<uint32_t*>(rl_buf_ + o_key);
+  uint32_t* key2 = reinterpret_cast<uint32_t*>(rl_buf_ + o_key2);
+  int32_t* ids = reinterpret_cast<int32_t*>(rl_buf_ + o_ids);
+  int64_t* deg = reinterpret_cast<int64_t*>(rl_buf_ + o_deg);
+  int32_t* cnt = reinterpret_cast<int32_t*>(rl_buf_ + o_cnt);
+  TCG_CUDA(cudaMemsetAsync(cnt, 0, sizeof(int32_t), stream_));
+  const unsigned g1 = static_cast<unsigned>((n + 255) / 256);
+  dev::relabel_keys<<<g1, 256, 0, stream_>>>(d_row_ptr_, n_, key, ids, cnt);
+  size_t b = 0;
+  TCG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, b, key, key2, ids, d_perm_, static_cast<int>(n), 0, 32, stream_));
+  TCG_CUDA(cub::DeviceRadixSort::SortPairs(cub_tmp(b), b, key, key2, ids, d_perm_, static_cast<int>(n), 0, 32, stream_));
+  int32_t nact = 0;
+  copy_sync(&nact, cnt, sizeof(int32_t), cudaMemcpyDeviceToHost);
+  TCG_CUDA(cudaMemsetAsync(d_inv_, 0xFF, sizeof(int32_t) * n, stream_));
+  dev::relabel_inverse<<<static_cast<unsigned>((nact + 1 + 255) / 256), 256, 0, stream_>>>(d_row_ptr_, d_perm_, nact, d_inv_, deg);
+  b = 0;
+  TCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, deg, d_rp2_, static_cast<int>(nact + 1), stream_));
+  TCG_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp(b), b, deg, d_rp2_, static_cast<int>(nact + 1), stream_));
+  if (nnz > 0) {
+    dev::relabel_fill<<<148 * 8, 256, 0, stream_>>>(d_row_ptr_, d_col_, d_perm_, d_inv_, d_rp2_, nact, d_col2_);
+    std::swap(d_col_, d_col2_);
+    std::swap(col_cap_, col2_cap_);
+  }
+  std::swap(d_row_ptr_, d_rp2_);
+  std::swap(row_ptr_cap_, rp2_cap_);
+  // (a row's new ids are in the order of its old ids: only the vertex-range
+  // part schedules of the full-table SpMM need ascending rows -- sort_rows)
+  rows_sorted_ = nnz == 0;
+  TCG_CUDA(cudaGetLastError());
+  n_ = nact;
+  nsrc_ = nact;
+  relabeled_ = true;
+}
+
+// Rows ascending (the vertex-range parts of the full-table SpMM cut rows by
+// id): a segmented sort of the relabeled rows, on first need.
+void Engine::sort_rows() {
+  if (rows_sorted_) return;
+  size_t b = 0;
+  TCG_CUDA(cub::DeviceSegmentedSort::SortKeys(nullptr, b, d_col_, d_col2_, static_cast<int>(nnz_), n_, d_row_ptr_,
+                                              d_row_ptr_ + 1, stream_));
+  TCG_CUDA(cub::DeviceSegmentedSort::SortKeys(cub_tmp(b), b, d_col_, d_col2_, static_cast<int>(nnz_), n_, d_row_ptr_,
+                                              d_row_ptr_ + 1, stream_));
+  std::swap(d_col_, d_col2_);
+  std::swap(col_cap_, col2_cap_);
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+  host_col_.clear();
+  rows_sorted_ = true;
+}
+
+std::vector<int32_t> Engine::host_perm() {
+  std::vector<int32_t> p(static_cast<size_t>(std::max(n_, 0)));
+  if (relabeled_ && n_ > 0) copy_sync(p.data(), d_perm_, sizeof(int32_t) * n_, cudaMemcpyDeviceToHost);
+  else for (int32_t i = 0; i < n_; ++i) p[i] = i;
+  return p;
+}
+
+// per-vertex fp64 values of the internal rows -> caller order (host), 0 for
+// isolated vertices; enqueued on stream_ (the caller synchronizes)
+void Engine::unpermute_to_host(const double* d_internal, double* host) {
+  if (!relabeled_) {
+    TCG_CUDA(cudaMemcpyAsync(host, d_internal, sizeof(double) * n_, cudaMemcpyDeviceToHost, stream_));
+    return;
+  }
+  if (pv_out_cap_ < nglob_) {
+    dfree(d_pv_out_);
+    pv_out_cap_ = 0;
+    TCG_CUDA(cudaMalloc(&d_pv_out_, sizeof(double) * std::max<int64_t>(nglob_, 1)));
+    pv_out_cap_ = nglob_;
+  }
+  TCG_CUDA(cudaMemsetAsync(d_pv_out_, 0, sizeof(double) * nglob_, stream_));
+  if (n_ > 0)
+    dev::scatter_rows_f64<<<static_cast<unsigned>((n_ + 255) / 256), 256, 0, stream_>>>(d_internal, d_perm_, n_, d_pv_out_);
+  TCG_CUDA(cudaMemcpyAsync(host, d_pv_out_, sizeof(double) * nglob_, cudaMemcpyDeviceToHost, stream_));
 }
 
 // Whole-row segment schedule (sched_[1]), degree order and hub-row chunks of
@@ -588,6 +730,7 @@ void Engine::prep_graph_device() {
 // Vertex-range part schedules for the full-table SpMM (P parts per panel).
 void Engine::ensure_schedules(int P) {
   if (sched_.count(P)) return;
+  if (P > 1) sort_rows();
   if (host_row_ptr_.empty()) {
     host_row_ptr_.resize(static_cast<size_t>(n_) + 1);
     copy_sync(host_row_ptr_.data(), d_row_ptr_, sizeof(int64_t) * (n_ + 1), cudaMemcpyDeviceToHost);
@@ -801,6 +944,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   }
   TCG_CUDA(cudaStreamSynchronize(stream_));
   have_template_ = true;
+  ++tpl_gen_;
   if (n_ >= 0) plan_arena();
   tables_valid_ = false;
 }
@@ -1164,6 +1308,9 @@ void Engine::plan_arena() {
     int64_t limit = static_cast<int64_t>(fr) + (arena_ ? arena_alloc_ : 0) - partial_bytes_ - (3ll << 30);
     if (cfg_.memory_budget > 0) limit = std::min<int64_t>(limit, cfg_.memory_budget);
     if (arena_bytes_ > limit) plan_arena_once(true);
+    if (std::getenv("TCG_VERBOSE"))
+      std::fprintf(stderr, "[tcg] plan: free %.2f GB, limit %.2f GB, arena %.2f GB, partial %.2f GB, streamed %d\n",
+                   fr / 1e9, limit / 1e9, arena_bytes_ / 1e9, partial_bytes_ / 1e9, arena_bytes_ > limit ? -1 : 0);
   }
 }
 
@@ -1522,6 +1669,7 @@ void Engine::spmm(const float* X, float* Y, int64_t cols) {
 // M_p to its color-rooted slots, then one pass per (group, part) over the
 // (part, color)-sorted rows, each producing the group's P' columns.
 void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out) {
+  const int k = e.slot_K + (e.pair ? 1 : 0);
   const int zw = e.rl_zw, G = e.rl_groups;
   const float* X = rooted_ema_ ? M : table_ptr(e.ct_off);
   int64_t xstride = 0;  // pair layout: floats between the copies of two row colors
@@ -1537,7 +1685,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const size_t smem = static_cast<size_t>(4) * 32 * (wx + 1);
     TCG_CUDA(cudaFuncSetAttribute(dev::pair_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
     dev::pair_expand<<<static_cast<unsigned>((n_ + 31) / 32), 256, smem, stream_>>>(M, wx, d_colors, vpx ? e.d_xmap_v : e.d_xmap,
-                                                                                      plan_.k, G, zw, n_, cp);
+                                                                                      k, G, zw, n_, cp);
     ++launches_;
     X = cp;
     xstride = static_cast<int64_t>(G) * n_ * zw;
@@ -1585,11 +1733,19 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
       const unsigned blocks = static_cast<unsigned>((ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps);
       const int first = q == 0 ? 1 : 0;
       int part = q;
+      // L2 policy of the gathers: the first hot_rows rows of the (relabeled,
+      // degree-ordered) source evict_last, the rest evict_first
+      uint32_t hot = hot_packed_;
+      if (hot_mb_ >= 0) {
+        const int64_t rows = (static_cast<int64_t>(hot_mb_) << 20) / (4 * zw);
+        hot = rows >= (int64_t{1} << (32 - dev::kColorBits)) ? 0xFFFFFFFFu : static_cast<uint32_t>(rows) << dev::kColorBits;
+      }
       void* args[] = {const_cast<dev::Seg**>(&segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
                       const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
                       const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
                       const_cast<int*>(&fpad), const_cast<int32_t*>(&Cst), &n_, &Pp, &d_partial_,
-                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride, const_cast<int*>(&e.slot_K)};
+                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride, const_cast<int*>(&e.slot_K),
+                      &hot};
       TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {
@@ -1745,9 +1901,67 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   }
 }
 
+// Per coloring: every row stably sorted by neighbour colour (rotated order,
+// packed entries, part cuts) for the rooted SpMMs, the neighbour colour
+// histogram hf (nullable) as a by-product, and -- for pair-layout SpMMs --
+// the whole-row segments re-ordered by row colour.
+void Engine::bucket_coloring(const uint8_t* d_gcolors, const uint8_t* d_colors, int k, float* hf, bool pair) {
+  TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
+  const size_t smem = sizeof(int) * 8 * k;
+  uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
+  int64_t* cuts = reinterpret_cast<int64_t*>(arena_ + rcut_off_);
+  const int hzw = dev::panel_width(k, 0);
+  if (nlong_ > 0) {  // hub rows: chunked over many CTAs
+    int* ccnt = reinterpret_cast<int*>(arena_ + lcnt_off_);
+    dev::bucket_long_count<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
+                                                                                   d_colors, k, ccnt);
+    dev::bucket_long_scan<<<static_cast<unsigned>((nlong_ + 7) / 8), 256, 0, stream_>>>(
+        d_lchunks_, d_lfirst_, d_row_ptr_, d_colors, nlong_, k, rooted_parts_, ccnt, cuts, hf, hzw);
+    dev::bucket_long_scatter<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
+                                                                                     d_colors, k, ccnt, rc);
+    launches_ += 3;
+  }
+  dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nlong_, nsmall_,
+                                                   k, rooted_parts_, rc, cuts, hf, hzw);
+  ++launches_;
+  if (nsmall_ < n_) {
+    dev::bucket_small<<<static_cast<unsigned>((n_ - nsmall_ + 255) / 256), 256, 0, stream_>>>(
+        d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nsmall_, n_, k, rooted_parts_, rc, cuts, hf, hzw);
+    ++launches_;
+  }
+  if (pair) {  // whole-row segments re-ordered by row color (stable)
+    const PartSchedule& ps = sched_.at(1)[0];
+    const int64_t nseg = ps.nseg_padded;
+    const int nchunks = static_cast<int>((nseg + dev::kVsChunk - 1) / dev::kVsChunk);
+    uint8_t* keys = reinterpret_cast<uint8_t*>(arena_ + pkey_off_);
+    int* pcnt = reinterpret_cast<int*>(arena_ + pcnt_off_);
+    int32_t* perm = reinterpret_cast<int32_t*>(arena_ + pperm_off_);
+    dev::seg_keys<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(ps.d_segs, nseg, ps.d_slot_row, d_colors,
+                                                                                 k, keys);
+    dev::vsort_count<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), k + 1, pcnt);
+    dev::vsort_scan<<<1, 1024, 0, stream_>>>(pcnt, nchunks, k + 1, nullptr, 0);
+    dev::vsort_scatter<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), k + 1, pcnt, perm);
+    dev::seg_gather<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(
+        ps.d_segs, perm, nseg, reinterpret_cast<dev::Seg*>(arena_ + pseg_off_));
+    launches_ += 5;
+  }
+  TCG_CUDA(cudaGetLastError());
+}
+
 // ---------------------------------------------------------------- one DP
 void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_acc,
                     tcg_node_stats* stats) {
+  if (relabeled_ && n_ > 0) {  // the caller's vertex order -> internal rows
+    if (colors_rl_cap_ < n_) {
+      dfree(d_colors_rl_);
+      colors_rl_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&d_colors_rl_, n_));
+      colors_rl_cap_ = n_;
+    }
+    dev::permute_colors<<<static_cast<unsigned>((n_ + 255) / 256), 256, 0, stream_>>>(d_colors_in, d_perm_, n_, d_colors_rl_);
+    ++launches_;
+    d_colors_in = d_colors_rl_;
+  }
   // d_colors: colors of this context's rows (eMA); d_gcolors: by gather id
   const uint8_t* d_colors = d_colors_in;
   const uint8_t* d_gcolors = d_colors_in;
@@ -1778,47 +1992,8 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     // (part, color)-sorted packed rows for the rooted SpMMs of this coloring
     size_t b0 = 0;
     if (prof_) { b0 = prof_->used; TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
-    TCG_CUDA(cudaMemsetAsync(d_counter_, 0, sizeof(int), stream_));
-    const size_t smem = sizeof(int) * 8 * plan_.k;
-    uint32_t* rc = reinterpret_cast<uint32_t*>(arena_ + rcol_off_);
-    int64_t* cuts = reinterpret_cast<int64_t*>(arena_ + rcut_off_);
     // the bucketing counts ARE the neighbour color histogram: fused
-    float* hf = need_hist_ ? table_ptr(hist_off_) : nullptr;
-    const int hzw = dev::panel_width(plan_.k, 0);
-    if (nlong_ > 0) {  // hub rows: chunked over many CTAs
-      int* ccnt = reinterpret_cast<int*>(arena_ + lcnt_off_);
-      dev::bucket_long_count<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
-                                                                                     d_colors, plan_.k, ccnt);
-      dev::bucket_long_scan<<<static_cast<unsigned>((nlong_ + 7) / 8), 256, 0, stream_>>>(
-          d_lchunks_, d_lfirst_, d_row_ptr_, d_colors, nlong_, plan_.k, rooted_parts_, ccnt, cuts, hf, hzw);
-      dev::bucket_long_scatter<<<static_cast<unsigned>(nlchunks_), 256, 0, stream_>>>(d_lchunks_, d_row_ptr_, d_col_, d_gcolors,
-                                                                                       d_colors, plan_.k, ccnt, rc);
-      launches_ += 3;
-    }
-    dev::bucket_rows<<<148 * 8, 256, smem, stream_>>>(d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nlong_, nsmall_,
-                                                     plan_.k, rooted_parts_, rc, cuts, hf, hzw);
-    ++launches_;
-    if (nsmall_ < n_) {
-      dev::bucket_small<<<static_cast<unsigned>((n_ - nsmall_ + 255) / 256), 256, 0, stream_>>>(
-          d_row_ptr_, d_col_, d_gcolors, d_colors, d_row_order_, nsmall_, n_, plan_.k, rooted_parts_, rc, cuts, hf, hzw);
-      ++launches_;
-    }
-    if (need_pair_) {  // whole-row segments re-ordered by row color (stable)
-      const PartSchedule& ps = sched_.at(1)[0];
-      const int64_t nseg = ps.nseg_padded;
-      const int nchunks = static_cast<int>((nseg + dev::kVsChunk - 1) / dev::kVsChunk);
-      uint8_t* keys = reinterpret_cast<uint8_t*>(arena_ + pkey_off_);
-      int* pcnt = reinterpret_cast<int*>(arena_ + pcnt_off_);
-      int32_t* perm = reinterpret_cast<int32_t*>(arena_ + pperm_off_);
-      dev::seg_keys<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(ps.d_segs, nseg, ps.d_slot_row, d_colors,
-                                                                                   plan_.k, keys);
-      dev::vsort_count<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), plan_.k + 1, pcnt);
-      dev::vsort_scan<<<1, 1024, 0, stream_>>>(pcnt, nchunks, plan_.k + 1, nullptr, 0);
-      dev::vsort_scatter<<<nchunks, 256, 0, stream_>>>(keys, static_cast<int32_t>(nseg), plan_.k + 1, pcnt, perm);
-      dev::seg_gather<<<static_cast<unsigned>((nseg + 255) / 256), 256, 0, stream_>>>(
-          ps.d_segs, perm, nseg, reinterpret_cast<dev::Seg*>(arena_ + pseg_off_));
-      launches_ += 5;
-    }
+    bucket_coloring(d_gcolors, d_colors, plan_.k, need_hist_ ? table_ptr(hist_off_) : nullptr, need_pair_);
     TCG_CUDA(cudaGetLastError());
     if (prof_) { prof_->spmm.emplace_back(b0, prof_->used); TCG_CUDA(cudaEventRecord(prof_->get(), stream_)); }
   }
@@ -1933,20 +2108,13 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
     if (stats) m.t2 = mark();
     marks.push_back(m);
   }
-  const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
-  if (n_ > 0 && !exec_.empty()) {
-    if (rooted_ema_ && exec_.back().rt_vtx)  // per-vertex values only
-      dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
-                                                n_, d_total);
-    else if (rooted_ema_)
-      dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, max_tiles_, d_total);
-    else if (exec_.back().vtx)  // vertex-per-CTA root wrote per-vertex values only
-      dev::root_reduce<<<1, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
-                                                n_, d_total);
-    else
-      dev::root_reduce<<<1, 1024, 0, stream_>>>(d_tile_tot_, ntiles, d_total);
+  if (n_ > 0 && !exec_.empty() && d_total) {
+    // fixed-shape fp64 sum of the per-vertex root counts (internal row order;
+    // one segment per copy when this is a batch engine)
+    dev::root_reduce<<<batch_copies_, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
+                                                          n_ / batch_copies_, d_total);
     ++launches_;
-  } else {
+  } else if (d_total) {
     TCG_CUDA(cudaMemsetAsync(d_total, 0, sizeof(double), stream_));
   }
   TCG_CUDA(cudaGetLastError());
@@ -1997,8 +2165,7 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
     } else if (sharded()) {
       gather_per_vertex(reinterpret_cast<const double*>(arena_ + exec_.back().out_off), per_vertex);
     } else {
-      TCG_CUDA(cudaMemcpyAsync(per_vertex, arena_ + exec_.back().out_off, sizeof(double) * n_,
-                               cudaMemcpyDeviceToHost, stream_));
+      unpermute_to_host(reinterpret_cast<const double*>(arena_ + exec_.back().out_off), per_vertex);
     }
   }
   if (cfg_.flags & TCG_KEEP_TABLES) {
@@ -2052,8 +2219,12 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
       const int c = std::min(chunk, iterations - i0);
       for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
       gen_colors(seeds.data(), c, d_colors_);
-      for (int j = 0; j < c; ++j)
-        run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, d_acc, nullptr);
+      for (int j = 0; j < c;) {
+        const int B = pick_batch(c - j);
+        if (B > 1) run_batch(d_colors_ + static_cast<int64_t>(j) * nglob_, B, d_totals + i0 + j, d_acc);
+        else run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, d_acc, nullptr);
+        j += B;
+      }
     }
     if (timing) {
       const double q = since();
@@ -2067,7 +2238,7 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
       if (sharded()) {
         gather_per_vertex(d_acc, acc.data());
       } else {
-        TCG_CUDA(cudaMemcpyAsync(acc.data(), d_acc, sizeof(double) * n_, cudaMemcpyDeviceToHost, stream_));
+        unpermute_to_host(d_acc, acc.data());
       }
     }
     TCG_CUDA(cudaStreamSynchronize(stream_));
@@ -2094,6 +2265,86 @@ void Engine::estimate(uint64_t seed, int iterations, double* totals, double* est
   }
   if (timing) std::fprintf(stderr, "[tcg timing] estimate: total %.1f ms\n", since());
   tables_valid_ = false;
+}
+
+// ------------------------------------------------------- batched colorings
+// Batch size for `count` pending colorings: small graphs only (the union of
+// B copies <= 2^20 rows and 2^26 entries, its tables <= 8 GB), B <= 64.
+int Engine::pick_batch(int count) const {
+  static const int mode = [] {
+    const char* s = std::getenv("TCG_BATCH");
+    return s ? std::atoi(s) : 1;
+  }();
+  if (!mode || count < 2 || sharded() || n_ <= 0 || exec_.empty() || batch_copies_ > 1) return 1;
+  int64_t B = std::min<int64_t>({count, 64, (int64_t{1} << 20) / n_, (int64_t{1} << 26) / std::max<int64_t>(nnz_, 1),
+                                 (int64_t{8} << 30) / std::max<int64_t>(arena_bytes_ + partial_bytes_, 1)});
+  return B >= 2 ? static_cast<int>(B) : 1;
+}
+
+// The engine over the B-fold union of this engine's (internal) graph, same
+// template, same stream; rebuilt when the graph, the template or B changes.
+Engine* Engine::batch_engine(int B) {
+  if (batch_ && batch_copies_ == 1 && batch_->batch_copies_ == B && batch_graph_gen_ == graph_gen_ &&
+      batch_tpl_gen_ == tpl_gen_)
+    return batch_.get();
+  batch_.reset();
+  tcg_config c = cfg_;
+  c.flags &= ~TCG_KEEP_TABLES;
+  c.memory_budget = 0;
+  auto be = std::make_unique<Engine>(c, stream_);
+  be->no_relabel_ = true;
+  be->batch_copies_ = B;
+  be->limit_override_ = limit_override_;
+  const int64_t nU = static_cast<int64_t>(n_) * B, eU = nnz_ * B;
+  int64_t* rpU = nullptr;
+  int32_t* colU = nullptr;
+  try {
+    TCG_CUDA(cudaMalloc(&rpU, sizeof(int64_t) * (nU + 1)));
+    TCG_CUDA(cudaMalloc(&colU, sizeof(int32_t) * std::max<int64_t>(eU, 1)));
+    dev::union_graph<<<148 * 4, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, nnz_, B, rpU, colU);
+    TCG_CUDA(cudaGetLastError());
+    std::vector<int32_t> edges;
+    for (const auto& pr : tpl_.edges) {
+      edges.push_back(pr.first);
+      edges.push_back(pr.second);
+    }
+    be->set_template(tpl_.k, edges.data(), tpl_.root);
+    be->set_graph_ptrs(static_cast<int32_t>(nU), rpU, colU, false);
+    be->ensure_arena();
+  } catch (...) {
+    dfree(rpU);
+    dfree(colU);
+    throw;
+  }
+  TCG_CUDA(cudaStreamSynchronize(stream_));
+  dfree(rpU);
+  dfree(colU);
+  batch_ = std::move(be);
+  batch_graph_gen_ = graph_gen_;
+  batch_tpl_gen_ = tpl_gen_;
+  return batch_.get();
+}
+
+// B colorings (caller order) as one DP over the union: the copies' totals
+// (fixed-shape per-copy reductions == run_dp's) and per-vertex accumulation
+// in coloring order, so results equal B separate run_dp calls bit for bit.
+void Engine::run_batch(const uint8_t* d_colors, int B, double* d_totals, double* d_acc) {
+  Engine* be = batch_engine(B);
+  be->ensure_colors(static_cast<int64_t>(n_) * B);
+  dev::batch_colors<<<static_cast<unsigned>((static_cast<int64_t>(n_) * B + 255) / 256), 256, 0, stream_>>>(
+      d_colors, nglob_, relabeled_ ? d_perm_ : nullptr, n_, B, be->d_colors_);
+  ++launches_;
+  be->prof_ = prof_;
+  const int64_t l0 = be->launches_;
+  be->run_dp(be->d_colors_, d_totals, nullptr, nullptr);
+  be->prof_ = nullptr;
+  launches_ += be->launches_ - l0;
+  if (d_acc) {
+    dev::fold_copies<<<static_cast<unsigned>((n_ + 255) / 256), 256, 0, stream_>>>(
+        reinterpret_cast<const double*>(be->arena_ + be->exec_.back().out_off), n_, B, d_acc);
+    ++launches_;
+  }
+  TCG_CUDA(cudaGetLastError());
 }
 
 // ------------------------------------------------------------ bench timing
@@ -2129,8 +2380,12 @@ void Engine::time_colorings(uint64_t seed, int count, bool per_kernel, double* t
       const int c = std::min(chunk, count - i0);
       for (int j = 0; j < c; ++j) seeds[j] = seed + static_cast<uint64_t>(i0 + j);
       gen_colors(seeds.data(), c, d_colors_);
-      for (int j = 0; j < c; ++j)
-        run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, nullptr, nullptr);
+      for (int j = 0; j < c;) {
+        const int B = pick_batch(c - j);
+        if (B > 1) run_batch(d_colors_ + static_cast<int64_t>(j) * nglob_, B, d_totals + i0 + j, nullptr);
+        else run_dp(d_colors_ + static_cast<int64_t>(j) * nglob_, d_totals + i0 + j, nullptr, nullptr);
+        j += B;
+      }
     }
     TCG_CUDA(cudaEventRecord(e1, stream_));
     TCG_CUDA(cudaEventSynchronize(e1));
@@ -2199,13 +2454,30 @@ void Engine::node_table(int id, int which, double* out) {
   if (!(cfg_.flags & TCG_KEEP_TABLES)) throw invalid_argument("context not created with TCG_KEEP_TABLES");
   if (!tables_valid_) throw invalid_argument("no coloring has been run since the last change");
   if (id < 0 || id >= plan_.num_nodes) throw invalid_argument("node id out of range");
+  const int64_t k = plan_.k;
+  if (plan_.is_leaf(id) && which == 0) {  // the one-hot leaf table, caller order
+    std::fill(out, out + static_cast<int64_t>(nglob_) * k, 0.0);
+    for (int64_t v = 0; v < nglob_; ++v) out[v * k + last_colors_[v]] = 1.0;
+    return;
+  }
+  if (!relabeled_) {
+    node_table_internal(id, which, out, last_colors_);
+    return;
+  }
+  // internal rows -> the caller's vertices (isolated vertices: zero rows)
+  const int64_t C = plan_.is_leaf(id) ? k : id == plan_.full_node() ? 1 : binom()(plan_.k, plan_.size[id]);
+  const std::vector<int32_t> perm = host_perm();
+  std::vector<uint8_t> lc(static_cast<size_t>(n_));
+  for (int32_t i = 0; i < n_; ++i) lc[i] = last_colors_[perm[i]];
+  std::vector<double> tmp(static_cast<size_t>(n_) * C);
+  node_table_internal(id, which, tmp.data(), lc);
+  std::fill(out, out + static_cast<int64_t>(nglob_) * C, 0.0);
+  for (int32_t i = 0; i < n_; ++i) std::copy(tmp.begin() + i * C, tmp.begin() + (i + 1) * C, out + perm[i] * C);
+}
+
+void Engine::node_table_internal(int id, int which, double* out, const std::vector<uint8_t>& lc) {
   const int64_t n = n_, k = plan_.k;
   if (plan_.is_leaf(id)) {
-    if (which == 0) {
-      std::fill(out, out + n * k, 0.0);
-      for (int64_t v = 0; v < n; ++v) out[v * k + last_colors_[v]] = 1.0;
-      return;
-    }
     if (hist_off_ < 0) throw invalid_argument("no neighbour histogram in this plan");
     std::vector<float> h(dev::table_floats(k, n));
     copy_sync(h.data(), arena_ + hist_off_, h.size() * 4, cudaMemcpyDeviceToHost);
@@ -2238,7 +2510,7 @@ void Engine::node_table(int id, int which, double* out) {
       for (int c = 0; c < k && !e.amap_host.empty(); ++c)
         for (int32_t q = 0; q < e.Ws; ++q) qof[static_cast<size_t>(c) * e.Ws + e.amap_host[static_cast<size_t>(c) * e.Ws + q]] = q;
       for (int64_t v = 0; v < n; ++v) {
-        const int c = last_colors_[v];
+        const int c = lc[v];
         for (int64_t S = 0; S < C; ++S) {
           const int64_t j = rel[static_cast<size_t>(S) * k + c];
           double x = 0.0;
@@ -2284,7 +2556,7 @@ void Engine::node_table(int id, int which, double* out) {
         }
         for (int64_t v = 0; v < n; ++v)
           for (int64_t c = 0; c < C; ++c) {
-            const int cv = last_colors_[v];
+            const int cv = lc[v];
             if (mask[static_cast<size_t>(c)] >> cv & 1u) { out[v * C + c] = 0.0; continue; }
             const int64_t col = e.pair ? e.rl_perm[rel[static_cast<size_t>(c) * k + cv]] : e.rl_perm[c];
             out[v * C + c] = t[dev::panel_offset(e.Cps, n, v, col)];
@@ -2304,9 +2576,10 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   const int64_t n = n_;
   for (int p = 0; p < dev::num_panels(cols); ++p) ensure_schedules(parts_for_width(dev::panel_width(cols, p)));
+  const std::vector<int32_t> perm = host_perm();  // internal row -> caller vertex
   std::vector<float> xp(dev::table_floats(cols, n), 0.f);
   for (int64_t v = 0; v < n; ++v)
-    for (int64_t c = 0; c < cols; ++c) xp[dev::panel_offset(cols, n, v, c)] = x[v * cols + c];
+    for (int64_t c = 0; c < cols; ++c) xp[dev::panel_offset(cols, n, v, c)] = x[perm[v] * cols + c];
   float *dx = nullptr, *dy = nullptr;
   double* saved_partial = d_partial_;
   double* dp = nullptr;
@@ -2326,8 +2599,194 @@ void Engine::spmm_host(const float* x, int cols, float* y) {
     throw;
   }
   dfree(dx); dfree(dy); dfree(dp);
+  std::fill(y, y + static_cast<int64_t>(nglob_) * cols, 0.f);  // isolated vertices: 0
   for (int64_t v = 0; v < n; ++v)
-    for (int64_t c = 0; c < cols; ++c) y[v * cols + c] = xp[dev::panel_offset(cols, n, v, c)];
+    for (int64_t c = 0; c < cols; ++c) y[perm[v] * cols + c] = xp[dev::panel_offset(cols, n, v, c)];
+}
+
+// Kernel-level hook of the PRODUCTION rooted SpMM (tcg_spmm_rooted): one
+// passive table M (n x C(k, s), caller order, rooted: M[u, S] = 0 unless
+// c(u) is in S) through exactly the per-coloring path a DP node runs --
+// bucket_coloring (rotated colour order, hub-row chunks), the k-colour slot
+// layout (spmm_rooted<zw, 4, false>) or the pair layout (pair_expand +
+// spmm_rooted<zw, 4, true>), rooted_fixup for rows split into segments --
+// and Y[v, T] = sum over u in N(v) of M[u, T] for every T missing c(v) (the
+// columns any eMA consumes; 0 elsewhere).  la_kernels.hpp:83-102 semantics.
+void Engine::spmm_rooted_host(int k, int s, bool pair, const uint8_t* colors, const float* x, float* y) {
+  if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
+  if (sharded()) throw invalid_argument("tcg_spmm_rooted is not available on a sharded context");
+  if (k < 2 || k > kMaxK || s < 1 || s >= k) throw invalid_argument("need 2 <= k <= 20 and 1 <= s < k");
+  if (pair && k < 3) throw invalid_argument("the pair layout needs k >= 3");
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  const Binom& B = binom();
+  const int64_t n = n_, C = B(k, s);
+  for (int32_t v = 0; v < nglob_; ++v)
+    if (colors[v] >= k) throw invalid_argument("coloring value out of range [0, k)");
+  const std::vector<int32_t> perm = host_perm();
+  std::vector<uint8_t> lc(static_cast<size_t>(n));
+  for (int64_t i = 0; i < n; ++i) lc[i] = colors[perm[i]];
+  int cs[kMaxK];
+  NodeExec e;
+  e.id = -1;
+  e.p = -1;
+  e.sp = s;
+  e.rooted = true;
+  e.pair = pair;
+  const RootedLayout rl = build_rooted_layout(pair ? k - 1 : k, s);
+  e.Cps = rl.store_cols;
+  e.rl_zw = rl.zw;
+  e.rl_groups = rl.groups;
+  e.rl_fbase = rl.fbase;
+  e.rl_fsize = rl.fsize;
+  e.rl_perm = rl.perm;
+  e.slot_K = pair ? k - 1 : k;
+  int fpad_max = 0;
+  for (int g = 0; g < rl.groups; ++g)
+    fpad_max = std::max(fpad_max, (g + 1 < rl.groups ? rl.fbase[g + 1] : rl.store_cols) - rl.fbase[g]);
+  e.rooted_smem = static_cast<size_t>(dev::kSpmmWarps) * (128 / rl.zw) * (fpad_max + 4) * 4 + 2 * (e.slot_K + 1) * rl.zw;
+  const int slots = rl.groups * rl.zw;
+  // input: the k-colour slot layout (groups x zw columns), or RR (pair)
+  const int64_t wx = B(k - 1, s - 1);
+  const int64_t in_cols = pair ? wx : slots;
+  std::vector<float> xin(dev::table_floats(in_cols, n), 0.f);
+  std::vector<int16_t> xm;
+  if (pair) {
+    e.Wx = static_cast<int32_t>(wx);
+    xm.assign(static_cast<size_t>(k) * k * slots, -1);
+    for (int cu = 0; cu < k; ++cu)
+      for (int cv = 0; cv < k; ++cv) {
+        if (cu == cv) continue;
+        const int cr = cu - (cu > cv ? 1 : 0);
+        for (int i = 0; i < slots; ++i) {
+          const int32_t col1 = rl.slot_col[static_cast<size_t>(cr) * slots + i];
+          if (col1 < 0) continue;
+          set_of(k - 1, col1, s, cs);
+          for (int q = 0; q < s; ++q) cs[q] = cs[q] >= cv ? cs[q] + 1 : cs[q];
+          xm[(static_cast<size_t>(cu) * k + cv) * slots + i] = static_cast<int16_t>(relabeled_index(cs, s, cu));
+        }
+      }
+    for (int64_t u = 0; u < n; ++u) {  // RR column j of u = M[u, (set j past c(u)) + c(u)]
+      const int cu = lc[u];
+      for (int64_t j = 0; j < wx; ++j) {
+        set_of(k - 1, j, s - 1, cs);
+        int t[kMaxK], m = 0;
+        bool put = false;
+        for (int q = 0; q < s - 1; ++q) {
+          const int c = cs[q] >= cu ? cs[q] + 1 : cs[q];
+          if (!put && c > cu) { t[m++] = cu; put = true; }
+          t[m++] = c;
+        }
+        if (!put) t[m++] = cu;
+        xin[dev::panel_offset(in_cols, n, u, j)] = x[static_cast<int64_t>(perm[u]) * C + index_of(t, s)];
+      }
+    }
+  } else {
+    for (int64_t u = 0; u < n; ++u)
+      for (int i = 0; i < slots; ++i) {
+        const int32_t col = rl.slot_col[static_cast<size_t>(lc[u]) * slots + i];
+        if (col >= 0) xin[dev::panel_offset(in_cols, n, u, i)] = x[static_cast<int64_t>(perm[u]) * C + col];
+      }
+  }
+  // scratch arena for this call (the engine's own arena and offsets are restored)
+  const int psave = rooted_parts_;
+  char* asave = arena_;
+  const int64_t o_rc = rcol_off_, o_cut = rcut_off_, o_lc = lcnt_off_, o_seg = pseg_off_, o_key = pkey_off_,
+                o_perm = pperm_off_, o_cnt = pcnt_off_;
+  double* part_save = d_partial_;
+  const int64_t nseg = sched_.at(1)[0].nseg_padded;
+  ArenaPlanner ap;
+  rcol_off_ = ap.alloc(4 * std::max<int64_t>(nnz_, 1));
+  rcut_off_ = ap.alloc(8 * n * 2);
+  lcnt_off_ = ap.alloc(4 * 32 * static_cast<int64_t>(std::max(nlchunks_, 1)));
+  pseg_off_ = ap.alloc(static_cast<int64_t>(sizeof(dev::Seg)) * nseg);
+  pkey_off_ = ap.alloc(nseg);
+  pperm_off_ = ap.alloc(4 * nseg);
+  pcnt_off_ = ap.alloc(4 * ((nseg + dev::kVsChunk - 1) / dev::kVsChunk + 1) * (k + 1));
+  const int64_t o_in = ap.alloc(4 * static_cast<int64_t>(xin.size()));
+  e.ct_off = pair ? ap.alloc(4ll * k * slots * n) : -1;
+  const int64_t o_out = ap.alloc(table_bytes(e.Cps));
+  const int64_t o_col = ap.alloc(std::max<int64_t>(n, 1));
+  const int64_t o_dummy = ap.alloc(2 * static_cast<int64_t>(e.slot_K + 1) * slots);
+  const int64_t o_xm = ap.alloc(2 * std::max<int64_t>(static_cast<int64_t>(xm.size()), 1));
+  const int64_t o_part = ap.alloc(8 * std::max<int64_t>(1, static_cast<int64_t>(sched_.at(1)[0].nslots)) *
+                                  static_cast<int64_t>(e.rooted_smem / (4 * dev::kSpmmWarps * (128 / rl.zw))));
+  char* scratch = nullptr;
+  std::vector<float> pp(dev::table_floats(e.Cps, n));
+  try {
+    TCG_CUDA(cudaMalloc(&scratch, std::max<int64_t>(ap.peak, kAlign)));
+    arena_ = scratch;
+    rooted_parts_ = 1;
+    d_partial_ = reinterpret_cast<double*>(scratch + o_part);
+    const std::vector<int16_t> dummy = dummy_slots(rl, e.slot_K);
+    e.d_slot_acc = reinterpret_cast<int16_t*>(scratch + o_dummy);
+    TCG_CUDA(cudaMemcpyAsync(e.d_slot_acc, dummy.data(), 2 * dummy.size(), cudaMemcpyHostToDevice, stream_));
+    if (pair) {
+      e.d_xmap = reinterpret_cast<int16_t*>(scratch + o_xm);
+      TCG_CUDA(cudaMemcpyAsync(e.d_xmap, xm.data(), 2 * xm.size(), cudaMemcpyHostToDevice, stream_));
+    }
+    uint8_t* dcol = reinterpret_cast<uint8_t*>(scratch + o_col);
+    if (n) TCG_CUDA(cudaMemcpyAsync(dcol, lc.data(), n, cudaMemcpyHostToDevice, stream_));
+    TCG_CUDA(cudaMemcpyAsync(scratch + o_in, xin.data(), 4 * xin.size(), cudaMemcpyHostToDevice, stream_));
+    if (n > 0) {
+      bucket_coloring(dcol, dcol, k, nullptr, pair);
+      const bool save_ema = rooted_ema_;
+      rooted_ema_ = true;  // the input is already in the SpMM's layout
+      try {
+        rooted_spmm(e, reinterpret_cast<const float*>(scratch + o_in), reinterpret_cast<float*>(scratch + o_out), dcol);
+      } catch (...) {
+        rooted_ema_ = save_ema;
+        throw;
+      }
+      rooted_ema_ = save_ema;
+    }
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    copy_sync(pp.data(), scratch + o_out, 4 * pp.size(), cudaMemcpyDeviceToHost);
+  } catch (...) {
+    arena_ = asave;
+    rooted_parts_ = psave;
+    d_partial_ = part_save;
+    rcol_off_ = o_rc; rcut_off_ = o_cut; lcnt_off_ = o_lc; pseg_off_ = o_seg; pkey_off_ = o_key;
+    pperm_off_ = o_perm; pcnt_off_ = o_cnt;
+    if (scratch) cudaFree(scratch);
+    throw;
+  }
+  arena_ = asave;
+  rooted_parts_ = psave;
+  d_partial_ = part_save;
+  rcol_off_ = o_rc; rcut_off_ = o_cut; lcnt_off_ = o_lc; pseg_off_ = o_seg; pkey_off_ = o_key;
+  pperm_off_ = o_perm; pcnt_off_ = o_cnt;
+  cudaFree(scratch);
+  tables_valid_ = false;
+  // P' storage -> caller order, full C(k, s) columns
+  std::fill(y, y + static_cast<int64_t>(nglob_) * C, 0.f);
+  std::vector<uint32_t> mask(static_cast<size_t>(C));
+  std::vector<int64_t> rel;
+  for (int64_t c = 0; c < C; ++c) {
+    set_of(k, c, s, cs);
+    uint32_t m = 0;
+    for (int j = 0; j < s; ++j) m |= 1u << cs[j];
+    mask[static_cast<size_t>(c)] = m;
+  }
+  if (pair) {
+    rel.assign(static_cast<size_t>(C) * k, -1);
+    for (int64_t c = 0; c < C; ++c) {
+      set_of(k, c, s, cs);
+      for (int q = 0; q < k; ++q)
+        if (!(mask[static_cast<size_t>(c)] >> q & 1u)) {
+          int tt[kMaxK];
+          for (int j = 0; j < s; ++j) tt[j] = cs[j] > q ? cs[j] - 1 : cs[j];
+          rel[static_cast<size_t>(c) * k + q] = index_of(tt, s);
+        }
+    }
+  }
+  for (int64_t v = 0; v < n; ++v) {
+    const int cv = lc[v];
+    for (int64_t c = 0; c < C; ++c) {
+      if (mask[static_cast<size_t>(c)] >> cv & 1u) continue;
+      const int64_t col = pair ? rl.perm[rel[static_cast<size_t>(c) * k + cv]] : rl.perm[c];
+      y[static_cast<int64_t>(perm[v]) * C + c] = pp[dev::panel_offset(e.Cps, n, v, col)];
+    }
+  }
 }
 
 }  // namespace tcg

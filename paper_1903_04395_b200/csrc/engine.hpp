@@ -139,7 +139,7 @@ class Engine {
   void set_shard(int rank, int world, std::unique_ptr<Transport> t);
   bool sharded() const { return world_ > 1 || static_cast<bool>(tr_); }
   int32_t n_global() const { return nglob_; }
-  explicit Engine(const tcg_config& cfg);
+  explicit Engine(const tcg_config& cfg, cudaStream_t shared_stream = nullptr);
   ~Engine();
 
   void set_graph(const Csr& g);
@@ -158,7 +158,9 @@ class Engine {
   void estimate(uint64_t seed, int iterations, double* totals, double* est, double* se,
                 double* per_vertex_est);
   void node_table(int node_id, int which, double* out);
+  void node_table_internal(int node_id, int which, double* out, const std::vector<uint8_t>& colors);
   void spmm_host(const float* x, int cols, float* y);
+  void spmm_rooted_host(int k, int s, bool pair, const uint8_t* colors, const float* x, float* y);
   void set_rejection_limit(uint64_t limit) { limit_override_ = limit; }
   int64_t launches() const { return launches_; }
   void time_colorings(uint64_t seed, int count, bool per_kernel, double* totals, tcg_timing* out);
@@ -179,6 +181,18 @@ class Engine {
   void hist(const uint8_t* d_colors, float* H);
   float* table_ptr(int64_t off) const { return reinterpret_cast<float*>(arena_ + off); }
   int64_t table_bytes(int64_t cols) const { return 4 * dev::table_floats(cols, n_); }
+
+  // batched colorings: B colorings of a small graph as one DP
+  // over the B-fold disjoint union, on a second engine sharing this stream
+  std::unique_ptr<Engine> batch_;
+  int batch_copies_ = 1;             // > 1: this engine holds a union of that many copies
+  bool no_relabel_ = false;          // (batch engines: the union keeps its copies contiguous)
+  bool own_stream_ = true;
+  uint64_t graph_gen_ = 0, tpl_gen_ = 0, batch_graph_gen_ = ~0ull, batch_tpl_gen_ = ~0ull;
+  int pick_batch(int count) const;
+  Engine* batch_engine(int B);
+  // B colorings (caller order, nglob_ bytes each) -> totals[B], acc (nullable) += per-vertex
+  void run_batch(const uint8_t* d_colors, int B, double* d_totals, double* d_acc);
 
   // per-kernel event pairs recorded by run_dp when prof_ is set
   struct Prof {
@@ -249,6 +263,31 @@ class Engine {
   void* gp_tmp_ = nullptr;
   size_t gp_tmp_cap_ = 0;
   void prep_graph_device();
+  void* cub_tmp(size_t bytes);
+  // degree-aware relabeling + isolated-vertex compaction (SURVEY 8(f)4,
+  // kernels_graph.cuh): internal row i = caller vertex perm[i]; n_ = rows with
+  // a neighbour.  Colors are permuted per coloring, per-vertex results
+  // scattered back; the caller never sees internal ids.
+  bool relabeled_ = false, rows_sorted_ = true;
+  void relabel_device();
+  void sort_rows();
+  uint32_t hot_packed_ = 0xFFFFFFFFu;  // rooted SpMM gathers: packed entries below it evict_last, others evict_first
+  int hot_mb_ = -1;                    // >= 0: L2 megabytes of hub rows kept per gather source (TCG_HOT_MB)
+  int32_t* d_perm_ = nullptr;        // internal row -> caller vertex (n_ live rows)
+  int32_t* d_inv_ = nullptr;         // caller vertex -> internal row, or -1 (isolated)
+  int64_t perm_cap_ = 0, inv_cap_ = 0;
+  int64_t* d_rp2_ = nullptr;         // relabel scratch: new row_ptr (swapped into d_row_ptr_)
+  int32_t* d_col2_ = nullptr;        // relabel scratch: new col (before the per-row sort)
+  int64_t rp2_cap_ = 0, col2_cap_ = 0;
+  char* rl_buf_ = nullptr;           // relabel scratch: keys, ids, degrees, counter
+  int64_t rl_cap_ = -1;
+  uint8_t* d_colors_rl_ = nullptr;   // one coloring in internal row order
+  int64_t colors_rl_cap_ = 0;
+  double* d_pv_out_ = nullptr;       // per-vertex results in caller order (nglob_)
+  int64_t pv_out_cap_ = 0;
+  std::vector<int32_t> host_perm() ;  // d_perm_ on the host (inspection paths)
+  // per-vertex fp64 values of the internal rows -> caller order on the host
+  void unpermute_to_host(const double* d_internal, double* host);
   int64_t lcnt_off_ = -1;            // per-coloring chunk color counts [chunks][32]
   int* d_counter_ = nullptr;
 
@@ -270,6 +309,7 @@ class Engine {
   int64_t rcol_off_ = -1;            // per-coloring color-sorted packed CSR
   int64_t rcut_off_ = -1;            // per-coloring part (color class) cuts, n * (parts + 1)
   // Pp: full P' (group-major), or the n x Ct scratch of a streamed node (out = its output table)
+  void bucket_coloring(const uint8_t* d_gcolors, const uint8_t* d_colors, int k, float* hf, bool pair);
   void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out = nullptr);
   bool rooted_ema_ = false;          // every table rooted; eMA on same-color vertex tiles
   int max_tiles_ = 0;                // ceil(n / 32) + k

@@ -650,7 +650,8 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
             const int64_t* __restrict__ cuts, int nparts, int part, const int32_t* __restrict__ slot_row,
             const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
             int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
-            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride, int kdummy) {
+            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride, int kdummy,
+            uint32_t hot) {
   constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
   extern __shared__ float racc_sm[];
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
@@ -726,7 +727,9 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       v[j] = make_float4(0, 0, 0, 0);
-      if (j < count) v[j] = ld_keep_f4(row_addr(Xr, pk[j], ZW / 8), pkeep);
+      // the relabeled hub prefix (packed entries below `hot`) stays in L2;
+      // the long tail of rarely-gathered rows streams through
+      if (j < count) v[j] = ld_keep_f4(row_addr(Xr, pk[j], ZW / 8), pk[j] < hot ? pkeep : pstream);
     }
     if (count > 0 && static_cast<int>(c_slot) != cur) {
       scatter();
@@ -1409,11 +1412,17 @@ ema_root(const float* __restrict__ Am, const float* __restrict__ Pm,
 
 // Deterministic fp64 sum of the per-tile totals (engines.hpp:125-129; the
 // reference's sequential sum differs only at the 1e-16 level).
-__global__ void root_reduce(const double* __restrict__ tile_tot, int64_t ntiles,
+// Segment blockIdx.x of x (len values each) -> total[blockIdx.x]: per-vertex
+// root counts in internal row order, a fixed-shape tree (1024 strided
+// partial sums, then a halving tree), so a coloring's total does not depend
+// on whether it ran alone or as one copy of a batch.
+__global__ void root_reduce(const double* __restrict__ x, int64_t len,
                             double* __restrict__ total) {
   __shared__ double red[1024];
+  const double* tile_tot = x + static_cast<int64_t>(blockIdx.x) * len;
+  total += blockIdx.x;
   double s = 0;
-  for (int64_t i = threadIdx.x; i < ntiles; i += blockDim.x) s += tile_tot[i];
+  for (int64_t i = threadIdx.x; i < len; i += blockDim.x) s += tile_tot[i];
   red[threadIdx.x] = s;
   __syncthreads();
   for (int o = blockDim.x / 2; o; o >>= 1) {
@@ -1421,6 +1430,37 @@ __global__ void root_reduce(const double* __restrict__ tile_tot, int64_t ntiles,
     __syncthreads();
   }
   if (threadIdx.x == 0) *total = red[0];
+}
+
+// --------------------------------------------------- batched colorings
+// Colorings on a batch axis: B colorings of a small graph run
+// as ONE coloring of the B-fold disjoint union (copy b = rows [b n, (b+1) n)),
+// so every launch of the DP covers B colorings.
+__global__ void union_graph(const int64_t* __restrict__ rp, const int32_t* __restrict__ col, int32_t n,
+                            int64_t nnz, int B, int64_t* __restrict__ rpU, int32_t* __restrict__ colU) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  const int64_t t0 = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  for (int64_t t = t0; t <= static_cast<int64_t>(n) * B; t += stride)
+    rpU[t] = t == static_cast<int64_t>(n) * B ? nnz * B : (t / n) * nnz + rp[t % n];
+  for (int64_t t = t0; t < nnz * B; t += stride)
+    colU[t] = static_cast<int32_t>((t / nnz) * n + col[t % nnz]);
+}
+// colors of copy b = coloring b, in internal row order
+__global__ void batch_colors(const uint8_t* __restrict__ in, int64_t nglob, const int32_t* __restrict__ perm,
+                             int32_t n, int B, uint8_t* __restrict__ out) {
+  const int64_t t = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (t >= static_cast<int64_t>(n) * B) return;
+  const int64_t b = t / n, i = t % n;
+  out[t] = in[b * nglob + (perm ? perm[i] : i)];
+}
+// per-vertex accumulation over the copies in coloring order (== one
+// root_acc[v] += count per coloring)
+__global__ void fold_copies(const double* __restrict__ pv, int32_t n, int B, double* __restrict__ acc) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = acc[i];
+  for (int b = 0; b < B; ++b) s += pv[static_cast<int64_t>(b) * n + i];
+  acc[i] = s;
 }
 
 }  // namespace dev

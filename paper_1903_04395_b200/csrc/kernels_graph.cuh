@@ -90,5 +90,66 @@ __global__ void graph_long_chunks(const int64_t* __restrict__ row_ptr, const int
     chunks[first[r] + q] = make_int4(v, static_cast<int32_t>(o), static_cast<int32_t>(min(d, o + kLongChunk)), q);
 }
 
+// ---------------------------------------------------------------- relabeling
+// Degree-aware relabeling with isolated-vertex compaction (the
+// reference's permutation hook is Graph::apply_permutation, graph.hpp:189-207):
+// new id = rank in descending degree (stable: ascending old id), isolated
+// vertices (degree 0, necessarily last) dropped.  Every count table then has
+// n_act rows, and the hub rows every SpMM gathers most often sit in one
+// contiguous, L2-resident prefix of each panel.
+
+// key = ~deg (ascending key = descending degree), ids = old id, nact += deg > 0
+__global__ void relabel_keys(const int64_t* __restrict__ row_ptr, int32_t n, uint32_t* __restrict__ key,
+                             int32_t* __restrict__ ids, int32_t* __restrict__ nact) {
+  const int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const bool live = v < n && row_ptr[v + 1] > row_ptr[v];
+  if (v < n) {
+    key[v] = ~static_cast<uint32_t>(row_ptr[v + 1] - row_ptr[v]);
+    ids[v] = static_cast<int32_t>(v);
+  }
+  const unsigned m = __ballot_sync(0xffffffffu, live);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(nact, __popc(m));
+}
+
+// inv[perm[i]] = i and deg'[i] = deg(perm[i]) for the nact live rows; deg'[nact] = 0
+__global__ void relabel_inverse(const int64_t* __restrict__ row_ptr, const int32_t* __restrict__ perm, int32_t nact,
+                                int32_t* __restrict__ inv, int64_t* __restrict__ deg) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i > nact) return;
+  if (i == nact) { deg[i] = 0; return; }
+  const int32_t v = perm[i];
+  inv[v] = static_cast<int32_t>(i);
+  deg[i] = row_ptr[v + 1] - row_ptr[v];
+}
+
+// warp per new row i: col'[rp'[i] + j] = inv[col[rp[perm[i]] + j]] (the
+// neighbours of a live vertex are live: the CSR is symmetric)
+__global__ void __launch_bounds__(256)
+relabel_fill(const int64_t* __restrict__ rp_old, const int32_t* __restrict__ col_old, const int32_t* __restrict__ perm,
+             const int32_t* __restrict__ inv, const int64_t* __restrict__ rp_new, int32_t nact, int32_t* __restrict__ col_new) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5); i < nact; i += nw) {
+    const int32_t v = perm[i];
+    const int64_t b = rp_old[v], d = rp_old[v + 1] - b, o = rp_new[i];
+    for (int64_t j = lane; j < d; j += 32) col_new[o + j] = __ldg(inv + __ldg(col_old + b + j));
+  }
+}
+
+// per coloring: colors of the internal rows, out[i] = in[perm[i]]
+__global__ void permute_colors(const uint8_t* __restrict__ in, const int32_t* __restrict__ perm, int32_t n,
+                               uint8_t* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = in[perm[i]];
+}
+
+// per-vertex fp64 results back to the caller's ids: out[perm[i]] = in[i]
+// (out pre-zeroed: isolated vertices count 0)
+__global__ void scatter_rows_f64(const double* __restrict__ in, const int32_t* __restrict__ perm, int32_t n,
+                                 double* __restrict__ out) {
+  const int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (i < n) out[perm[i]] = in[i];
+}
+
 }  // namespace dev
 }  // namespace tcg

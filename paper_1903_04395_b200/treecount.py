@@ -461,6 +461,15 @@ class Context:
         check(lib.tcg_spmm(self._h, _ptr(x), x.shape[1], _ptr(y)))
         return y
 
+    def spmm_rooted(self, k: int, s: int, colors: np.ndarray, x: np.ndarray, pair: bool = False) -> np.ndarray:
+        """Y = A M through the production rooted SpMM (tcg_spmm_rooted); only the
+        columns missing c(v) are computed (the rest are 0)."""
+        x = np.ascontiguousarray(x, dtype=np.float32)
+        colors = np.ascontiguousarray(colors, dtype=np.uint8)
+        y = np.zeros_like(x)
+        check(lib.tcg_spmm_rooted(self._h, k, s, 1 if pair else 0, _ptr(colors), _ptr(x), _ptr(y)))
+        return y
+
     def set_rejection_limit(self, limit: int) -> None:
         check(lib.tcg_set_rejection_limit(self._h, limit))
 

@@ -15,7 +15,16 @@ child process):
   colour-class parts (P' accumulated across parts);
 * TCG_PAIR=0 -- no pair layout (every rooted SpMM over the k-color slot
   layout); TCG_PAIR=2 -- the pair layout for every node whose copies fit;
-* TCG_VIRT=0 -- every active-leaf table materialized (no virtual tables).
+* TCG_VIRT=0 -- every active-leaf table materialized (no virtual tables);
+* TCG_RELABEL=0 -- no degree relabeling / isolated-vertex compaction (the
+  caller's vertex ids are the internal rows);
+* TCG_DEDUP=0 -- identical sub-templates recomputed (no aliasing);
+* TCG_EMA_BLOCKED=0 -- no register-blocked eMA (every non-leaf node through
+  the generic rooted node kernels);
+* TCG_RTV_PLEAF=0 -- wide nodes over a leaf passive child through
+  ema_rtv_blocked instead of the drop-table kernel;
+* TCG_RT_WARP=0 -- narrow rooted nodes CTA-per-tile instead of warp-per-tile;
+* TCG_ROOTED=0 with TCG_PART_KB=64 -- full-table SpMM in many vertex-range parts.
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -77,9 +86,12 @@ print("OK")
 
 @pytest.mark.parametrize("env", [{"TCG_RT_VTX": "2"}, {"TCG_ROOTED_EMA": "0"}, {"TCG_ROOTED": "0"},
                                  {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"},
-                                 {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}, {"TCG_VIRT": "0"}],
+                                 {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}, {"TCG_VIRT": "0"}, {"TCG_RELABEL": "0"},
+                                 {"TCG_DEDUP": "0"}, {"TCG_EMA_BLOCKED": "0"}, {"TCG_RTV_PLEAF": "0"},
+                                 {"TCG_RT_WARP": "0"}, {"TCG_ROOTED": "0", "TCG_PART_KB": "64"}],
                          ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
-                              "rooted_parts", "pair_off", "pair_all", "virt_off"])
+                              "rooted_parts", "pair_off", "pair_all", "virt_off", "relabel_off", "dedup_off",
+                              "blocked_off", "pleaf_off", "rt_warp_off", "full_table_parts"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,

@@ -130,6 +130,76 @@ def test_spmm_hub_rows_split_segments():
     assert np.array_equal(y, dense_ref(g, x).astype(np.float32))
 
 
+# ------------------------------------------------ production rooted SpMM (tcg_spmm_rooted)
+def rooted_table(rng, n, k, s, colors, hi=1000):
+    """Random integer-valued passive table, rooted: M[u, S] = 0 unless c(u) in S."""
+    ix = T.ColorIndexer(k)
+    has = np.array([[c in ix.set_of(S, s) for c in range(k)] for S in range(ix.num_sets(s))])  # [S, c]
+    x = rng.integers(0, hi, size=(n, ix.num_sets(s))).astype(np.float32)
+    x[~has[:, colors].T] = 0
+    return x, has
+
+
+def dense_rooted_ref(g, x, has, colors):
+    y = dense_ref(g, x)
+    y[has[:, colors].T] = 0  # only the columns missing c(v) are computed
+    return y
+
+
+@pytest.mark.parametrize("pair", [False, True])
+def test_spmm_rooted_spec_examples(pair):
+    # test_la_kernels.cpp:24-43 through the production kernel: with k = 2 (3 for
+    # the pair layout), s = 1 and colors c, the consumed column of row v is
+    # {c(u)} for its neighbours u, so y carries the spmv KATs
+    k = 3 if pair else 2
+    g = T.from_edges([(0, 1)])
+    c = spmm_ctx(g)
+    x = np.zeros((2, k), np.float32)
+    x[0, 0], x[1, 1] = 1, 2
+    y = c.spmm_rooted(k, 1, np.array([0, 1], np.uint8), x, pair)
+    assert y[0, 1] == 2 and y[1, 0] == 1
+    g = T.from_edges([(0, 1), (1, 2), (2, 0)])
+    x = np.zeros((3, k), np.float32)
+    for v, val in enumerate([1, 2, 3]):
+        x[v, v % k] = val
+    y = spmm_ctx(g).spmm_rooted(k, 1, np.array([v % k for v in range(3)], np.uint8), x, pair)
+    if not pair:  # k = 2: vertices 0 and 2 share color 0
+        assert y[0, 1] == 2 and y[1, 0] == 1 + 3 and y[2, 1] == 2
+    else:
+        assert y[0, 1] == 2 and y[0, 2] == 3 and y[1, 0] == 1 and y[1, 2] == 3 and y[2, 0] == 1 and y[2, 1] == 2
+
+
+@pytest.mark.parametrize("pair", [False, True])
+@pytest.mark.parametrize("k,s", [(5, 2), (7, 3), (12, 4), (12, 5), (15, 3)])
+def test_spmm_rooted_dense_reference_integer_valued(k, s, pair):
+    """The default SpMM kernel (spmm_rooted) is EXACT on integer-valued tables
+    (fp32 8-neighbour trees below 2^24, fp64 run sums): random graphs whose
+    rows include hubs above one segment (1,024) and above one bucketing chunk
+    (4,096 neighbours: bucket_long), against the dense reference."""
+    rng = np.random.default_rng(k * 100 + s + pair)
+    for trial in range(3):
+        n = int(rng.integers(200, 9000))
+        e = [tuple(x) for x in rng.integers(0, n, size=(int(rng.integers(2, 12)) * n, 2))]
+        hubs = rng.choice(n, size=3, replace=False)
+        for h, d in zip(hubs, (n - 1, 5000, 1500)):
+            e += [(int(h), int(u)) for u in rng.choice(n, size=min(d, n - 1), replace=False) if u != h]
+        g = T.from_edges(e, n)
+        colors = rng.integers(0, k, size=n).astype(np.uint8)
+        x, has = rooted_table(rng, n, k, s, colors, hi=1000)
+        y = spmm_ctx(g).spmm_rooted(k, s, colors, x, pair)
+        assert np.array_equal(y, dense_rooted_ref(g, x, has, colors).astype(np.float32)), (trial, n)
+
+
+def test_spmm_rooted_isolated_and_empty():
+    g = T.from_edges([(0, 1)], 40)  # 38 isolated vertices (compacted away internally)
+    k, s = 4, 2
+    colors = (np.arange(40) % k).astype(np.uint8)
+    x, has = rooted_table(np.random.default_rng(1), 40, k, s, colors)
+    y = spmm_ctx(g).spmm_rooted(k, s, colors, x)
+    assert np.array_equal(y, dense_rooted_ref(g, x, has, colors).astype(np.float32))
+    assert np.all(y[2:] == 0)
+
+
 # ---------------------------------------------------------------- engine KATs
 def test_engine_kat_k3_edge():
     # test_engines.cpp:28-41
