@@ -7,13 +7,16 @@
  * exceptions cross the ABI.  Status codes mirror the reference's exception
  * classes:
  *   TCG_OK        0  success
- *   TCG_EINVAL    1  std::invalid_argument / parse_error (bad graph, template,
- *                    k, iterations < 1, coloring size mismatch)
+ *   TCG_EINVAL    1  std::invalid_argument (k out of range, iterations < 1,
+ *                    coloring size / value mismatch, NULL arguments)
  *   TCG_ERESOURCE 2  memory_budget_error (engines.hpp:37-44) or device OOM --
  *                    the CLI's exit code 2 class (treecount_cli.cpp:501-503)
  *   TCG_ECUDA     3  CUDA failure
  *   TCG_ENONFINITE 4 non-finite rooted total (overflow guard, SURVEY finding 2)
  *   TCG_ELOGIC    5  std::logic_error (liveness / internal invariant)
+ *   TCG_EPARSE    6  treecount::parse_error (graph.hpp:18-21): bad graph input
+ *                    (vertex id out of range, CSR invariants) or template input
+ *                    (not a tree, root out of range; templates.hpp:37-88)
  * The message of the last failure is available from tcg_last_error().
  *
  * Ownership: inputs are caller-owned and copied; outputs are caller-allocated.
@@ -35,7 +38,8 @@ enum {
   TCG_ERESOURCE = 2,
   TCG_ECUDA = 3,
   TCG_ENONFINITE = 4,
-  TCG_ELOGIC = 5
+  TCG_ELOGIC = 5,
+  TCG_EPARSE = 6
 };
 
 #define TCG_MAX_K 20                   /* color_index.hpp:15 kMaxTemplateSize */
@@ -143,6 +147,15 @@ void tcg_destroy(tcg_ctx* ctx);
 /* Upload the graph (copied host -> device; builds the SpMM row schedule). */
 int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t* col);
 int tcg_set_graph_handle(tcg_ctx* ctx, const tcg_graph* g);
+/* graph.hpp:65-95 from_edges ON THE DEVICE: m raw (u,v) int32 pairs (any
+ * direction, duplicates and self-loops allowed) -> the reference's CSR
+ * (symmetric union, no loops, no duplicates, rows ascending) built by a
+ * radix sort + dedup on the GPU; n_hint < 0 = max id + 1.  Ids out of range
+ * -> TCG_EPARSE ("vertex id out of range [0, n)"), as the reference. */
+int tcg_set_graph_edges(tcg_ctx* ctx, const int32_t* edges, int64_t m, int32_t n_hint);
+/* The context's graph as a CSR over the caller's vertex ids (inspection):
+ * *n, *nnz, row_ptr[n+1] and col[nnz] -- every pointer nullable. */
+int tcg_get_graph_csr(tcg_ctx* ctx, int32_t* n, int64_t* nnz, int64_t* row_ptr, int32_t* col);
 /* Validate + partition + split tables + |Aut| on the host; upload tables. */
 int tcg_set_template(tcg_ctx* ctx, int k, const int32_t* edges, int root);
 /* Device bytes one coloring needs (arena peak + graph + schedules). */

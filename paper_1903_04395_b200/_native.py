@@ -21,7 +21,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
-TCG_OK, TCG_EINVAL, TCG_ERESOURCE, TCG_ECUDA, TCG_ENONFINITE, TCG_ELOGIC = range(6)
+TCG_OK, TCG_EINVAL, TCG_ERESOURCE, TCG_ECUDA, TCG_ENONFINITE, TCG_ELOGIC, TCG_EPARSE = range(7)
 TCG_MAX_K = 20
 TCG_MAX_NODES = 2 * TCG_MAX_K - 1
 TCG_KEEP_TABLES = 1
@@ -90,6 +90,8 @@ _SIGS = {
     "tcg_node_table": (C.c_int, [vp, C.c_int, C.c_int, vp]),
     "tcg_spmm": (C.c_int, [vp, vp, C.c_int, vp]),
     "tcg_spmm_rooted": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, vp, vp, vp]),
+    "tcg_set_graph_edges": (C.c_int, [vp, vp, i64, i32]),
+    "tcg_get_graph_csr": (C.c_int, [vp, P(i32), P(i64), vp, vp]),
     "tcg_set_rejection_limit": (C.c_int, [vp, u64]),
     "tcg_time_colorings": (C.c_int, [vp, u64, C.c_int, C.c_int, vp, P(TcgTiming)]),
     "tcg_kernel_launches": (i64, [vp]),
@@ -118,8 +120,13 @@ class TcgError(Exception):
     """Base for status codes other than TCG_OK."""
 
 
-class ParseError(TcgError, ValueError):
-    """TCG_EINVAL: the reference's std::invalid_argument / parse_error."""
+class InvalidArgument(TcgError, ValueError):
+    """TCG_EINVAL: the reference's std::invalid_argument."""
+
+
+class ParseError(InvalidArgument):
+    """TCG_EPARSE: the reference's treecount::parse_error (graph / template input).
+    (A subclass of InvalidArgument so callers catching either see both.)"""
 
 
 class MemoryBudgetError(TcgError, RuntimeError):
@@ -143,7 +150,7 @@ class LogicError(TcgError, RuntimeError):
     """TCG_ELOGIC: std::logic_error."""
 
 
-_ERR = {TCG_EINVAL: ParseError, TCG_ERESOURCE: MemoryBudgetError, TCG_ECUDA: CudaError,
+_ERR = {TCG_EINVAL: InvalidArgument, TCG_EPARSE: ParseError, TCG_ERESOURCE: MemoryBudgetError, TCG_ECUDA: CudaError,
         TCG_ENONFINITE: NonFiniteError, TCG_ELOGIC: LogicError}
 
 

@@ -24,6 +24,9 @@ int guarded(F&& f) {
   try {
     f();
     return TCG_OK;
+  } catch (const tcg::parse_error& e) {
+    g_err = e.what();
+    return TCG_EPARSE;
   } catch (const tcg::invalid_argument& e) {
     g_err = e.what();
     return TCG_EINVAL;
@@ -321,6 +324,21 @@ int tcg_spmm(tcg_ctx* ctx, const float* x, int cols, float* y) {
     need(x, "x");
     need(y, "y");
     ctx->eng->spmm_host(x, cols, y);
+  });
+}
+
+int tcg_set_graph_edges(tcg_ctx* ctx, const int32_t* edges, int64_t m, int32_t n_hint) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    if (m > 0) need(edges, "edges");
+    ctx->eng->set_graph_edges(edges, m, n_hint);
+  });
+}
+
+int tcg_get_graph_csr(tcg_ctx* ctx, int32_t* n, int64_t* nnz, int64_t* row_ptr, int32_t* col) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    ctx->eng->graph_csr(n, nnz, row_ptr, col);
   });
 }
 

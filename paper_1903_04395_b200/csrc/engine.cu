@@ -225,7 +225,6 @@ Engine::Engine(const tcg_config& cfg, cudaStream_t shared_stream) : cfg_(cfg) {
   // B200 that costs more than the L2 misses of the unsplit gather source
   // (cfg3 49.9 -> 47.9 ms, cfg4 1666 -> 1049 ms).
   if (const char* e = std::getenv("TCG_ROOTED_PARTS")) rooted_part_mb_ = std::atoi(e);
-  if (const char* e = std::getenv("TCG_HOT_MB")) hot_mb_ = std::atoi(e);
   if (shared_stream) {
     stream_ = shared_stream;
     own_stream_ = false;
@@ -401,7 +400,7 @@ void Engine::set_graph(const Csr& gin) {
 // is validated on the device when `validate`, and only O(n) host work builds
 // the whole-row schedule and the degree order.  Vertex-range part schedules
 // (full-table SpMM only) are built on first use (ensure_schedules).
-void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate) {
+void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate, int64_t nnz) {
   TCG_CUDA(cudaSetDevice(cfg_.device));
   release_graph();
   nglob_ = n;
@@ -409,8 +408,122 @@ void Engine::set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* co
   nloc_ = n;
   nsrc_ = n;
   n_ = n;
-  nnz_ = row_ptr[n];
+  nnz_ = nnz >= 0 ? nnz : row_ptr[n];  // (nnz given: device buffers, e.g. a batch union)
   finish_graph(row_ptr, col, validate);
+}
+
+// graph.hpp:65-95 from_edges ON THE DEVICE (kernels_graph.cuh edges_*): the
+// caller's raw edge list (possibly directed, duplicated, self-looped) -> the
+// reference's CSR (symmetric union, no loops, no duplicates, rows ascending)
+// built in d_row_ptr_ / d_col_ by one radix sort, then the usual
+// relabeling and schedules.  n_hint < 0: max id + 1.
+void Engine::set_graph_edges(const int32_t* edges, int64_t m, int32_t n_hint) {
+  if (sharded()) throw invalid_argument("tcg_set_graph_edges is not available on a sharded context");
+  if (m < 0) throw invalid_argument("negative edge count");
+  if (m > (int64_t{1} << 29)) throw invalid_argument("edge list too long for the device CSR build (2^29 edges)");
+  TCG_CUDA(cudaSetDevice(cfg_.device));
+  release_graph();
+  const int64_t cnt = 2 * m;
+  int32_t* dE = nullptr;
+  uint64_t *k1 = nullptr, *k2 = nullptr;
+  int32_t *keep = nullptr, *pos = nullptr;
+  int64_t* deg = nullptr;
+  auto cleanup = [&] {
+    dfree(dE); dfree(k1); dfree(k2); dfree(keep); dfree(pos); dfree(deg);
+  };
+  try {
+    TCG_CUDA(cudaMalloc(&dE, sizeof(int32_t) * std::max<int64_t>(cnt, 2) + 16));
+    int32_t* mm = dE + std::max<int64_t>(cnt, 2);  // {max, min}
+    const int32_t init[2] = {INT32_MIN, INT32_MAX};
+    TCG_CUDA(cudaMemcpyAsync(mm, init, sizeof(init), cudaMemcpyHostToDevice, stream_));
+    if (cnt) {
+      TCG_CUDA(cudaMemcpyAsync(dE, edges, sizeof(int32_t) * cnt, cudaMemcpyDefault, stream_));
+      dev::edges_minmax<<<148 * 4, 256, 0, stream_>>>(dE, cnt, mm, mm + 1);
+    }
+    int32_t h[2];
+    copy_sync(h, mm, sizeof(h), cudaMemcpyDeviceToHost);
+    const int32_t n = n_hint >= 0 ? n_hint : (cnt ? h[0] + 1 : 0);
+    if (cnt && (h[1] < 0 || h[0] >= n)) throw parse_error("vertex id out of range [0, " + std::to_string(n) + ")");
+    int bits = 1;
+    while ((int64_t{1} << bits) < n) ++bits;
+    TCG_CUDA(cudaMalloc(&deg, sizeof(int64_t) * (static_cast<size_t>(n) + 1)));
+    TCG_CUDA(cudaMemsetAsync(deg, 0, sizeof(int64_t) * (static_cast<size_t>(n) + 1), stream_));
+    int64_t nnz = 0;
+    if (cnt) {
+      TCG_CUDA(cudaMalloc(&k1, sizeof(uint64_t) * cnt));
+      TCG_CUDA(cudaMalloc(&k2, sizeof(uint64_t) * cnt));
+      TCG_CUDA(cudaMalloc(&keep, sizeof(int32_t) * cnt));
+      TCG_CUDA(cudaMalloc(&pos, sizeof(int32_t) * cnt));
+      dev::edges_keys<<<148 * 8, 256, 0, stream_>>>(dE, m, bits, k1);
+      size_t b = 0;
+      TCG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b, k1, k2, static_cast<int>(cnt), 0, 2 * bits, stream_));
+      TCG_CUDA(cub::DeviceRadixSort::SortKeys(cub_tmp(b), b, k1, k2, static_cast<int>(cnt), 0, 2 * bits, stream_));
+      dev::edges_keep<<<148 * 8, 256, 0, stream_>>>(k2, cnt, bits, keep, deg);
+      b = 0;
+      TCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, keep, pos, static_cast<int>(cnt), stream_));
+      TCG_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp(b), b, keep, pos, static_cast<int>(cnt), stream_));
+      int32_t tail[2];
+      TCG_CUDA(cudaMemcpyAsync(&tail[0], pos + cnt - 1, 4, cudaMemcpyDeviceToHost, stream_));
+      TCG_CUDA(cudaMemcpyAsync(&tail[1], keep + cnt - 1, 4, cudaMemcpyDeviceToHost, stream_));
+      TCG_CUDA(cudaStreamSynchronize(stream_));
+      nnz = static_cast<int64_t>(tail[0]) + tail[1];
+    }
+    if (row_ptr_cap_ < static_cast<int64_t>(n) + 1) {
+      dfree(d_row_ptr_);
+      row_ptr_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&d_row_ptr_, sizeof(int64_t) * (static_cast<size_t>(n) + 1)));
+      row_ptr_cap_ = static_cast<int64_t>(n) + 1;
+    }
+    if (col_cap_ < std::max<int64_t>(nnz, 1)) {
+      dfree(d_col_);
+      col_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz, 1)));
+      col_cap_ = std::max<int64_t>(nnz, 1);
+    }
+    size_t b = 0;
+    TCG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, b, deg, d_row_ptr_, n + 1, stream_));
+    TCG_CUDA(cub::DeviceScan::ExclusiveSum(cub_tmp(b), b, deg, d_row_ptr_, n + 1, stream_));
+    if (cnt) dev::edges_emit<<<148 * 8, 256, 0, stream_>>>(k2, keep, pos, cnt, bits, d_col_);
+    TCG_CUDA(cudaGetLastError());
+    TCG_CUDA(cudaStreamSynchronize(stream_));
+    nglob_ = n;
+    rows_ = {0, static_cast<int64_t>(n)};
+    nloc_ = n;
+    nsrc_ = n;
+    n_ = n;
+    nnz_ = nnz;
+  } catch (...) {
+    cleanup();
+    throw;
+  }
+  cleanup();
+  finish_graph(nullptr, nullptr, false);
+}
+
+// CSR of the caller's vertices (the relabeling undone): row_ptr[n+1], col[nnz]
+// (nullable), rows ascending -- inspection of a device-built graph.
+void Engine::graph_csr(int32_t* n_out, int64_t* nnz_out, int64_t* row_ptr, int32_t* col) {
+  if (n_ < 0) throw invalid_argument("no graph set (tcg_set_graph)");
+  if (sharded()) throw invalid_argument("graph CSR is not inspectable on a sharded context");
+  if (n_out) *n_out = nglob_;
+  if (nnz_out) *nnz_out = nnz_;
+  if (!row_ptr && !col) return;
+  std::vector<int64_t> rp(static_cast<size_t>(n_) + 1);
+  std::vector<int32_t> cl(static_cast<size_t>(std::max<int64_t>(nnz_, 1)));
+  copy_sync(rp.data(), d_row_ptr_, sizeof(int64_t) * rp.size(), cudaMemcpyDeviceToHost);
+  if (nnz_) copy_sync(cl.data(), d_col_, sizeof(int32_t) * nnz_, cudaMemcpyDeviceToHost);
+  const std::vector<int32_t> perm = host_perm();
+  std::vector<int64_t> deg(static_cast<size_t>(nglob_) + 1, 0);
+  for (int32_t i = 0; i < n_; ++i) deg[perm[i]] = rp[i + 1] - rp[i];
+  std::vector<int64_t> out_rp(static_cast<size_t>(nglob_) + 1, 0);
+  for (int32_t v = 0; v < nglob_; ++v) out_rp[v + 1] = out_rp[v] + deg[v];
+  if (row_ptr) std::copy(out_rp.begin(), out_rp.end(), row_ptr);
+  if (col)
+    for (int32_t i = 0; i < n_; ++i) {
+      int32_t* dst = col + out_rp[perm[i]];
+      for (int64_t e = rp[i]; e < rp[i + 1]; ++e) *dst++ = perm[cl[e]];
+      std::sort(col + out_rp[perm[i]], dst);
+    }
 }
 
 void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool validate) {
@@ -431,9 +544,12 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
     TCG_CUDA(cudaMalloc(&d_col_, sizeof(int32_t) * std::max<int64_t>(nnz_, 1)));
     col_cap_ = std::max<int64_t>(nnz_, 1);
   }
-  // (cudaMemcpyDefault: host buffers from the caller, device buffers from a batch union)
-  TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyDefault, stream_));
-  if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyDefault, stream_));
+  // (cudaMemcpyDefault: host buffers from the caller, device buffers from a
+  // batch union; row_ptr == nullptr: the CSR was built in place, set_graph_edges)
+  if (row_ptr) {
+    TCG_CUDA(cudaMemcpyAsync(d_row_ptr_, row_ptr, sizeof(int64_t) * (n_ + 1), cudaMemcpyDefault, stream_));
+    if (nnz_) TCG_CUDA(cudaMemcpyAsync(d_col_, col, sizeof(int32_t) * nnz_, cudaMemcpyDefault, stream_));
+  }
   if (validate && nnz_) {
     TCG_CUDA(cudaMemsetAsync(reinterpret_cast<int*>(d_scalars_ + 4), 0, sizeof(int), stream_));
     dev::validate_csr<<<148 * 8, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, reinterpret_cast<int*>(d_scalars_ + 4));
@@ -445,8 +561,8 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
     if (bad) {
       const int32_t n = n_;
       release_graph();
-      if (bad == 1) throw invalid_argument("CSR column out of range [0, " + std::to_string(n) + ") or self-loop");
-      throw invalid_argument("CSR row not strictly ascending");
+      if (bad == 1) throw parse_error("CSR column out of range [0, " + std::to_string(n) + ") or self-loop");
+      throw parse_error("CSR row not strictly ascending");
     }
   }
   static const int relabel_mode = [] {
@@ -548,6 +664,8 @@ void Engine::relabel_device() {
   n_ = nact;
   nsrc_ = nact;
   relabeled_ = true;
+  static const bool sort_mode = std::getenv("TCG_SORT_ROWS") && std::atoi(std::getenv("TCG_SORT_ROWS")) > 0;
+  if (sort_mode) sort_rows();
 }
 
 // Rows ascending (the vertex-range parts of the full-table SpMM cut rows by
@@ -1733,19 +1851,11 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
       const unsigned blocks = static_cast<unsigned>((ntasks + dev::kSpmmWarps - 1) / dev::kSpmmWarps);
       const int first = q == 0 ? 1 : 0;
       int part = q;
-      // L2 policy of the gathers: the first hot_rows rows of the (relabeled,
-      // degree-ordered) source evict_last, the rest evict_first
-      uint32_t hot = hot_packed_;
-      if (hot_mb_ >= 0) {
-        const int64_t rows = (static_cast<int64_t>(hot_mb_) << 20) / (4 * zw);
-        hot = rows >= (int64_t{1} << (32 - dev::kColorBits)) ? 0xFFFFFFFFu : static_cast<uint32_t>(rows) << dev::kColorBits;
-      }
       void* args[] = {const_cast<dev::Seg**>(&segs), const_cast<int64_t*>(&ntasks), const_cast<uint32_t**>(&colb),
                       const_cast<int64_t**>(&cuts), &rooted_parts_, &part, const_cast<int32_t**>(&ps.d_slot_row),
                       const_cast<float**>(&Xg), const_cast<int16_t**>(&sl), &slot_stride, const_cast<int*>(&fbase),
                       const_cast<int*>(&fpad), const_cast<int32_t*>(&Cst), &n_, &Pp, &d_partial_,
-                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride, const_cast<int*>(&e.slot_K),
-                      &hot};
+                      const_cast<int*>(&first), const_cast<uint8_t**>(&rowc), &xstride, const_cast<int*>(&e.slot_K)};
       TCG_CUDA(cudaLaunchKernel(kern, dim3(blocks), dim3(dev::kSpmmWarps * 32), args, smem, stream_));
       ++launches_;
       if (ps.nsplit_rows) {
@@ -2309,7 +2419,7 @@ Engine* Engine::batch_engine(int B) {
       edges.push_back(pr.second);
     }
     be->set_template(tpl_.k, edges.data(), tpl_.root);
-    be->set_graph_ptrs(static_cast<int32_t>(nU), rpU, colU, false);
+    be->set_graph_ptrs(static_cast<int32_t>(nU), rpU, colU, false, eU);
     be->ensure_arena();
   } catch (...) {
     dfree(rpU);

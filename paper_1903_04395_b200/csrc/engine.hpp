@@ -145,7 +145,9 @@ class Engine {
   void set_graph(const Csr& g);
   // unsharded graph from caller buffers (not copied on the host); validate =
   // check ids / order / loops on the device
-  void set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate);
+  void set_graph_ptrs(int32_t n, const int64_t* row_ptr, const int32_t* col, bool validate, int64_t nnz = -1);
+  void set_graph_edges(const int32_t* edges, int64_t m, int32_t n_hint);
+  void graph_csr(int32_t* n, int64_t* nnz, int64_t* row_ptr, int32_t* col);
   void set_template(int k, const int32_t* edges, int root);
   int64_t required_bytes() const;
   const Plan& plan() const { return plan_; }
@@ -271,8 +273,6 @@ class Engine {
   bool relabeled_ = false, rows_sorted_ = true;
   void relabel_device();
   void sort_rows();
-  uint32_t hot_packed_ = 0xFFFFFFFFu;  // rooted SpMM gathers: packed entries below it evict_last, others evict_first
-  int hot_mb_ = -1;                    // >= 0: L2 megabytes of hub rows kept per gather source (TCG_HOT_MB)
   int32_t* d_perm_ = nullptr;        // internal row -> caller vertex (n_ live rows)
   int32_t* d_inv_ = nullptr;         // caller vertex -> internal row, or -1 (isolated)
   int64_t perm_cap_ = 0, inv_cap_ = 0;

@@ -99,7 +99,7 @@ Csr csr_from_edges(const int32_t* edges, int64_t m, int32_t n_hint) {
     for (int64_t j = b; j < e; ++j)
       if (edges[j] < 0 || edges[j] >= n) { bad = true; return; }
   });
-  if (bad) throw invalid_argument("vertex id out of range [0, " + std::to_string(n) + ")");
+  if (bad) throw parse_error("vertex id out of range [0, " + std::to_string(n) + ")");
 
   Csr g;
   g.n = n;
@@ -144,9 +144,9 @@ Csr csr_from_edges(const int32_t* edges, int64_t m, int32_t n_hint) {
 }
 
 Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col, bool check_symmetry) {
-  if (n < 0 || !row_ptr || row_ptr[0] != 0) throw invalid_argument("bad CSR row_ptr");
+  if (n < 0 || !row_ptr || row_ptr[0] != 0) throw parse_error("bad CSR row_ptr");
   for (int32_t v = 0; v < n; ++v)
-    if (row_ptr[v + 1] < row_ptr[v]) throw invalid_argument("CSR row_ptr not monotone");
+    if (row_ptr[v + 1] < row_ptr[v]) throw parse_error("CSR row_ptr not monotone");
   Csr g;
   g.n = n;
   g.row_ptr.assign(row_ptr, row_ptr + n + 1);
@@ -164,9 +164,9 @@ Csr csr_adopt(int32_t n, const int64_t* row_ptr, const int32_t* col, bool check_
       }
     }
   });
-  if (bad == 1) throw invalid_argument("CSR column out of range or self-loop");
-  if (bad == 2) throw invalid_argument("CSR row not strictly ascending");
-  if (bad == 3) throw invalid_argument("CSR not symmetric");
+  if (bad == 1) throw parse_error("CSR column out of range or self-loop");
+  if (bad == 2) throw parse_error("CSR row not strictly ascending");
+  if (bad == 3) throw parse_error("CSR not symmetric");
   return g;
 }
 
@@ -546,7 +546,7 @@ static uint32_t component(const Template& t, uint32_t mask, int from, int blocke
 }
 
 Template make_template(int k, const int32_t* edges, int root) {
-  if (k < 1) throw invalid_argument("not a tree: empty template");
+  if (k < 1) throw parse_error("not a tree: empty template");
   if (k > kMaxK) throw invalid_argument("color count k must be in [1, 20]");
   Template t;
   t.k = k;
@@ -555,21 +555,21 @@ Template make_template(int k, const int32_t* edges, int root) {
   for (int e = 0; e < k - 1; ++e) {
     const int u = edges[2 * e], v = edges[2 * e + 1];
     if (u < 0 || v < 0 || u >= k || v >= k || u == v)
-      throw invalid_argument("not a tree: bad edge " + std::to_string(u) + " " + std::to_string(v));
+      throw parse_error("not a tree: bad edge " + std::to_string(u) + " " + std::to_string(v));
     max_id = std::max({max_id, u, v});
     t.edges.emplace_back(u, v);
     t.adj[u] |= 1u << v;
     t.adj[v] |= 1u << u;
   }
-  if (max_id + 1 != k) throw invalid_argument("not a tree: vertex ids must be 0..k-1");
+  if (max_id + 1 != k) throw parse_error("not a tree: vertex ids must be 0..k-1");
   const uint32_t all = k == 32 ? ~0u : (1u << k) - 1;
-  if (component(t, all, 0, -1) != all) throw invalid_argument("not a tree: disconnected");
+  if (component(t, all, 0, -1) != all) throw parse_error("not a tree: disconnected");
   if (root < 0) {  // templates.hpp:67-74: max degree, smallest id
     root = 0;
     for (int v = 1; v < k; ++v)
       if (__builtin_popcount(t.adj[v]) > __builtin_popcount(t.adj[root])) root = v;
   }
-  if (root >= k) throw invalid_argument("template root out of range");
+  if (root >= k) throw parse_error("template root out of range");
   t.root = root;
   return t;
 }

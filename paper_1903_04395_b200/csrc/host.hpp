@@ -21,6 +21,8 @@ namespace tcg {
 
 // Error classes mirroring the reference's exception types.
 struct invalid_argument : std::runtime_error { using std::runtime_error::runtime_error; };
+// treecount::parse_error (graph.hpp:18-21): bad graph / template INPUT
+struct parse_error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct resource_error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct cuda_error : std::runtime_error { using std::runtime_error::runtime_error; };
 struct nonfinite_error : std::runtime_error { using std::runtime_error::runtime_error; };

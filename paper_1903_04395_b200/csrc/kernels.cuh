@@ -650,8 +650,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
             const int64_t* __restrict__ cuts, int nparts, int part, const int32_t* __restrict__ slot_row,
             const float* __restrict__ X, const int16_t* __restrict__ slot_acc, int slot_stride,
             int fbase, int fpad, int Cstore, int32_t n, float* __restrict__ Y,
-            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride, int kdummy,
-            uint32_t hot) {
+            double* __restrict__ partial, int first, const uint8_t* __restrict__ rowc, int64_t xstride, int kdummy) {
   constexpr int G = ZW / 4, SPW = 32 / G, R = 8, NI = R / G;
   extern __shared__ float racc_sm[];
   const int lane = threadIdx.x & 31, g = lane / G, l = lane % G, warp = threadIdx.x >> 5;
@@ -727,9 +726,7 @@ spmm_rooted(const Seg* __restrict__ segs, int64_t ntasks, const uint32_t* __rest
 #pragma unroll
     for (int j = 0; j < R; ++j) {
       v[j] = make_float4(0, 0, 0, 0);
-      // the relabeled hub prefix (packed entries below `hot`) stays in L2;
-      // the long tail of rarely-gathered rows streams through
-      if (j < count) v[j] = ld_keep_f4(row_addr(Xr, pk[j], ZW / 8), pk[j] < hot ? pkeep : pstream);
+      if (j < count) v[j] = ld_keep_f4(row_addr(Xr, pk[j], ZW / 8), pkeep);
     }
     if (count > 0 && static_cast<int>(c_slot) != cur) {
       scatter();

@@ -90,6 +90,59 @@ __global__ void graph_long_chunks(const int64_t* __restrict__ row_ptr, const int
     chunks[first[r] + q] = make_int4(v, static_cast<int32_t>(o), static_cast<int32_t>(min(d, o + kLongChunk)), q);
 }
 
+// ------------------------------------------------------- CSR from edges
+// graph.hpp:65-95 from_edges on the device: every (u, v) edge becomes the two
+// directed keys u << b | v and v << b | u (b = bits of n); one radix sort, then
+// a key survives if it differs from its predecessor (dedup) and is not a
+// self-loop; its high part counts toward row u, its low part is the column.
+// Rows come out ascending, symmetric, loop- and duplicate-free -- the
+// reference's CSR.  ids out of range are flagged (bad = 1).
+__global__ void edges_minmax(const int32_t* __restrict__ e, int64_t cnt, int32_t* __restrict__ mx,
+                             int32_t* __restrict__ mn) {
+  int32_t a = INT32_MIN, b = INT32_MAX;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    a = max(a, e[i]);
+    b = min(b, e[i]);
+  }
+  for (int o = 16; o; o >>= 1) {
+    a = max(a, __shfl_xor_sync(0xffffffffu, a, o));
+    b = min(b, __shfl_xor_sync(0xffffffffu, b, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(mx, a);
+    atomicMin(mn, b);
+  }
+}
+__global__ void edges_keys(const int32_t* __restrict__ e, int64_t m, int bits, uint64_t* __restrict__ keys) {
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < m;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t u = static_cast<uint32_t>(e[2 * i]), v = static_cast<uint32_t>(e[2 * i + 1]);
+    keys[2 * i] = u << bits | v;
+    keys[2 * i + 1] = v << bits | u;
+  }
+}
+// keep[i] = first of its run and not a self-loop; deg[u] += keep
+__global__ void edges_keep(const uint64_t* __restrict__ k, int64_t cnt, int bits, int32_t* __restrict__ keep,
+                           int64_t* __restrict__ deg) {
+  const uint64_t lo = (uint64_t{1} << bits) - 1;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const uint64_t x = k[i];
+    const uint64_t u = x >> bits, v = x & lo;
+    const bool ok = u != v && (i == 0 || k[i - 1] != x);
+    keep[i] = ok;
+    if (ok) atomicAdd(reinterpret_cast<unsigned long long*>(deg + u), 1ull);
+  }
+}
+__global__ void edges_emit(const uint64_t* __restrict__ k, const int32_t* __restrict__ keep,
+                           const int32_t* __restrict__ pos, int64_t cnt, int bits, int32_t* __restrict__ col) {
+  const uint64_t lo = (uint64_t{1} << bits) - 1;
+  for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cnt;
+       i += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    if (keep[i]) col[pos[i]] = static_cast<int32_t>(k[i] & lo);
+}
+
 // ---------------------------------------------------------------- relabeling
 // Degree-aware relabeling with isolated-vertex compaction (the
 // reference's permutation hook is Graph::apply_permutation, graph.hpp:189-207):

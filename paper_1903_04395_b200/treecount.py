@@ -22,7 +22,7 @@ from typing import Optional
 import numpy as np
 
 from . import _native as N
-from ._native import (CudaError, LogicError, MemoryBudgetError, NonFiniteError, ParseError,
+from ._native import (CudaError, InvalidArgument, LogicError, MemoryBudgetError, NonFiniteError, ParseError,
                       TcgError, check, lib)
 
 kMaxTemplateSize = N.TCG_MAX_K  # color_index.hpp:15
@@ -202,7 +202,7 @@ class ColorIndexer:
 
     def __init__(self, k: int):
         if k < 1 or k > kMaxTemplateSize:
-            raise ParseError(f"color count k must be in [1, {kMaxTemplateSize}]")
+            raise InvalidArgument(f"color count k must be in [1, {kMaxTemplateSize}]")
         self._k = k
 
     def k(self) -> int:
@@ -221,7 +221,7 @@ class ColorIndexer:
         c = np.ascontiguousarray(colors, dtype=np.int32)
         r = lib.tcg_color_index_of(self._k, _ptr(c), len(c))
         if r < 0:
-            raise ParseError((lib.tcg_last_error() or b"").decode())
+            raise InvalidArgument((lib.tcg_last_error() or b"").decode())
         return int(r)
 
     def set_of(self, index: int, h: int) -> list:
@@ -251,9 +251,9 @@ def build_split_table(parent_size: int, active_size: int, indexer: ColorIndexer)
     k = indexer.k()
     passive = parent_size - active_size
     if active_size < 1 or passive < 1:
-        raise ParseError("split requires nonempty active and passive children")
+        raise InvalidArgument("split requires nonempty active and passive children")
     if parent_size > k:
-        raise ParseError("sub-template larger than color count")
+        raise InvalidArgument("sub-template larger than color count")
     cs, ca, cp = indexer.num_sets(parent_size), indexer.num_sets(active_size), indexer.num_sets(passive)
     pairs, partners = indexer.binom(parent_size, active_size), indexer.binom(k - passive, active_size)
     arrs = [np.zeros(cs * pairs, np.int32) for _ in range(4)]
@@ -289,7 +289,7 @@ def engine_from_name(s: str) -> EngineKind:
     try:
         return EngineKind(s)
     except ValueError:
-        raise ParseError(f"unknown engine '{s}'") from None
+        raise InvalidArgument(f"unknown engine '{s}'") from None
 
 
 @dataclass
@@ -405,6 +405,22 @@ class Context:
         check(lib.tcg_set_graph(self._h, n, _ptr(row_ptr), _ptr(col) if col.size else None))
         self.n, self.graph = n, None
 
+    def set_graph_edges(self, edges, n_hint: int = -1) -> None:
+        """graph.hpp:65-95 from_edges on the device (tcg_set_graph_edges)."""
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.int32).reshape(-1, 2))
+        check(lib.tcg_set_graph_edges(self._h, _ptr(e) if e.size else None, e.shape[0], n_hint))
+        self.graph = None
+        self.n = int(self.graph_csr()[0].shape[0] - 1)
+
+    def graph_csr(self):
+        """(row_ptr, col) of the context's graph over the caller's vertex ids."""
+        n, nnz = C.c_int32(), C.c_int64()
+        check(lib.tcg_get_graph_csr(self._h, C.byref(n), C.byref(nnz), None, None))
+        rp = np.zeros(n.value + 1, np.int64)
+        col = np.zeros(max(nnz.value, 1), np.int32)
+        check(lib.tcg_get_graph_csr(self._h, None, None, _ptr(rp), _ptr(col)))
+        return rp, col[:nnz.value]
+
     def set_template(self, t: TemplateTree) -> None:
         check(lib.tcg_set_template(self._h, t.k, _ptr(t._edge_array()), t.root))
         self.k = t.k
@@ -431,7 +447,7 @@ class Context:
         st = (N.TcgNodeStats * N.TCG_MAX_NODES)() if stats else None
         cl = np.ascontiguousarray(colors, dtype=np.uint8) if colors is not None else None
         if cl is not None and cl.shape[0] != self.n:
-            raise ParseError("coloring size does not match graph")
+            raise InvalidArgument("coloring size does not match graph")
         check(lib.tcg_run_coloring(self._h, seed, _ptr(cl) if cl is not None and cl.size else None,
                                    C.byref(total), _ptr(pv), st))
         return total.value, (pv[:self.n] if pv is not None else None), st
@@ -514,14 +530,14 @@ def _context(g: Graph, t: TemplateTree, cfg: EngineConfig) -> Context:
 
 def _require_b200(kind: EngineKind) -> None:
     if kind is not EngineKind.b200:
-        raise ParseError(f"engine '{kind.value}' is a reference CPU engine; this package "
+        raise InvalidArgument(f"engine '{kind.value}' is a reference CPU engine; this package "
                          "provides EngineKind.b200")
 
 
 def random_coloring(g: Graph, k: int, seed: int, device: int = 0) -> Coloring:
     """count_table.hpp:90-99, generated on the GPU (bit-exact MT19937-64)."""
     if k < 1:
-        raise ParseError("k must be >= 1")
+        raise InvalidArgument("k must be >= 1")
     ctx = _context(g, single_vertex_template() if k == 1 else
                    TemplateTree(k, [(i, i + 1) for i in range(k - 1)], 0), EngineConfig(device=device))
     return Coloring(ctx.coloring(seed), seed)
@@ -543,9 +559,9 @@ def run_iteration(kind: EngineKind, g: Graph, plan_or_template, coloring: Colori
     t = (plan_or_template if isinstance(plan_or_template, TemplateTree)
          else _template_of_plan(plan_or_template))
     if indexer is not None and indexer.k() != t.k:
-        raise ParseError("indexer and plan disagree on k")
+        raise InvalidArgument("indexer and plan disagree on k")
     if len(coloring.color) != g.n:
-        raise ParseError("coloring size does not match graph")
+        raise InvalidArgument("coloring size does not match graph")
     ctx = _context(g, t, cfg)
     total, pv, st = ctx.run_coloring(coloring.seed, coloring.color, per_vertex=cfg.keep_full_table,
                                      stats=True)
@@ -581,7 +597,7 @@ def estimate(g: Graph, t: TemplateTree, kind: EngineKind, iterations: int, seed:
     """estimator.hpp:49-93: colorings seed, seed+1, ...; scaled by 1/(aut * k!/k^k)."""
     _require_b200(kind)
     if iterations < 1:
-        raise ParseError("iterations must be >= 1")
+        raise InvalidArgument("iterations must be >= 1")
     cfg = cfg or EngineConfig()
     ctx = _context(g, t, cfg)
     plan, aut = ctx.plan()

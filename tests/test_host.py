@@ -77,10 +77,11 @@ def test_rmat_matches_oracle(scale, ef, probs, seed):
 
 
 def test_rmat_spec_validation():
-    with pytest.raises(T.ParseError):
-        T.generate_rmat(T.RmatSpec(0, 10, .25, .25, .25, .25, 1))
-    with pytest.raises(T.ParseError):
-        T.generate_rmat(T.RmatSpec(5, 10, .5, .25, .25, .25, 1))
+    # synthgen.hpp:40-46 throws std::invalid_argument (not parse_error)
+    for spec in (T.RmatSpec(0, 10, .25, .25, .25, .25, 1), T.RmatSpec(5, 10, .5, .25, .25, .25, 1)):
+        with pytest.raises(T.InvalidArgument) as ei:
+            T.generate_rmat(spec)
+        assert not isinstance(ei.value, T.ParseError)
 
 
 def test_template_validation():
@@ -159,9 +160,9 @@ def test_split_tables_match_oracle():
 
 def test_split_table_rejects_empty_child():
     ix = T.ColorIndexer(3)
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         T.build_split_table(2, 2, ix)
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         T.build_split_table(2, 0, ix)
 
 
@@ -169,11 +170,11 @@ def test_color_indexer():
     ix = T.ColorIndexer(3)
     assert ix.index_of([0, 1]) == 0 and ix.index_of([0, 2]) == 1 and ix.index_of([1, 2]) == 2
     assert ix.set_of(2, 2) == [1, 2]
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         ix.index_of([1, 1])
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         ix.set_of(3, 2)
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         T.ColorIndexer(21)
     assert T.ColorIndexer(20).binom(20, 10) == 184756
     for k in range(1, 11):
@@ -196,13 +197,13 @@ def test_engine_requires_gpu_or_fails_loudly():
     import torch
     if torch.cuda.is_available():
         pytest.skip("GPU present")
-    with pytest.raises((T.CudaError, T.ParseError)):
+    with pytest.raises((T.CudaError, T.InvalidArgument)):
         T.Context(0)
 
 
 def test_non_b200_engine_kinds_refused():
     g = T.from_edges([(0, 1)])
-    with pytest.raises(T.ParseError):
+    with pytest.raises(T.InvalidArgument):
         T.estimate(g, T.make_template([(0, 1)], 0), T.EngineKind.vectorized, 1, 1)
 
 
