@@ -14,6 +14,11 @@ Multi-GPU (torchrun, one rank per GPU): colorings are independent units, so
 every rank runs its own K colorings (seeds offset by rank) on a replica of the
 graph -- weak scaling, no data-path collective.  `value` is the whole-job
 per-coloring time: max-over-ranks device time / (N * K).
+With --shard (graphs whose tables outgrow one GPU: cfg4, cfg5 at 8 GPUs) every
+rank owns 1/N of the vertex rows and all ranks run the SAME K colorings
+jointly; each SpMM panel is all-gathered by the library's own NCCL
+communicator on a communication stream, prefetched one group ahead -- strong
+scaling, `value` = max-over-ranks device time / K.
 """
 from __future__ import annotations
 
@@ -32,6 +37,10 @@ METRIC = "per-coloring time and SpMM+eMA HBM GB/s (k=12/17 trees, R-MAT), 1/2/4/
 
 CONFIGS = {
     # name: (rmat spec (scale, edges, a, b, c, d, seed), template parent array, colorings per estimate)
+    # cfg1's graph (uniform random pairs from Rng(1)) is the CSR stored in
+    # tests/golden/cfg1.npz, built by the reference's from_edges (tests/golden/make_golden.py)
+    "cfg1": (None, [-1, 0, 1, 1, 3], 10,
+             "uniform random pairs n=16384, 8n draws (Rng(1)), k=5 tree (colorings batched on the device)"),
     "cfg2": ((20, 16 << 20, .57, .19, .19, .05, 1), [-1, 0, 0, 1, 1, 2, 2], 10,
              "R-MAT scale 20 ef16 (.57,.19,.19,.05), k=7 complete binary tree"),
     "cfg3": ((20, 100 << 20, .45, .15, .15, .25, 1), [-1, 0, 1, 2, 0, 4, 4, 6, 0, 8, 9, 9], 3,
@@ -155,19 +164,32 @@ def barrier(dist, local):
         pass
 
 
+def cfg1_csr():
+    import numpy as np
+    z = np.load(os.path.join(ROOT, "tests", "golden", "cfg1.npz"))
+    return 16384, z["row_ptr"], z["col"]
+
+
 def build_graph(spec):
     import paper_1903_04395_b200 as T
     t0 = time.perf_counter()
+    if spec is None:
+        n, rp, cl = cfg1_csr()
+        g = T.Graph.from_csr(n, rp, cl)
+        log(f"[bench] graph n={g.n} nnz={g.nnz()} (cfg1 CSR from tests/golden/cfg1.npz)")
+        return g
     g = T.generate_rmat(T.RmatSpec(*spec))
     log(f"[bench] graph n={g.n} nnz={g.nnz()} max_deg={g.max_degree} built in {time.perf_counter() - t0:.1f}s (host C++)")
     return g
 
 
-def bench_config(name, n, nnz, k, world):
+def bench_config(name, n, nnz, k, world, shard=False):
     """The `config` object of BOTH arms (identical, so the driver can pair them)."""
     csr_mb = (8 * (n + 1) + 4 * nnz) / 1e6
+    par = (f"vertex-sharded x{world} (library-owned NCCL all-gather of each SpMM panel)" if shard
+           else f"replicas x{world} (colorings)")
     return {"workload": f"{name}: {CONFIGS[name][3]}", "n": int(n), "nnz": int(nnz), "k": int(k),
-            "template_root": 0, "step": "1 coloring", "parallelism": f"replicas x{world} (colorings)",
+            "template_root": 0, "step": "1 coloring", "parallelism": par,
             "l2": "no flush: inputs larger than L2 (CSR %.0f MB + count tables vs 126 MB L2)" % csr_mb}
 
 
@@ -222,7 +244,11 @@ def run_reference(args, rank, world, local, dist):
         print(json.dumps({"impl": "reference", "unavailable": f"{type(ex).__name__}: {ex}"}))
         return
     t0 = time.perf_counter()
-    rg = O.RefGraph.rmat(*spec)
+    if spec is None:
+        n0, rp0, cl0 = cfg1_csr()
+        rg = O.RefGraph.from_csr(n0, rp0, cl0)
+    else:
+        rg = O.RefGraph.rmat(*spec)
     n, rp, _ = rg.csr()
     nnz = int(rp[-1])
     gsec = time.perf_counter() - t0
@@ -255,7 +281,7 @@ def run_reference(args, rank, world, local, dist):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": full_ms / args.steps,
         "higher_is_better": False, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic R-MAT from the reference's own generate_rmat (graph seed 1), coloring seed 1",
-        "config": bench_config(args.config, n, nnz, k, world),
+        "config": bench_config(args.config, n, nnz, k, world, args.shard),
         "cpu_baseline": {"value": full_ms, "unit": "ms/coloring", "cores": cores, "kind": "reference",
                          "sample": f"ONE FULL coloring (seed 1) of the unmodified reference vectorized engine "
                                    f"(oracle/_ref: random_coloring + IterationRun::run order, Z=16, fp64, "
@@ -280,12 +306,19 @@ def run_b200(args, rank, world, local, dist):
     spec, parents, ncol, desc = CONFIGS[args.config]
     g = build_graph(spec)
     t = T.template_from_parents(parents, 0)
-    ctx = T.Context(device=local)
+
+    def new_ctx():
+        c = T.Context(device=local)
+        if args.shard:  # vertex-sharded over the ranks: the library's own NCCL communicator
+            c.set_shard_nccl(rank, world)
+        return c
+    ctx = new_ctx()
     ctx.set_graph(g)
     ctx.set_template(t)
     need = ctx.required_device_bytes()
     log(f"[bench] rank {rank}: device bytes {need / 1e9:.2f} GB")
-    seed0 = rank_seeds(rank, args.warmup, args.steps)[0]
+    # replicas: disjoint colorings per rank; sharded: every rank runs the same colorings jointly
+    seed0 = 1 if args.shard else rank_seeds(rank, args.warmup, args.steps)[0]
     ctx.time(seed0, args.warmup, per_kernel=False)               # warm-up colorings
     barrier(dist, local)
     l0 = ctx.kernel_launches()
@@ -294,7 +327,7 @@ def run_b200(args, rank, world, local, dist):
     barrier(dist, local)
     launches = ctx.kernel_launches() - l0
     ms_max = allreduce_max(dist, tm.total_ms, local)
-    value = ms_max / (args.steps * world)
+    value = ms_max / (args.steps * (1 if args.shard else world))
 
     # end to end through the public C ABI with HOST buffers: one estimate()
     # call per step = H2D of the CSR + `ncol` colorings + D2H of the totals and
@@ -308,7 +341,7 @@ def run_b200(args, rank, world, local, dist):
         rp, cl = rp_t.numpy(), cl_t.numpy()
         rp[:] = g.csc_col_ptr
         cl[:] = g.csc_rows
-        ectx = T.Context(device=local)
+        ectx = new_ctx()
         ectx.set_template(t)
         ectx.set_graph_csr(g.n, rp, cl)
         ectx.estimate(1, ncol, per_vertex=True)                   # warm (allocations; not timed)
@@ -324,7 +357,7 @@ def run_b200(args, rank, world, local, dist):
         e_s = time.perf_counter() - t0
         barrier(dist, local)
         e_s = allreduce_max(dist, e_s, local)
-        e2e = {"value": e_s * 1e3 / (e_steps * ncol * world), "unit": "ms/coloring",
+        e2e = {"value": e_s * 1e3 / (e_steps * ncol * (1 if args.shard else world)), "unit": "ms/coloring",
                "h2d_bytes_per_step": int(rp.nbytes + cl.nbytes + 8),
                "d2h_bytes_per_step": int(8 * ncol + 8 * g.n),
                "colorings_per_step": ncol, "steps": e_steps, "step_ms": step_ms,
@@ -361,9 +394,10 @@ def run_b200(args, rank, world, local, dist):
     line = {
         "metric": METRIC, "value": value, "unit": "ms/coloring", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": False,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 tables, f64 accumulate/root",
+        "scaling": "strong" if args.shard else "weak", "vs_baseline": None,
+        "dtype": "f32 tables, f64 accumulate/root",
         "data": "synthetic R-MAT from the reference generator (graph seed 1), colorings seeds 1.. on device",
-        "config": bench_config(args.config, g.n, g.nnz(), len(parents), world),
+        "config": bench_config(args.config, g.n, g.nnz(), len(parents), world, args.shard),
         "device_bytes": need,
         "roofline": {"kernel": "spmm phase (bucket_rows + segment colour order + pair_expand + spmm_rooted + rooted_fixup)",
                      "bound": "hbm", "achieved": spmm_gbs, "peak": hbm_peak,
@@ -402,6 +436,9 @@ def main():
     ap.add_argument("--config", choices=sorted(CONFIGS), default=DEFAULT_CONFIG)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard", action="store_true",
+                    help="vertex-shard ONE coloring over the N ranks (NCCL all-gathers; cfg4/cfg5 at 8 GPUs) "
+                         "instead of replicas")
     args = ap.parse_args()
     if args.warmup < 3:
         log("[bench] warmup raised to 3 (timing rules)")

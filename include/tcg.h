@@ -240,6 +240,16 @@ typedef int (*tcg_allgather_fn)(void* user, const void* send, size_t bytes, void
 int tcg_set_shard_device(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user);
 /* Host transport (tests, any backend): send/recv are HOST buffers. */
 int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user);
+/* NCCL data plane owned by the library (production, one process per GPU):
+ * rank 0 calls tcg_nccl_unique_id, the caller hands the 128 bytes to every
+ * rank (any side channel: torch.distributed, MPI, a file), and each rank
+ * calls tcg_set_shard_nccl.  The library creates its own communicator
+ * (ncclCommInitRank over the process's NCCL, resolved at run time) and
+ * enqueues every panel all-gather on a communication stream, double-buffered
+ * against the SpMM of the previous group -- no host synchronization per panel. */
+#define TCG_NCCL_ID_BYTES 128
+int tcg_nccl_unique_id(uint8_t id[TCG_NCCL_ID_BYTES]);
+int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_NCCL_ID_BYTES]);
 
 /* Kernel launches issued by this context since creation (evidence for
  * bench.py's gpu_launches). */

@@ -25,6 +25,7 @@ TCG_OK, TCG_EINVAL, TCG_ERESOURCE, TCG_ECUDA, TCG_ENONFINITE, TCG_ELOGIC, TCG_EP
 TCG_MAX_K = 20
 TCG_MAX_NODES = 2 * TCG_MAX_K - 1
 TCG_KEEP_TABLES = 1
+TCG_NCCL_ID_BYTES = 128
 
 
 class TcgPlan(C.Structure):
@@ -98,6 +99,8 @@ _SIGS = {
     "tcg_shard_bounds": (C.c_int, [i32, vp, C.c_int, vp]),
     "tcg_set_shard_device": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "tcg_set_shard_host": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+    "tcg_nccl_unique_id": (C.c_int, [vp]),
+    "tcg_set_shard_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp]),
 }
 
 # int (*)(void* user, const void* send, size_t bytes, void* recv)

@@ -240,9 +240,9 @@ int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t
     // the reference's Graph invariants are the caller's contract here (as for
     // a treecount::Graph); row_ptr is checked on the host, ids / order / loops
     // on the device after the upload (O(nnz) there, no host copy)
-    if (n < 0 || row_ptr[0] != 0) throw tcg::invalid_argument("bad CSR row_ptr");
+    if (n < 0 || row_ptr[0] != 0) throw tcg::parse_error("bad CSR row_ptr");
     for (int32_t v = 0; v < n; ++v)
-      if (row_ptr[v + 1] < row_ptr[v]) throw tcg::invalid_argument("CSR row_ptr not monotone");
+      if (row_ptr[v + 1] < row_ptr[v]) throw tcg::parse_error("CSR row_ptr not monotone");
     if (row_ptr[n] > 0) need(col, "col");
     if (ctx->eng->sharded()) ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col, /*check_symmetry=*/false));
     else ctx->eng->set_graph_ptrs(n, row_ptr, col, /*validate=*/true);
@@ -382,6 +382,23 @@ int tcg_set_shard_device(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn,
     need(ctx, "ctx");
     if (!fn) throw tcg::invalid_argument("allgather callback is NULL");
     ctx->eng->set_shard(rank, world, tcg::make_device_transport(fn, user));
+  });
+}
+
+int tcg_nccl_unique_id(uint8_t id[TCG_NCCL_ID_BYTES]) {
+  return guarded([&] {
+    need(id, "id");
+    tcg::nccl_unique_id(id);
+  });
+}
+
+int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_NCCL_ID_BYTES]) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(id, "id");
+    if (world < 1 || rank < 0 || rank >= world) throw tcg::invalid_argument("bad shard rank/world");
+    cudaSetDevice(ctx->eng->device());
+    ctx->eng->set_shard(rank, world, tcg::make_nccl_transport(rank, world, id));
   });
 }
 

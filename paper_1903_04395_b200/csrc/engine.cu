@@ -244,7 +244,18 @@ Engine::~Engine() {
   dfree(d_seeds_);
   dfree(d_colors_);
   batch_.reset();
+  tr_.reset();  // (a communicator before its streams)
+  if (comm_) cudaStreamDestroy(comm_);
+  for (cudaEvent_t e : {ev_in_, ev_g_[0], ev_g_[1], ev_u_[0], ev_u_[1]})
+    if (e) cudaEventDestroy(e);
   if (stream_ && own_stream_) cudaStreamDestroy(stream_);
+}
+
+void Engine::ensure_comm() {
+  if (comm_) return;
+  TCG_CUDA(cudaStreamCreateWithFlags(&comm_, cudaStreamNonBlocking));
+  for (cudaEvent_t* e : {&ev_in_, &ev_g_[0], &ev_g_[1], &ev_u_[0], &ev_u_[1]})
+    TCG_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
 }
 
 void Engine::free_graph_buffers() {
@@ -280,6 +291,7 @@ void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the n
   sched_.clear();
   d_row_order_ = nullptr;  // (graph-prep block; d_tile_tot_ / d_counter_ are kept)
   dfree(d_xfull_);
+  dfree(d_xfull2_);
   dfree(d_colors_pad_);
   dfree(d_gather_);
   dfree(d_rows_);
@@ -387,6 +399,10 @@ void Engine::set_graph(const Csr& gin) {
   n_ = g.n;
   nnz_ = g.nnz();
   TCG_CUDA(cudaMalloc(&d_xfull_, sizeof(float) * dev::kZ * std::max<int64_t>(nsrc_, 1)));
+  if (tr_ && tr_->async()) {  // double buffer + communication stream (rooted_spmm prefetch)
+    TCG_CUDA(cudaMalloc(&d_xfull2_, sizeof(float) * dev::kZ * std::max<int64_t>(nsrc_, 1)));
+    ensure_comm();
+  }
   TCG_CUDA(cudaMalloc(&d_colors_pad_, std::max<int64_t>(nsrc_, 1)));
   // [0, 2048): this rank's totals chunk; [2048, 2048 * (world + 1)): gathered
   TCG_CUDA(cudaMalloc(&d_gather_, sizeof(double) * 2048 * (world_ + 1)));
@@ -1833,9 +1849,29 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
   const uint8_t* rowc = e.pair ? d_colors : nullptr;
   TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rooted_smem)));
   const int spw = 128 / zw;
+  // sharded + async transport (NCCL): group g+1's panel is all-gathered on the
+  // communication stream while group g's SpMM runs (two buffers; event
+  // ordering only, no host synchronization)
+  const bool pipe = sharded() && tr_->async();
+  float* xbuf[2] = {d_xfull_, d_xfull2_};
+  auto gather_async = [&](int g) {
+    const float* src = X + static_cast<int64_t>(g) * n_ * (e.pair ? zw : dev::kZ);
+    if (g >= 2) TCG_CUDA(cudaStreamWaitEvent(comm_, ev_u_[g % 2], 0));  // SpMM g-2 done reading the buffer
+    tr_->allgather(src, sizeof(float) * static_cast<size_t>(n_) * zw, xbuf[g % 2], comm_);
+    TCG_CUDA(cudaEventRecord(ev_g_[g % 2], comm_));
+  };
+  if (pipe && G > 0) {
+    TCG_CUDA(cudaEventRecord(ev_in_, stream_));  // the passive table is complete
+    TCG_CUDA(cudaStreamWaitEvent(comm_, ev_in_, 0));
+    gather_async(0);
+  }
   for (int g = 0; g < G; ++g) {
     const float* Xg = X + static_cast<int64_t>(g) * n_ * (e.pair ? zw : dev::kZ);
-    if (sharded()) {
+    if (pipe) {
+      if (g + 1 < G) gather_async(g + 1);
+      TCG_CUDA(cudaStreamWaitEvent(stream_, ev_g_[g % 2], 0));
+      Xg = xbuf[g % 2];
+    } else if (sharded()) {
       tr_->allgather(Xg, sizeof(float) * static_cast<size_t>(n_) * zw, d_xfull_, stream_);
       Xg = d_xfull_;
     }
@@ -1865,6 +1901,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
         ++launches_;
       }
     }
+    if (pipe) TCG_CUDA(cudaEventRecord(ev_u_[g % 2], stream_));
     if (out) {  // the group's P' columns are complete: scatter into the active-leaf output
       const int64_t total = static_cast<int64_t>(n_) * fpad;
       dev::pstream_copy<<<static_cast<unsigned>(std::min<int64_t>((total + 255) / 256, 148 * 64)), 256, 0, stream_>>>(

@@ -126,8 +126,14 @@ struct PartSchedule {
 // All-gather of equal-size per-rank device buffers (SpMM panels, totals).
 struct Transport {
   virtual ~Transport() = default;
+  // async() == true: the all-gather is only ENQUEUED on s (stream-ordered);
+  // otherwise recv is complete when allgather returns
+  virtual bool async() const { return false; }
   virtual void allgather(const void* d_send, size_t bytes, void* d_recv, cudaStream_t s) = 0;
 };
+void nccl_unique_id(uint8_t* out);   // TCG_NCCL_ID_BYTES bytes
+int nccl_version();
+std::unique_ptr<Transport> make_nccl_transport(int rank, int world, const uint8_t* id);
 std::unique_ptr<Transport> make_device_transport(tcg_allgather_fn fn, void* user);
 std::unique_ptr<Transport> make_host_transport(tcg_allgather_fn fn, void* user);
 void set_host_transport_world(Transport* t, int world);
@@ -138,6 +144,7 @@ class Engine {
  public:
   void set_shard(int rank, int world, std::unique_ptr<Transport> t);
   bool sharded() const { return world_ > 1 || static_cast<bool>(tr_); }
+  int device() const { return cfg_.device; }
   int32_t n_global() const { return nglob_; }
   explicit Engine(const tcg_config& cfg, cudaStream_t shared_stream = nullptr);
   ~Engine();
@@ -222,6 +229,10 @@ class Engine {
   int32_t nsrc_ = -1;                // rows of a gather source (world * nmax, or n)
   int64_t* d_rows_ = nullptr;        // rows_ on device
   float* d_xfull_ = nullptr;         // all-gathered panel (world * nmax * 32 floats)
+  float* d_xfull2_ = nullptr;        // second buffer: async (NCCL) transports prefetch group g+1
+  cudaStream_t comm_ = nullptr;      // communication stream of an async transport
+  cudaEvent_t ev_in_ = nullptr, ev_g_[2] = {nullptr, nullptr}, ev_u_[2] = {nullptr, nullptr};
+  void ensure_comm();
   uint8_t* d_colors_pad_ = nullptr;  // colors in padded-global order
   double* d_gather_ = nullptr;       // small all-gather scratch (totals)
   void gather_colors(const uint8_t* d_colors);

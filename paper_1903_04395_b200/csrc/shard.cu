@@ -1,9 +1,17 @@
 // shard.cu -- vertex sharding support: row partition and the
 // all-gather transports used by the sharded SpMM (engine.cu).
-// The collective itself is supplied by the caller (C ABI callback): PyTorch
-// torch.distributed (NCCL) on device pointers in production, gloo on host
-// buffers in tests.  (Calling NCCL directly from this statically-linked
-// runtime failed with cross-runtime stream errors; torch owns NCCL here.)
+//   * NcclTransport (production): the library owns an NCCL communicator
+//     (libnccl resolved with dlopen at run time -- the process's already
+//     loaded NCCL, e.g. PyTorch's, else TCG_NCCL_LIB / libnccl.so.2 -- so
+//     libtcg.so never links a second NCCL), and all-gathers are enqueued
+//     ASYNCHRONOUSLY on a communication stream: the sharded rooted SpMM
+//     prefetches group g+1's panel over NVLink/NVSwitch while group g's
+//     gathers run (engine.cu rooted_spmm).
+//   * DeviceTransport / HostTransport: a caller-supplied callback
+//     (torch.distributed on device pointers; gloo on host buffers in tests).
+
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdlib>
@@ -71,7 +79,81 @@ struct HostTransport : Transport {
   }
 };
 
+// ---------------------------------------------------------------- NCCL
+struct NcclApi {
+  void* h = nullptr;
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  ncclResult_t (*GetVersion)(int*) = nullptr;
+};
+
+const NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    // the NCCL already in the process (PyTorch's) first, then TCG_NCCL_LIB, then the soname
+    a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+    if (!a.h)
+      if (const char* p = std::getenv("TCG_NCCL_LIB")) a.h = dlopen(p, RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) a.h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+    if (!a.h) return a;
+    auto sym = [&](const char* n) { return dlsym(a.h, n); };
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(sym("ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(sym("ncclCommInitRank"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(sym("ncclAllGather"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(sym("ncclCommDestroy"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
+    a.GetVersion = reinterpret_cast<decltype(a.GetVersion)>(sym("ncclGetVersion"));
+    return a;
+  }();
+  if (!api.h || !api.GetUniqueId || !api.CommInitRank || !api.AllGather || !api.CommDestroy)
+    throw cuda_error("NCCL not available (set TCG_NCCL_LIB to libnccl.so.2)");
+  return api;
+}
+
+void nccl_check(ncclResult_t r, const char* what) {
+  if (r != ncclSuccess)
+    throw cuda_error(std::string(what) + ": " + (nccl().GetErrorString ? nccl().GetErrorString(r) : "nccl error"));
+}
+
+struct NcclTransport : Transport {
+  ncclComm_t comm = nullptr;
+  int world = 1;
+  NcclTransport(int rank, int w, const uint8_t* id_bytes) : world(w) {
+    ncclUniqueId id;
+    static_assert(sizeof(id) == TCG_NCCL_ID_BYTES, "ncclUniqueId size");
+    std::memcpy(&id, id_bytes, sizeof(id));
+    nccl_check(nccl().CommInitRank(&comm, w, id, rank), "ncclCommInitRank");
+  }
+  ~NcclTransport() override {
+    if (comm) nccl().CommDestroy(comm);
+  }
+  bool async() const override { return true; }
+  // enqueued on s: recv is complete in stream order (no host sync)
+  void allgather(const void* d_send, size_t bytes, void* d_recv, cudaStream_t s) override {
+    nccl_check(nccl().AllGather(d_send, d_recv, bytes, ncclChar, comm, s), "ncclAllGather");
+  }
+};
+
 }  // namespace
+
+void nccl_unique_id(uint8_t* out) {
+  ncclUniqueId id;
+  nccl_check(nccl().GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(out, &id, sizeof(id));
+}
+
+int nccl_version() {
+  int v = 0;
+  if (nccl().GetVersion) nccl().GetVersion(&v);
+  return v;
+}
+
+std::unique_ptr<Transport> make_nccl_transport(int rank, int world, const uint8_t* id) {
+  return std::make_unique<NcclTransport>(rank, world, id);
+}
 
 std::unique_ptr<Transport> make_device_transport(tcg_allgather_fn fn, void* user) {
   return std::make_unique<DeviceTransport>(fn, user);

@@ -381,6 +381,30 @@ class Context:
         self._allgather_cb = N.ALLGATHER_FN(fn)  # keep alive
         check(lib.tcg_set_shard_device(self._h, rank, world, C.cast(self._allgather_cb, C.c_void_p), None))
 
+    def set_shard_nccl(self, rank: int, world: int, exchange=None) -> None:
+        """The library's own NCCL data plane (tcg_set_shard_nccl): rank 0 creates
+        the NCCL unique id, `exchange(id_bytes_or_None) -> id_bytes` hands it to
+        every rank (default: torch.distributed.broadcast_object_list over the
+        default process group), and each rank's context builds its
+        communicator; panel all-gathers then run asynchronously on the
+        library's communication stream."""
+        _nccl_env()
+        ident = None
+        if rank == 0:
+            buf = (C.c_uint8 * N.TCG_NCCL_ID_BYTES)()
+            check(lib.tcg_nccl_unique_id(buf))
+            ident = bytes(buf)
+        if world > 1:
+            if exchange is None:
+                import torch.distributed as dist
+                box = [ident]
+                dist.broadcast_object_list(box, src=0)
+                ident = box[0]
+            else:
+                ident = exchange(ident)
+        buf = (C.c_uint8 * N.TCG_NCCL_ID_BYTES).from_buffer_copy(ident)
+        check(lib.tcg_set_shard_nccl(self._h, rank, world, buf))
+
     def set_shard_host(self, rank: int, world: int, allgather) -> None:
         """Host transport: allgather(send: bytes-like np.uint8 array) -> np.uint8
         array of world*len(send) bytes in rank order (e.g. gloo)."""
@@ -500,6 +524,24 @@ class Context:
         totals = np.zeros(count, np.float64)
         check(lib.tcg_time_colorings(self._h, seed, count, int(per_kernel), _ptr(totals), C.byref(tm)))
         return tm, totals
+
+
+def _nccl_env() -> None:
+    """Point the library at the NCCL this Python environment ships (PyTorch's
+    nvidia-nccl wheel) unless TCG_NCCL_LIB is set; an NCCL already loaded in
+    the process is preferred by the library itself."""
+    import os
+    if os.environ.get("TCG_NCCL_LIB"):
+        return
+    try:
+        import nvidia.nccl
+        for d in nvidia.nccl.__path__:
+            p = os.path.join(d, "lib", "libnccl.so.2")
+            if os.path.exists(p):
+                os.environ["TCG_NCCL_LIB"] = p
+                return
+    except ImportError:
+        pass
 
 
 def shard_bounds(g: Graph, world: int) -> np.ndarray:

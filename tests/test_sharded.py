@@ -178,3 +178,40 @@ def test_sharded_two_ranks_host_transport(name):
     c.set_template(T.template_from_parents(parents, 0))
     t1, _, _ = c.run_coloring(9)
     assert abs(t1 - out[0][1]) <= 1e-6 * t1
+
+
+def _nccl_owned_worker(q):
+    import paper_1903_04395_b200 as TT
+    out = []
+    g = TT.generate_rmat(TT.RmatSpec(12, 32 << 12, .45, .15, .15, .25, 6))
+    for name in ("cfg2", "cfg3"):
+        c = TT.Context(0)
+        c.set_shard_nccl(0, 1)  # the library's own communicator (world 1: no exchange)
+        c.set_graph(g)
+        c.set_template(TT.template_from_parents(CFG_TEMPLATES[name], 0))
+        total, pv, _ = c.run_coloring(4, per_vertex=True)
+        totals, _, _, _ = c.estimate(4, 2)
+        out.append((name, total, pv, list(totals)))
+    q.put(out)
+
+
+@pytest.mark.gpu
+def test_sharded_world1_library_nccl():
+    """tcg_set_shard_nccl: the library-owned NCCL communicator (dlopen'd NCCL,
+    async all-gathers on the comm stream, group g+1 prefetched while group g's
+    SpMM runs) -- k=12 has 6+ compressed groups per SpMM, so the double buffer
+    and its events are exercised -- against the oracle."""
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    p = ctx.Process(target=_nccl_owned_worker, args=(q,))
+    p.start()
+    out = _get(q, [p])
+    p.join(timeout=120)
+    assert p.exitcode == 0
+    g = T.generate_rmat(T.RmatSpec(12, 32 << 12, .45, .15, .15, .25, 6))
+    for name, total, pv, totals in out:
+        ot, opv, _ = _ref(g, CFG_TEMPLATES[name], 4)
+        assert abs(total - ot) <= 1e-4 * ot, name
+        assert np.max(np.abs(pv - opv) / np.maximum(opv, 1)) <= 1e-4, name
+        assert totals[0] == total
