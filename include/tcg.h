@@ -142,6 +142,16 @@ typedef struct {
 } tcg_node_stats;
 
 int tcg_create(const tcg_config* cfg, tcg_ctx** out);
+/* One context over several GPUs of this process (the reference's
+ * run_iteration/estimate use the whole machine through their WorkerPool,
+ * engines.hpp:302-307): every device holds the graph and the template, and
+ * tcg_estimate / tcg_time_colorings spread the colorings seed+i over the
+ * devices in contiguous chunks (one host thread per device, no collective;
+ * totals in i order, the reference's estimator arithmetic).  Single-coloring
+ * and inspection calls run on device_ids[0].  Graphs too large for one GPU
+ * are vertex-sharded instead: one context per rank + tcg_set_shard_nccl. */
+int tcg_create_multi(const tcg_config* cfg, const int* device_ids, int ndev, tcg_ctx** out);
+int tcg_device_count_of(const tcg_ctx* ctx);
 void tcg_destroy(tcg_ctx* ctx);
 
 /* Upload the graph (copied host -> device; builds the SpMM row schedule). */

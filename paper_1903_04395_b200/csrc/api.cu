@@ -4,6 +4,9 @@
 // SURVEY 8(b)); no C++ exception crosses the ABI.
 #include <cstring>
 #include <memory>
+#include <thread>
+#include <cmath>
+#include <exception>
 #include <string>
 
 #include "../../include/tcg.h"
@@ -14,6 +17,9 @@ struct tcg_graph {
 };
 struct tcg_ctx {
   std::unique_ptr<tcg::Engine> eng;
+  // multi-device context (tcg_create_multi): one engine per further device;
+  // graph / template go to every engine, colorings are spread over them
+  std::vector<std::unique_ptr<tcg::Engine>> peers;
 };
 
 namespace {
@@ -53,6 +59,37 @@ int guarded(F&& f) {
 
 void need(const void* p, const char* what) {
   if (!p) throw tcg::invalid_argument(std::string(what) + " is NULL");
+}
+
+// f(engine, index) on every engine of the context, one host thread per
+// device (each engine sets its own device); the first failure is rethrown
+template <typename F>
+void for_all(tcg_ctx* ctx, F&& f) {
+  if (ctx->peers.empty()) {
+    f(*ctx->eng, 0);
+    return;
+  }
+  const size_t nd = ctx->peers.size() + 1;
+  std::vector<std::exception_ptr> err(nd);
+  std::vector<std::thread> th;
+  for (size_t d = 0; d < nd; ++d)
+    th.emplace_back([&, d] {
+      try {
+        f(d == 0 ? *ctx->eng : *ctx->peers[d - 1], static_cast<int>(d));
+      } catch (...) {
+        err[d] = std::current_exception();
+      }
+    });
+  for (auto& t : th) t.join();
+  for (auto& e : err)
+    if (e) std::rethrow_exception(e);
+}
+
+// colorings [0, count) split into contiguous per-device chunks
+std::vector<int> chunks_of(int count, size_t nd) {
+  std::vector<int> b(nd + 1);
+  for (size_t d = 0; d <= nd; ++d) b[d] = static_cast<int>(static_cast<int64_t>(count) * d / nd);
+  return b;
 }
 
 void fill_plan(const tcg::Plan& p, tcg_plan* out) {
@@ -231,6 +268,26 @@ int tcg_create(const tcg_config* cfg, tcg_ctx** out) {
   });
 }
 
+int tcg_create_multi(const tcg_config* cfg, const int* device_ids, int ndev, tcg_ctx** out) {
+  return guarded([&] {
+    need(out, "out");
+    need(device_ids, "device_ids");
+    if (ndev < 1) throw tcg::invalid_argument("ndev must be >= 1");
+    tcg_config c{};
+    if (cfg) c = *cfg;
+    auto ctx = std::make_unique<tcg_ctx>();
+    c.device = device_ids[0];
+    ctx->eng = std::make_unique<tcg::Engine>(c);
+    for (int d = 1; d < ndev; ++d) {
+      c.device = device_ids[d];
+      ctx->peers.push_back(std::make_unique<tcg::Engine>(c));
+    }
+    *out = ctx.release();
+  });
+}
+
+int tcg_device_count_of(const tcg_ctx* ctx) { return ctx ? static_cast<int>(ctx->peers.size()) + 1 : 0; }
+
 void tcg_destroy(tcg_ctx* ctx) { delete ctx; }
 
 int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t* col) {
@@ -245,7 +302,7 @@ int tcg_set_graph(tcg_ctx* ctx, int32_t n, const int64_t* row_ptr, const int32_t
       if (row_ptr[v + 1] < row_ptr[v]) throw tcg::parse_error("CSR row_ptr not monotone");
     if (row_ptr[n] > 0) need(col, "col");
     if (ctx->eng->sharded()) ctx->eng->set_graph(tcg::csr_adopt(n, row_ptr, col, /*check_symmetry=*/false));
-    else ctx->eng->set_graph_ptrs(n, row_ptr, col, /*validate=*/true);
+    else for_all(ctx, [&](tcg::Engine& e, int) { e.set_graph_ptrs(n, row_ptr, col, /*validate=*/true); });
   });
 }
 
@@ -253,7 +310,7 @@ int tcg_set_graph_handle(tcg_ctx* ctx, const tcg_graph* g) {
   return guarded([&] {
     need(ctx, "ctx");
     need(g, "graph");
-    ctx->eng->set_graph(g->csr);
+    for_all(ctx, [&](tcg::Engine& e, int) { e.set_graph(g->csr); });
   });
 }
 
@@ -261,7 +318,7 @@ int tcg_set_template(tcg_ctx* ctx, int k, const int32_t* edges, int root) {
   return guarded([&] {
     need(ctx, "ctx");
     if (k > 1) need(edges, "edges");
-    ctx->eng->set_template(k, edges, root);
+    for_all(ctx, [&](tcg::Engine& e, int) { e.set_template(k, edges, root); });
   });
 }
 
@@ -305,8 +362,41 @@ int tcg_estimate(tcg_ctx* ctx, uint64_t seed, int iterations, double* rooted_tot
     need(rooted_totals, "rooted_totals");
     need(estimate, "estimate");
     need(stderr_of_mean, "stderr_of_mean");
-    ctx->eng->estimate(seed, iterations, rooted_totals, estimate, stderr_of_mean,
-                       per_vertex_estimate);
+    if (ctx->peers.empty()) {
+      ctx->eng->estimate(seed, iterations, rooted_totals, estimate, stderr_of_mean, per_vertex_estimate);
+      return;
+    }
+    // colorings seed + i spread over the devices in contiguous chunks; totals
+    // land in i order, the estimator arithmetic is the reference's
+    if (iterations < 1) throw tcg::invalid_argument("iterations must be >= 1");
+    const size_t nd = ctx->peers.size() + 1;
+    const std::vector<int> b = chunks_of(iterations, nd);
+    const int32_t n = ctx->eng->n_global();
+    std::vector<std::vector<double>> pv(nd);
+    for_all(ctx, [&](tcg::Engine& e, int d) {
+      const int cnt = b[d + 1] - b[d];
+      if (cnt == 0) return;
+      double est = 0, se = 0;
+      if (per_vertex_estimate) pv[d].assign(static_cast<size_t>(std::max(n, 0)), 0.0);
+      e.estimate(seed + static_cast<uint64_t>(b[d]), cnt, rooted_totals + b[d], &est, &se,
+                 per_vertex_estimate ? pv[d].data() : nullptr);
+    });
+    double mean = 0.0;  // estimator.hpp:80-91
+    for (int i = 0; i < iterations; ++i) mean += rooted_totals[i];
+    mean /= static_cast<double>(iterations);
+    double var = 0.0;
+    for (int i = 0; i < iterations; ++i) var += (rooted_totals[i] - mean) * (rooted_totals[i] - mean);
+    const double scale = 1.0 / (static_cast<double>(ctx->eng->aut()) * tcg::colorful_probability(ctx->eng->plan().k));
+    *estimate = mean * scale;
+    *stderr_of_mean = iterations > 1 ? std::sqrt(var / (static_cast<double>(iterations) *
+                                                        static_cast<double>(iterations - 1))) * scale : 0.0;
+    if (per_vertex_estimate)
+      for (int32_t v = 0; v < n; ++v) {
+        double s = 0.0;  // device (= coloring) order
+        for (size_t d = 0; d < nd; ++d)
+          if (!pv[d].empty()) s += pv[d][v] * (b[d + 1] - b[d]);
+        per_vertex_estimate[v] = s / iterations;
+      }
   });
 }
 
@@ -331,7 +421,7 @@ int tcg_set_graph_edges(tcg_ctx* ctx, const int32_t* edges, int64_t m, int32_t n
   return guarded([&] {
     need(ctx, "ctx");
     if (m > 0) need(edges, "edges");
-    ctx->eng->set_graph_edges(edges, m, n_hint);
+    for_all(ctx, [&](tcg::Engine& e, int) { e.set_graph_edges(edges, m, n_hint); });
   });
 }
 
@@ -355,7 +445,7 @@ int tcg_spmm_rooted(tcg_ctx* ctx, int k, int s, int pair, const uint8_t* colors,
 int tcg_set_rejection_limit(tcg_ctx* ctx, uint64_t limit) {
   return guarded([&] {
     need(ctx, "ctx");
-    ctx->eng->set_rejection_limit(limit);
+    for_all(ctx, [&](tcg::Engine& e, int) { e.set_rejection_limit(limit); });
   });
 }
 
@@ -364,7 +454,36 @@ int tcg_time_colorings(tcg_ctx* ctx, uint64_t seed, int count, int per_kernel, d
   return guarded([&] {
     need(ctx, "ctx");
     need(out, "out");
-    ctx->eng->time_colorings(seed, count, per_kernel != 0, totals, out);
+    if (ctx->peers.empty()) {
+      ctx->eng->time_colorings(seed, count, per_kernel != 0, totals, out);
+      return;
+    }
+    // devices time their chunks concurrently: total = the slowest device
+    if (count < 1) throw tcg::invalid_argument("count must be >= 1");
+    const size_t nd = ctx->peers.size() + 1;
+    const std::vector<int> b = chunks_of(count, nd);
+    std::vector<tcg_timing> t(nd);
+    std::vector<double> tot(static_cast<size_t>(count));
+    for_all(ctx, [&](tcg::Engine& e, int d) {
+      if (b[d + 1] > b[d])
+        e.time_colorings(seed + static_cast<uint64_t>(b[d]), b[d + 1] - b[d], per_kernel != 0, tot.data() + b[d], &t[d]);
+    });
+    tcg_timing r{};
+    for (const auto& x : t) {
+      r.total_ms = std::max(r.total_ms, x.total_ms);
+      r.spmm_ms = std::max(r.spmm_ms, x.spmm_ms);
+      r.ema_ms = std::max(r.ema_ms, x.ema_ms);
+      r.spmm_launches += x.spmm_launches;
+      r.ema_launches += x.ema_launches;
+      r.launches += x.launches;
+      r.spmm_alg_bytes += x.spmm_alg_bytes;
+      r.hist_alg_bytes += x.hist_alg_bytes;
+      r.ema_alg_bytes += x.ema_alg_bytes;
+      r.ema_flops += x.ema_flops;
+      r.spmm_gathered_bytes += x.spmm_gathered_bytes;
+    }
+    *out = r;
+    if (totals) std::copy(tot.begin(), tot.end(), totals);
   });
 }
 
@@ -380,6 +499,7 @@ int tcg_shard_bounds(int32_t n, const int64_t* row_ptr, int world, int64_t* boun
 int tcg_set_shard_device(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user) {
   return guarded([&] {
     need(ctx, "ctx");
+    if (!ctx->peers.empty()) throw tcg::invalid_argument("a multi-device context spreads colorings; shard with one context per rank");
     if (!fn) throw tcg::invalid_argument("allgather callback is NULL");
     ctx->eng->set_shard(rank, world, tcg::make_device_transport(fn, user));
   });
@@ -395,6 +515,7 @@ int tcg_nccl_unique_id(uint8_t id[TCG_NCCL_ID_BYTES]) {
 int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_NCCL_ID_BYTES]) {
   return guarded([&] {
     need(ctx, "ctx");
+    if (!ctx->peers.empty()) throw tcg::invalid_argument("a multi-device context spreads colorings; shard with one context per rank");
     need(id, "id");
     if (world < 1 || rank < 0 || rank >= world) throw tcg::invalid_argument("bad shard rank/world");
     cudaSetDevice(ctx->eng->device());
@@ -405,6 +526,7 @@ int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_N
 int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user) {
   return guarded([&] {
     need(ctx, "ctx");
+    if (!ctx->peers.empty()) throw tcg::invalid_argument("a multi-device context spreads colorings; shard with one context per rank");
     if (!fn) throw tcg::invalid_argument("allgather callback is NULL");
     auto t = tcg::make_host_transport(fn, user);
     tcg::set_host_transport_world(t.get(), world);
@@ -412,6 +534,11 @@ int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, v
   });
 }
 
-int64_t tcg_kernel_launches(const tcg_ctx* ctx) { return ctx ? ctx->eng->launches() : -1; }
+int64_t tcg_kernel_launches(const tcg_ctx* ctx) {
+  if (!ctx) return -1;
+  int64_t s = ctx->eng->launches();
+  for (const auto& p : ctx->peers) s += p->launches();
+  return s;
+}
 
 }  // extern "C"

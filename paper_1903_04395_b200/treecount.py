@@ -339,14 +339,20 @@ class Coloring:  # count_table.hpp:85-88
 
 
 class Context:
-    """One device engine (tcg_ctx): graph + template resident on one GPU."""
+    """One device engine (tcg_ctx): graph + template resident on one GPU, or --
+    with `devices=[...]` (tcg_create_multi) -- on several GPUs of this process,
+    colorings of estimate()/time() spread over them."""
 
-    def __init__(self, device: int = 0, memory_budget: int = 0, keep_tables: bool = False):
+    def __init__(self, device: int = 0, memory_budget: int = 0, keep_tables: bool = False, devices=None):
         cfg = N.TcgConfig()
         cfg.device, cfg.memory_budget = device, memory_budget
         cfg.flags = N.TCG_KEEP_TABLES if keep_tables else 0
         h = C.c_void_p()
-        check(lib.tcg_create(C.byref(cfg), C.byref(h)))
+        if devices is not None:
+            ids = (C.c_int * len(devices))(*devices)
+            check(lib.tcg_create_multi(C.byref(cfg), ids, len(devices), C.byref(h)))
+        else:
+            check(lib.tcg_create(C.byref(cfg), C.byref(h)))
         self._h = h
         self._fin = weakref.finalize(self, lib.tcg_destroy, h)
         self.n = None

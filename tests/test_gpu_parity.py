@@ -572,3 +572,24 @@ def test_device_from_edges_rmat_scale():
     c.set_graph_edges(np.random.default_rng(0).permutation(e), g.n)
     rp, col = c.graph_csr()
     assert np.array_equal(rp, g.csc_col_ptr) and np.array_equal(col, g.csc_rows)
+
+
+# ------------------------------------------------------ multi-device context
+def test_multi_device_context_spreads_colorings():
+    """tcg_create_multi: one context over several devices (here device 0 twice:
+    two independent engines, no collective) -- estimate() spreads colorings
+    seed+i over them; totals equal the single-device context's bit for bit."""
+    g = T.generate_rmat(T.RmatSpec(14, 16 << 14, .45, .15, .15, .25, 2))
+    t = T.template_from_parents(CFG_TEMPLATES["cfg3"], 0)
+    one = ctx_for(g, t)
+    multi = T.Context(devices=[0, 0])
+    multi.set_graph(g)
+    multi.set_template(t)
+    for iters in (1, 2, 5):
+        a = one.estimate(3, iters, per_vertex=True)
+        b = multi.estimate(3, iters, per_vertex=True)
+        assert a[0].tolist() == b[0].tolist()
+        assert rel_err([b[1]], [a[1]]) <= 1e-12 and rel_err([b[2]], [a[2]]) <= 1e-12 or iters == 1
+        assert_close(b[3], a[3], 1e-12)
+    tm, totals = multi.time(7, 4)
+    assert totals.tolist() == one.estimate(7, 4)[0].tolist()
