@@ -283,6 +283,9 @@ void Engine::free_graph_buffers() {
   colors_rl_cap_ = 0;
   dfree(d_pv_out_);
   pv_out_cap_ = 0;
+  dfree(d_urp_);
+  dfree(d_ucol_);
+  urp_cap_ = ucol_cap_ = 0;
 }
 
 void Engine::release_graph() {  // (d_row_ptr_ / d_col_ stay allocated for the next graph)
@@ -2431,44 +2434,47 @@ int Engine::pick_batch(int count) const {
 // The engine over the B-fold union of this engine's (internal) graph, same
 // template, same stream; rebuilt when the graph, the template or B changes.
 Engine* Engine::batch_engine(int B) {
-  if (batch_ && batch_copies_ == 1 && batch_->batch_copies_ == B && batch_graph_gen_ == graph_gen_ &&
-      batch_tpl_gen_ == tpl_gen_)
-    return batch_.get();
-  batch_.reset();
-  tcg_config c = cfg_;
-  c.flags &= ~TCG_KEEP_TABLES;
-  c.memory_budget = 0;
-  auto be = std::make_unique<Engine>(c, stream_);
-  be->no_relabel_ = true;
-  be->batch_copies_ = B;
-  be->limit_override_ = limit_override_;
-  const int64_t nU = static_cast<int64_t>(n_) * B, eU = nnz_ * B;
-  int64_t* rpU = nullptr;
-  int32_t* colU = nullptr;
-  try {
-    TCG_CUDA(cudaMalloc(&rpU, sizeof(int64_t) * (nU + 1)));
-    TCG_CUDA(cudaMalloc(&colU, sizeof(int32_t) * std::max<int64_t>(eU, 1)));
-    dev::union_graph<<<148 * 4, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, nnz_, B, rpU, colU);
-    TCG_CUDA(cudaGetLastError());
+  if (!batch_ || batch_->batch_copies_ != B || batch_tpl_gen_ != tpl_gen_) {
+    batch_.reset();
+    tcg_config c = cfg_;
+    c.flags &= ~TCG_KEEP_TABLES;
+    c.memory_budget = 0;
+    auto be = std::make_unique<Engine>(c, stream_);
+    be->no_relabel_ = true;
+    be->batch_copies_ = B;
+    be->limit_override_ = limit_override_;
     std::vector<int32_t> edges;
     for (const auto& pr : tpl_.edges) {
       edges.push_back(pr.first);
       edges.push_back(pr.second);
     }
     be->set_template(tpl_.k, edges.data(), tpl_.root);
-    be->set_graph_ptrs(static_cast<int32_t>(nU), rpU, colU, false, eU);
-    be->ensure_arena();
-  } catch (...) {
-    dfree(rpU);
-    dfree(colU);
-    throw;
+    batch_ = std::move(be);
+    batch_tpl_gen_ = tpl_gen_;
+    batch_graph_gen_ = ~0ull;
   }
-  TCG_CUDA(cudaStreamSynchronize(stream_));
-  dfree(rpU);
-  dfree(colU);
-  batch_ = std::move(be);
-  batch_graph_gen_ = graph_gen_;
-  batch_tpl_gen_ = tpl_gen_;
+  if (batch_graph_gen_ != graph_gen_) {
+    // the union of this graph's copies, built on the device in scratch kept
+    // across graphs (e2e: a new CSR per call), then handed to the batch engine
+    const int64_t nU = static_cast<int64_t>(n_) * B, eU = nnz_ * B;
+    if (urp_cap_ < nU + 1) {
+      dfree(d_urp_);
+      urp_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&d_urp_, sizeof(int64_t) * (nU + 1)));
+      urp_cap_ = nU + 1;
+    }
+    if (ucol_cap_ < std::max<int64_t>(eU, 1)) {
+      dfree(d_ucol_);
+      ucol_cap_ = 0;
+      TCG_CUDA(cudaMalloc(&d_ucol_, sizeof(int32_t) * std::max<int64_t>(eU, 1)));
+      ucol_cap_ = std::max<int64_t>(eU, 1);
+    }
+    dev::union_graph<<<148 * 4, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, nnz_, B, d_urp_, d_ucol_);
+    TCG_CUDA(cudaGetLastError());
+    batch_->set_graph_ptrs(static_cast<int32_t>(nU), d_urp_, d_ucol_, false, eU);
+    batch_->ensure_arena();
+    batch_graph_gen_ = graph_gen_;
+  }
   return batch_.get();
 }
 

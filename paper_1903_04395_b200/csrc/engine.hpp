@@ -199,6 +199,9 @@ class Engine {
   bool own_stream_ = true;
   uint64_t graph_gen_ = 0, tpl_gen_ = 0, batch_graph_gen_ = ~0ull, batch_tpl_gen_ = ~0ull;
   int pick_batch(int count) const;
+  int64_t* d_urp_ = nullptr;         // union CSR scratch (kept across graphs)
+  int32_t* d_ucol_ = nullptr;
+  int64_t urp_cap_ = 0, ucol_cap_ = 0;
   Engine* batch_engine(int B);
   // B colorings (caller order, nglob_ bytes each) -> totals[B], acc (nullable) += per-vertex
   void run_batch(const uint8_t* d_colors, int B, double* d_totals, double* d_acc);
