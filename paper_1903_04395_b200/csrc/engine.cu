@@ -604,7 +604,7 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   if (!d_counter_) TCG_CUDA(cudaMalloc(&d_counter_, 64));
   const auto t3 = now();
   const int64_t ntiles = (n_ + dev::kTileV - 1) / dev::kTileV;
-  ensure_tile_tot(ntiles);
+  ensure_tile_tot(std::max<int64_t>(ntiles, static_cast<int64_t>(batch_copies_) * dev::kRootChunks));
   TCG_CUDA(cudaStreamSynchronize(stream_));
   const auto t4 = now();
   if (have_template_) plan_arena();
@@ -1320,7 +1320,10 @@ void Engine::setup_rooted_ema(int max_smem) {
           std::vector<dev::GroupDesc> gr;
           std::vector<dev::BlockDesc> bl;
           if (e.rt_vtx) {  // vertex-per-CTA: the widest H1 the (k-1) colors allow (<= 8)
-            e.rtv_h = std::max(dev::kH1, std::min(6, k - 1));
+            // H = 6 (measured on cfg5 node 1 / node 2 eMA, H = 6 / 7 / 8: 308 / 433 / 353 ms
+            // and 120 / 167 / 321 ms -- 8 with the larger operand set streamed from
+            // shared memory)
+            e.rtv_h = dev::kH1;
             build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl, e.rtv_h, 16);
             std::vector<uint2> b2(bl.size());  // packed 8 B descriptors
             for (size_t i = 0; i < bl.size(); ++i)
@@ -1989,7 +1992,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
       dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
-      auto kern = e.rtv_h == 8 ? dev::ema_rtv_blocked<8> : e.rtv_h == 7 ? dev::ema_rtv_blocked<7> : dev::ema_rtv_blocked<6>;
+      auto kern = dev::ema_rtv_blocked<6>;
       attr(reinterpret_cast<const void*>(kern));
       kern<<<vgrid, 256, e.rt_smem, stream_>>>(
           A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
@@ -2261,9 +2264,11 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
   if (n_ > 0 && !exec_.empty() && d_total) {
     // fixed-shape fp64 sum of the per-vertex root counts (internal row order;
     // one segment per copy when this is a batch engine)
-    dev::root_reduce<<<batch_copies_, 1024, 0, stream_>>>(reinterpret_cast<const double*>(arena_ + exec_.back().out_off),
-                                                          n_ / batch_copies_, d_total);
-    ++launches_;
+    ensure_tile_tot(static_cast<int64_t>(batch_copies_) * dev::kRootChunks);
+    dev::root_partial<<<batch_copies_ * dev::kRootChunks, 256, 0, stream_>>>(
+        reinterpret_cast<const double*>(arena_ + exec_.back().out_off), n_ / batch_copies_, d_tile_tot_);
+    dev::root_reduce<<<batch_copies_, 64, 0, stream_>>>(d_tile_tot_, dev::kRootChunks, d_total);
+    launches_ += 2;
   } else if (d_total) {
     TCG_CUDA(cudaMemsetAsync(d_total, 0, sizeof(double), stream_));
   }

@@ -1409,10 +1409,29 @@ ema_root(const float* __restrict__ Am, const float* __restrict__ Pm,
 
 // Deterministic fp64 sum of the per-tile totals (engines.hpp:125-129; the
 // reference's sequential sum differs only at the 1e-16 level).
-// Segment blockIdx.x of x (len values each) -> total[blockIdx.x]: per-vertex
-// root counts in internal row order, a fixed-shape tree (1024 strided
-// partial sums, then a halving tree), so a coloring's total does not depend
-// on whether it ran alone or as one copy of a batch.
+// Per-vertex root counts (internal row order) of segment s (len values each;
+// one segment per copy of a batch) -> total[s], in a fixed shape that only
+// depends on len -- so a coloring's total does not depend on whether it ran
+// alone or as one copy of a batch: CTA (s, c) of kRootChunks sums its
+// contiguous chunk (256 strided partials + a halving tree) into part[], then
+// root_reduce folds the kRootChunks partials of each segment in order.
+constexpr int kRootChunks = 64;
+__global__ void __launch_bounds__(256)
+root_partial(const double* __restrict__ x, int64_t len, double* __restrict__ part) {
+  __shared__ double red[256];
+  const int64_t seg = blockIdx.x / kRootChunks, c = blockIdx.x % kRootChunks;
+  const int64_t b = len * c / kRootChunks, e = len * (c + 1) / kRootChunks;
+  const double* xs = x + seg * len;
+  double s = 0;
+  for (int64_t i = b + threadIdx.x; i < e; i += blockDim.x) s += xs[i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = red[0];
+}
 __global__ void root_reduce(const double* __restrict__ x, int64_t len,
                             double* __restrict__ total) {
   __shared__ double red[1024];
