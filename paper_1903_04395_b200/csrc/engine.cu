@@ -214,6 +214,7 @@ Engine::Engine(const tcg_config& cfg, cudaStream_t shared_stream) : cfg_(cfg) {
   TCG_CUDA(cudaSetDevice(cfg.device));
   cudaDeviceProp prop;
   TCG_CUDA(cudaGetDeviceProperties(&prop, cfg.device));
+  num_sms_ = prop.multiProcessorCount;
   if (prop.major != 10)
     throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor));
@@ -916,6 +917,7 @@ void Engine::set_template(int k, const int32_t* edges, int root) {
   need_hist_ = false;
   int max_smem = 0;
   TCG_CUDA(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, cfg_.device));
+  max_smem_ = max_smem;
   static const int rooted_mode = [] {
     const char* s = std::getenv("TCG_ROOTED");
     return s ? std::atoi(s) : 1;
@@ -1633,6 +1635,23 @@ void Engine::plan_arena_once(bool allow_stream) {
         }
       }
   }
+  // blocked rooted eMA with TMA-engine staging (opt-in, TCG_RT_TMA=1) when
+  // the raw rows of a tile and its transposed buffers fit one SM.  Measured on
+  // cfg3 node 1: 7.9 ms against 3.2 ms for the 2-CTA ema_rt_blocked -- one CTA
+  // per SM leaves the per-tile group-queue tail exposed (55% of stalls at the
+  // end-of-tile barrier: 26 output groups for 16 warps), and the raw buffer
+  // leaves no room for a second CTA.
+  static const int tma_mode = [] {
+    const char* s = std::getenv("TCG_RT_TMA");
+    return s ? std::atoi(s) : 0;
+  }();
+  for (auto& e : exec_) {
+    e.rt_tma_smem = 0;
+    if (!tma_mode || !rooted_ema_ || !e.rt_blocked || e.rt_vtx || e.root || e.a_leaf) continue;
+    const int64_t RS = static_cast<int64_t>(dev::num_panels(e.Ca_in) + dev::num_panels(e.Cpt)) * dev::kZ;
+    const int64_t sm = 4 * (32 * RS + static_cast<int64_t>(e.Wa + e.Wp) * dev::kSpitch);
+    if (sm <= max_smem_ - 4096) e.rt_tma_smem = static_cast<size_t>(sm);
+  }
   arena_bytes_ = ap.peak;
   partial_bytes_ = std::max<int64_t>(static_cast<int64_t>(max_slots_) * dev::kZ * 8, rooted_partial * 8);
 }
@@ -2027,6 +2046,17 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     while (L < 32 && (L * 4 < rf || L < std::min(32, e.Cout))) L *= 2;
     dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
         P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, L, out);
+  } else if (e.rt_blocked && e.rt_tma_smem) {
+    // persistent, TMA-engine staging double-buffered against the compute
+    auto kern = dev::ema_rt_blocked_tma;
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_tma_smem)));
+    const int RA = dev::num_panels(e.Ca_in) * dev::kZ;
+    const int RS = RA + dev::num_panels(e.Cpt) * dev::kZ;
+    const unsigned g = static_cast<unsigned>(std::max(1, std::min(max_tiles_, num_sms_)));
+    kern<<<g, dev::kRtTmaThreads, e.rt_tma_smem, stream_>>>(
+        A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_,
+        static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups, static_cast<const dev::BlockDesc*>(e.d_rt_blocks),
+        e.Ws, e.d_omap, e.Cout, n_, out, RS, RA);
   } else if (e.rt_blocked) {
     attr(reinterpret_cast<const void*>(dev::ema_rt_blocked));
     dev::ema_rt_blocked<<<grid, dev::kRtBlockedThreads, e.rt_smem, stream_>>>(

@@ -90,6 +90,7 @@ struct NodeExec {
   void* d_rt_blocks = nullptr;
   int rt_ngroups = 0;
   size_t rt_smem = 0;
+  size_t rt_tma_smem = 0;         // > 0: ema_rt_blocked_tma (raw rows + transposed tile fit one SM)
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
   void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)
@@ -327,6 +328,8 @@ class Engine {
   void rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uint8_t* d_colors, float* out = nullptr);
   bool rooted_ema_ = false;          // every table rooted; eMA on same-color vertex tiles
   int max_tiles_ = 0;                // ceil(n / 32) + k
+  int num_sms_ = 148;
+  int max_smem_ = 0;
   const uint8_t* d_colors_rt_ = nullptr;  // this context's row colors during run_dp
   int64_t vs_off_ = -1, tiles_off_ = -1, vcnt_off_ = -1;  // per-coloring vertex sort
   void setup_rooted_ema(int max_smem);

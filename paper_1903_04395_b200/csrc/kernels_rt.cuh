@@ -567,6 +567,177 @@ ema_rt_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__
     gi = __shfl_sync(0xffffffffu, gi, 0);
   }
 }
+// --------------------------------------------- TMA-staged blocked eMA
+// ema_rt_blocked as a PERSISTENT kernel whose tile staging runs on the TMA
+// engine: while the CTA computes tile t from the transposed [column][33]
+// buffers, the rows of tile t + gridDim.x are already in flight as
+// cp.async.bulk copies (SASS UBLKCP; one 16 B-aligned bulk copy per
+// (vertex, panel) row, completion on an mbarrier's transaction count) into a
+// row-major raw buffer.  The next iteration only transposes raw -> [col][33]
+// through the per-colour maps (conflict-free reads: lanes walk consecutive
+// columns of one vertex), so the HBM latency of staging is hidden behind the
+// previous tile's FMAs instead of stalling the CTA.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t phase) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+
+// issue the bulk copies of tile t's rows (A then P, every panel of every
+// vertex) into raw[v][RA + RP]; one thread arms the barrier first
+__device__ __forceinline__ void rt_issue_tile(const float* __restrict__ Am, int Ca, const float* __restrict__ Pm,
+                                              int Cpt, int32_t n, const int32_t* vids, int cnt, float* raw,
+                                              int RS, int RA, uint64_t* bar) {
+  const int lane = threadIdx.x & 31;
+  const int pa = num_panels(Ca), za = last_panel_width(Ca), pp = num_panels(Cpt), zp = last_panel_width(Cpt);
+  if (lane == 0) {
+    const uint32_t per_v = 4u * static_cast<uint32_t>((pa - 1) * kZ + za + (pp - 1) * kZ + zp);
+    mbar_expect_tx(bar, per_v * static_cast<uint32_t>(cnt));
+  }
+  __syncwarp();
+  if (lane < cnt) {
+    const int64_t v = vids[lane];
+    float* r = raw + static_cast<int64_t>(lane) * RS;
+    for (int p = 0; p < pa; ++p) {
+      const int zw = p == pa - 1 ? za : kZ;
+      bulk_g2s(r + p * kZ, Am + static_cast<int64_t>(p) * n * kZ + v * zw, 4u * zw, bar);
+    }
+    for (int p = 0; p < pp; ++p) {
+      const int zw = p == pp - 1 ? zp : kZ;
+      bulk_g2s(r + RA + p * kZ, Pm + static_cast<int64_t>(p) * n * kZ + v * zw, 4u * zw, bar);
+    }
+  }
+}
+
+constexpr int kRtTmaThreads = 512;
+__global__ void __launch_bounds__(kRtTmaThreads, 1)
+ema_rt_blocked_tma(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
+                   const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap, int Wp,
+                   const int32_t* __restrict__ vsorted, const int4* __restrict__ tiles, int ntiles,
+                   const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks, int Ws,
+                   const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out, int RS, int RA) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int next_group;
+  __shared__ int32_t vids[2][32];
+  __shared__ int4 tinfo[2];
+  float* raw = smem;                                // [32][RS], RS multiple of 32 floats
+  float* sA = smem + 32 * RS;                       // [Wa][33]
+  float* sP = sA + Wa * kSpitch;                    // [Wp][33]
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  auto load_tile = [&](int t, int buf) {            // tile t's info and vertex ids (warp 0)
+    const int4 ti = t < ntiles ? tiles[t] : make_int4(-1, 0, 0, 0);
+    if (lane == 0) tinfo[buf] = ti;
+    vids[buf][lane] = (ti.x >= 0 && lane < ti.z) ? vsorted[ti.y + lane] : -1;
+    __syncwarp();
+  };
+  uint32_t phase = 0;
+  int t = blockIdx.x, buf = 0;
+  if (threadIdx.x == 0) mbar_init(&bar, 1);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  // skip unused tiles (color -1) up front: they are numbered last per color
+  if (warp == 0) {
+    load_tile(t, 0);
+    if (t < ntiles && tinfo[0].x >= 0) rt_issue_tile(Am, Ca, Pm, Cpt, n, vids[0], tinfo[0].z, raw, RS, RA, &bar);
+  }
+  __syncthreads();
+  while (t < ntiles) {
+    const int4 ti = tinfo[buf];
+    const int tn = t + gridDim.x;
+    if (ti.x >= 0) {
+      mbar_wait(&bar, phase);
+      phase ^= 1u;
+      // transpose raw -> [col][33] through the colour's maps (every relabeled
+      // row has exactly one storage column, so each row is rewritten; lanes of
+      // missing vertices are never written out)
+      const int c = ti.x;
+      const int32_t* am = amap ? amap + static_cast<int64_t>(c) * Ca : nullptr;
+      const int32_t* pm = pmap + static_cast<int64_t>(c) * Cpt;
+      for (int v = warp; v < ti.z; v += nw) {
+        const float* r = raw + static_cast<int64_t>(v) * RS;
+        for (int col = lane; col < Ca; col += 32) {
+          const int m = am ? __ldg(am + col) : (col < Wa ? col : -1);
+          if (m >= 0) sA[m * kSpitch + v] = r[col];
+        }
+        for (int col = lane; col < Cpt; col += 32) {
+          const int m = __ldg(pm + col);
+          if (m >= 0) sP[m * kSpitch + v] = r[RA + col];
+        }
+      }
+      if (threadIdx.x == 0) next_group = nw;
+    }
+    __syncthreads();  // raw consumed, sA/sP ready
+    // prefetch the next tile's rows on the TMA engine while this one computes
+    if (warp == 0) {
+      load_tile(tn, buf ^ 1);
+      if (tn < ntiles && tinfo[buf ^ 1].x >= 0) {
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        rt_issue_tile(Am, Ca, Pm, Cpt, n, vids[buf ^ 1], tinfo[buf ^ 1].z, raw, RS, RA, &bar);
+      }
+    }
+    if (ti.x >= 0) {
+      const int64_t v = vids[buf][lane];
+      const int32_t* om = omap ? omap + static_cast<int64_t>(ti.x) * Ws : nullptr;
+      for (int gi = warp; gi < ngroups;) {
+        const GroupDesc gd = groups[gi];
+        float acc[kMaxAcc];
+#pragma unroll
+        for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
+        for (int b = gd.b0; b < gd.b1;) {
+          const BlockDesc h = blocks[b];
+          const int len = h.pad;
+          switch (h.ij) {
+            TCG_IJR(0, 1) TCG_IJR(0, 2) TCG_IJR(0, 3) TCG_IJR(0, 4) TCG_IJR(0, 5) TCG_IJR(0, 6)
+            TCG_IJR(1, 0) TCG_IJR(1, 1) TCG_IJR(1, 2) TCG_IJR(1, 3) TCG_IJR(1, 4) TCG_IJR(1, 5)
+            TCG_IJR(2, 0) TCG_IJR(2, 1) TCG_IJR(2, 2) TCG_IJR(2, 3) TCG_IJR(2, 4)
+            TCG_IJR(3, 0) TCG_IJR(3, 1) TCG_IJR(3, 2) TCG_IJR(3, 3)
+            TCG_IJR(4, 0) TCG_IJR(4, 1) TCG_IJR(4, 2)
+            TCG_IJR(5, 0) TCG_IJR(5, 1)
+            TCG_IJR(6, 0) TCG_IJR(0, 0)
+            default: break;
+          }
+          b += len;
+        }
+        if (v >= 0) {
+          const int cnt = cbin_rt<kH1>(gd.s1);
+#pragma unroll
+          for (int x = 0; x < kMaxAcc; ++x)
+            if (x < cnt) {
+              const int col = gd.out_off + x;
+              out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
+            }
+        }
+        if (lane == 0) gi = atomicAdd(&next_group, 1);
+        gi = __shfl_sync(0xffffffffu, gi, 0);
+      }
+    }
+    __syncthreads();  // sA/sP free for the next transpose
+    t = tn;
+    buf ^= 1;
+  }
+}
 #undef TCG_IJR
 
 // Root on a same-color tile: fp64 dot product over the C(k-1, a-1) splits of

@@ -24,7 +24,11 @@ child process):
 * TCG_RTV_PLEAF=0 -- wide nodes over a leaf passive child through
   ema_rtv_blocked instead of the drop-table kernel;
 * TCG_RT_WARP=0 -- narrow rooted nodes CTA-per-tile instead of warp-per-tile;
-* TCG_ROOTED=0 with TCG_PART_KB=64 -- full-table SpMM in many vertex-range parts.
+* TCG_ROOTED=0 with TCG_PART_KB=64 -- full-table SpMM in many vertex-range parts;
+* TCG_RT_TMA=1 -- the blocked rooted eMA as the persistent kernel with
+  TMA-engine (cp.async.bulk) staging of the next tile (ema_rt_blocked_tma;
+  measured slower, DESIGN.md 3, so not the default);
+* TCG_BATCH=0 -- no batched colorings (every coloring its own DP).
 
 Each child compares per-vertex counts, totals and every internal node table
 with the oracle (1e-4 relative, zero patterns exact).
@@ -69,6 +73,11 @@ def run(g, parents, root, seed, tables):
     if tables:
         for nid, want in tabs.items():
             check(c.node_table(nid, 0), want)
+    # estimate() (batched on the device for small graphs unless TCG_BATCH=0):
+    # every coloring's total equals its own run_coloring, bit for bit
+    totals, est, se, pve = c.estimate(seed, 3, per_vertex=True)
+    singles = [c.run_coloring(seed + i)[0] for i in range(3)]
+    assert list(totals) == singles, (list(totals), singles)
 
 rng = np.random.default_rng(7)
 for case in range(5):
@@ -88,10 +97,12 @@ print("OK")
                                  {"TCG_PSTREAM": "2"}, {"TCG_PSTREAM": "0"}, {"TCG_ROOTED_PARTS": "1", "TCG_PART_KB": "16"},
                                  {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}, {"TCG_VIRT": "0"}, {"TCG_RELABEL": "0"},
                                  {"TCG_DEDUP": "0"}, {"TCG_EMA_BLOCKED": "0"}, {"TCG_RTV_PLEAF": "0"},
-                                 {"TCG_RT_WARP": "0"}, {"TCG_ROOTED": "0", "TCG_PART_KB": "64"}],
+                                 {"TCG_RT_WARP": "0"}, {"TCG_ROOTED": "0", "TCG_PART_KB": "64"}, {"TCG_RT_TMA": "1"},
+                                 {"TCG_BATCH": "0"}],
                          ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
                               "rooted_parts", "pair_off", "pair_all", "virt_off", "relabel_off", "dedup_off",
-                              "blocked_off", "pleaf_off", "rt_warp_off", "full_table_parts"])
+                              "blocked_off", "pleaf_off", "rt_warp_off", "full_table_parts", "rt_tma_on",
+                              "batch_off"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
