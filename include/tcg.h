@@ -19,6 +19,13 @@
  *                    (not a tree, root out of range; templates.hpp:37-88)
  * The message of the last failure is available from tcg_last_error().
  *
+ * Numerics: count tables are fp32 (SpMM neighbour sums accumulate in fp64,
+ * the root and every total in fp64).  A non-root table entry is a colourful
+ * sub-template count rooted at one vertex and must stay below FLT_MAX
+ * (3.4e38): at the BASELINE configs the largest non-root entries are ~1e29
+ * (cfg3) to ~1e34 (cfg4 bound); a graph/template whose
+ * intermediate counts overflow fp32 yields an inf/nan rooted total, reported
+ * as TCG_ENONFINITE -- never a silently wrong count.
  * Ownership: inputs are caller-owned and copied; outputs are caller-allocated.
  * A context is single-threaded and blocks until results are on the host.
  */

@@ -218,10 +218,9 @@ Engine::Engine(const tcg_config& cfg, cudaStream_t shared_stream) : cfg_(cfg) {
   if (prop.major != 10)
     throw cuda_error("treecount-b200 is built for sm_100a (B200); device is sm_" +
                      std::to_string(prop.major) + std::to_string(prop.minor));
-  if (const char* e = std::getenv("TCG_PART_MB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 20;
   if (const char* e = std::getenv("TCG_PART_KB")) part_bytes_ = std::max(1ll, std::atoll(e)) << 10;  // tests
   // rooted SpMM: ONE part (whole rows, one launch per group) unless
-  // TCG_ROOTED_PARTS=1 splits it into colour classes of ~TCG_PART_MB.  Every
+  // TCG_ROOTED_PARTS=1 splits it into colour classes of ~part_bytes_.  Every
   // extra part re-reads and re-writes the group's P' columns; measured on
   // B200 that costs more than the L2 misses of the unsplit gather source
   // (cfg3 49.9 -> 47.9 ms, cfg4 1666 -> 1049 ms).
@@ -386,11 +385,13 @@ void Engine::set_graph(const Csr& gin) {
       local.row_ptr[i + 1] = local.row_ptr[i] + (i < nloc_ ? gin.row_ptr[r0 + i + 1] - gin.row_ptr[r0 + i] : 0);
     local.col.resize(static_cast<size_t>(local.row_ptr[nmax]));
     const int64_t e0 = gin.row_ptr[r0];
-    for (int64_t e = 0; e < local.row_ptr[nmax]; ++e) {
-      const int32_t u = gin.col[e0 + e];
-      const int r = static_cast<int>(std::upper_bound(rows_.begin(), rows_.end(), static_cast<int64_t>(u)) - rows_.begin()) - 1;
-      local.col[e] = static_cast<int32_t>(r * nmax + (u - rows_[r]));
-    }
+    parallel_for(local.row_ptr[nmax], [&](int64_t b, int64_t e1, int) {
+      for (int64_t e = b; e < e1; ++e) {
+        const int32_t u = gin.col[e0 + e];
+        const int r = static_cast<int>(std::upper_bound(rows_.begin(), rows_.end(), static_cast<int64_t>(u)) - rows_.begin()) - 1;
+        local.col[e] = static_cast<int32_t>(r * nmax + (u - rows_[r]));
+      }
+    });
     gp = &local;
     nsrc_ = static_cast<int32_t>(world_ * nmax);
     if (static_cast<int64_t>(world_) * nmax > INT32_MAX) throw invalid_argument("sharded graph too large");
@@ -596,7 +597,7 @@ void Engine::finish_graph(const int64_t* row_ptr, const int32_t* col, bool valid
   // Part size: dense rows (cfg3, avg degree ~200) gain from 64 MB parts; on
   // sparse skewed graphs (cfg2, avg ~30) the hub rows stay L2-resident anyway
   // and extra parts only add output passes (measured: profiles/ DESIGN.md 3).
-  if (!std::getenv("TCG_PART_MB") && !std::getenv("TCG_PART_KB"))
+  if (!std::getenv("TCG_PART_KB"))
     part_bytes_ = (n_ > 0 && nnz_ / std::max(n_, 1) >= 64) ? (64ll << 20) : (128ll << 20);
   max_slots_ = 0;
   const auto t2 = now();
@@ -684,8 +685,6 @@ void Engine::relabel_device() {
   n_ = nact;
   nsrc_ = nact;
   relabeled_ = true;
-  static const bool sort_mode = std::getenv("TCG_SORT_ROWS") && std::atoi(std::getenv("TCG_SORT_ROWS")) > 0;
-  if (sort_mode) sort_rows();
 }
 
 // Rows ascending (the vertex-range parts of the full-table SpMM cut rows by
@@ -2461,6 +2460,12 @@ int Engine::pick_batch(int count) const {
     return s ? std::atoi(s) : 1;
   }();
   if (!mode || count < 2 || sharded() || n_ <= 0 || exec_.empty() || batch_copies_ > 1) return 1;
+  // part schedules depend on the gather source's size (colour-class parts,
+  // vertex-range parts of the full-table SpMM): a union would cut, and round,
+  // differently -- keep those plans unbatched so results stay bit-identical
+  if (rooted_parts_ > 1) return 1;
+  for (const auto& e : exec_)
+    if (!e.p_leaf && !e.rooted && e.dup_of < 0 && e.pp_dup_of < 0) return 1;
   int64_t B = std::min<int64_t>({count, 64, (int64_t{1} << 20) / n_, (int64_t{1} << 26) / std::max<int64_t>(nnz_, 1),
                                  (int64_t{8} << 30) / std::max<int64_t>(arena_bytes_ + partial_bytes_, 1)});
   return B >= 2 ? static_cast<int>(B) : 1;

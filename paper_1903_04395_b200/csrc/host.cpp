@@ -23,7 +23,7 @@ int host_threads() {
 }
 
 // fn(begin, end, worker) over [0, total) in T static slices
-static void parallel_for(int64_t total, const std::function<void(int64_t, int64_t, int)>& fn) {
+void parallel_for(int64_t total, const std::function<void(int64_t, int64_t, int)>& fn) {
   const int T = static_cast<int>(std::min<int64_t>(host_threads(), std::max<int64_t>(1, total / 4096)));
   if (T <= 1) { fn(0, total, 0); return; }
   std::vector<std::thread> th;

@@ -12,6 +12,7 @@
 #pragma once
 
 #include <cstdint>
+#include <functional>
 #include <stdexcept>
 #include <string>
 #include <utility>
@@ -67,6 +68,8 @@ struct Csr {
 };
 
 int host_threads();
+// fn(begin, end, worker) over [0, total) in static slices on the host threads
+void parallel_for(int64_t total, const std::function<void(int64_t, int64_t, int)>& fn);
 // graph.hpp:65-95; throws invalid_argument on out-of-range ids.
 Csr csr_from_edges(const int32_t* edges, int64_t m, int32_t n_hint);
 // validates sorted / loop-free / duplicate-free / in range, and (check_symmetry)
