@@ -1644,12 +1644,24 @@ void Engine::plan_arena_once(bool allow_stream) {
     const char* s = std::getenv("TCG_RT_TMA");
     return s ? std::atoi(s) : 0;
   }();
+  // default: the warp-specialized pipeline (two transposed tiles per SM, a
+  // producer warp staging with cp.async, one group queue across tiles) when
+  // two tiles fit and every tile has at least one group per consumer warp
+  static const int pipe_mode = [] {
+    const char* s = std::getenv("TCG_RT_PIPE");
+    return s ? std::atoi(s) : 1;
+  }();
   for (auto& e : exec_) {
-    e.rt_tma_smem = 0;
-    if (!tma_mode || !rooted_ema_ || !e.rt_blocked || e.rt_vtx || e.root || e.a_leaf) continue;
-    const int64_t RS = static_cast<int64_t>(dev::num_panels(e.Ca_in) + dev::num_panels(e.Cpt)) * dev::kZ;
-    const int64_t sm = 4 * (32 * RS + static_cast<int64_t>(e.Wa + e.Wp) * dev::kSpitch);
-    if (sm <= max_smem_ - 4096) e.rt_tma_smem = static_cast<size_t>(sm);
+    e.rt_tma_smem = e.rt_pipe_smem = 0;
+    if (!rooted_ema_ || !e.rt_blocked || e.rt_vtx || e.root || e.a_leaf) continue;
+    if (tma_mode) {
+      const int64_t RS = static_cast<int64_t>(dev::num_panels(e.Ca_in) + dev::num_panels(e.Cpt)) * dev::kZ;
+      const int64_t sm = 4 * (32 * RS + static_cast<int64_t>(e.Wa + e.Wp) * dev::kSpitch);
+      if (sm <= max_smem_ - 4096) e.rt_tma_smem = static_cast<size_t>(sm);
+    } else if (pipe_mode && e.rt_ngroups >= dev::kRtPipeConsumers) {
+      const int64_t sm = 4 * 2 * static_cast<int64_t>(e.Wa + e.Wp) * dev::kSpitch;
+      if (sm <= max_smem_ - 4096) e.rt_pipe_smem = static_cast<size_t>(sm);
+    }
   }
   arena_bytes_ = ap.peak;
   partial_bytes_ = std::max<int64_t>(static_cast<int64_t>(max_slots_) * dev::kZ * 8, rooted_partial * 8);
@@ -2045,6 +2057,14 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     while (L < 32 && (L * 4 < rf || L < std::min(32, e.Cout))) L *= 2;
     dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
         P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, L, out);
+  } else if (e.rt_blocked && e.rt_pipe_smem) {
+    auto kern = dev::ema_rt_blocked_pipe;
+    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_pipe_smem)));
+    const unsigned g = static_cast<unsigned>(std::max(1, std::min(max_tiles_, num_sms_)));
+    kern<<<g, (dev::kRtPipeConsumers + 1) * 32, e.rt_pipe_smem, stream_>>>(
+        A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_,
+        static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups, static_cast<const dev::BlockDesc*>(e.d_rt_blocks),
+        e.Ws, e.d_omap, e.Cout, n_, out);
   } else if (e.rt_blocked && e.rt_tma_smem) {
     // persistent, TMA-engine staging double-buffered against the compute
     auto kern = dev::ema_rt_blocked_tma;

@@ -91,6 +91,7 @@ struct NodeExec {
   int rt_ngroups = 0;
   size_t rt_smem = 0;
   size_t rt_tma_smem = 0;         // > 0: ema_rt_blocked_tma (raw rows + transposed tile fit one SM)
+  size_t rt_pipe_smem = 0;        // > 0: ema_rt_blocked_pipe (two transposed tiles fit one SM)
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
   void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)

@@ -738,6 +738,157 @@ ema_rt_blocked_tma(const float* __restrict__ Am, int Wa, const int32_t* __restri
     buf ^= 1;
   }
 }
+// ------------------------------------ warp-specialized pipelined blocked eMA
+// ema_rt_blocked as a persistent, warp-specialized pipeline (the SM's smem
+// holds TWO transposed tiles, 2 x (Wa + Wp) x 33 floats):
+//   * warp 16 (producer) stages tile i + 2 into the buffer tile i used, the
+//     moment every output group of tile i is done (mbarrier `empty`), with
+//     4-byte cp.async copies (SASS LDGSTS) straight into the [column][33]
+//     layout through the per-colour maps -- no registers, no transpose pass;
+//     `full` completes when those copies land (cp.async.mbarrier.arrive);
+//   * warps 0-15 (consumers) take (tile, group) items from ONE queue that runs
+//     across tile boundaries, so a warp that finishes tile i's last group moves
+//     on to tile i+1 instead of waiting at a CTA barrier (the tail that made
+//     the TMA variant slow), and never waits for HBM unless the producer is
+//     two tiles behind.
+__device__ __forceinline__ void cp_async4(float* dst, const float* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(smem_u32(dst)), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t* bar) {
+  asm volatile("cp.async.mbarrier.arrive.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+constexpr int kRtPipeConsumers = 16;
+__global__ void __launch_bounds__((kRtPipeConsumers + 1) * 32, 1)
+ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
+                    const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap, int Wp,
+                    const int32_t* __restrict__ vsorted, const int4* __restrict__ tiles, int ntiles,
+                    const GroupDesc* __restrict__ groups, int ngroups, const BlockDesc* __restrict__ blocks, int Ws,
+                    const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out) {
+  extern __shared__ __align__(128) float smem[];
+  __shared__ __align__(8) uint64_t full[2], empty[2];
+  __shared__ int32_t vids[2][32];
+  __shared__ int4 tinfo[2];
+  __shared__ int next_item, ntile_cta;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int bufsz = (Wa + Wp) * kSpitch;
+  if (threadIdx.x == 0) {
+    mbar_init(&full[0], 1);
+    mbar_init(&full[1], 1);
+    mbar_init(&empty[0], static_cast<uint32_t>(ngroups));
+    mbar_init(&empty[1], static_cast<uint32_t>(ngroups));
+    next_item = 0;
+  }
+  if (warp == 0) {  // this CTA's tiles blockIdx.x + i * gridDim.x that hold vertices (a prefix)
+    int cnt = 0;
+    for (int i0 = 0;; i0 += 32) {
+      const int t = blockIdx.x + (i0 + lane) * static_cast<int>(gridDim.x);
+      const bool ok = t < ntiles && tiles[t].x >= 0;
+      const unsigned m = __ballot_sync(0xffffffffu, ok);
+      cnt += __popc(m);
+      if (m != 0xffffffffu) break;
+    }
+    if (lane == 0) ntile_cta = cnt;
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+  const int nt = ntile_cta;
+  if (warp == kRtPipeConsumers) {
+    // ------------------------------------------------------------ producer
+    for (int i = 0; i < nt; ++i) {
+      const int b = i & 1;
+      if (i >= 2) mbar_wait(&empty[b], static_cast<uint32_t>(((i >> 1) - 1) & 1));  // tile i-2 fully consumed
+      const int t = blockIdx.x + i * static_cast<int>(gridDim.x);
+      const int4 ti = tiles[t];
+      const int vid = lane < ti.z ? vsorted[ti.y + lane] : -1;
+      if (lane == 0) tinfo[b] = ti;
+      vids[b][lane] = vid;
+      float* sA = smem + b * bufsz;
+      float* sP = sA + Wa * kSpitch;
+      const int32_t* am = amap ? amap + static_cast<int64_t>(ti.x) * Ca : nullptr;
+      const int32_t* pm = pmap + static_cast<int64_t>(ti.x) * Cpt;
+      // lane = column (consecutive columns of one vertex row: coalesced reads)
+      for (int c0 = 0; c0 < Ca; c0 += 32) {
+        const int c = c0 + lane;
+        const int m = c < Ca ? (am ? __ldg(am + c) : (c < Wa ? c : -1)) : -1;
+        const int p = c / kZ, zw = panel_width(Ca, p);
+        const float* src = Am + static_cast<int64_t>(p) * n * kZ + (c % kZ);
+        for (int v = 0; v < ti.z; ++v) {
+          const int64_t u = __shfl_sync(0xffffffffu, vid, v);
+          if (m >= 0) cp_async4(sA + m * kSpitch + v, src + u * zw);
+        }
+      }
+      for (int c0 = 0; c0 < Cpt; c0 += 32) {
+        const int c = c0 + lane;
+        const int m = c < Cpt ? __ldg(pm + c) : -1;
+        const int p = c / kZ, zw = panel_width(Cpt, p);
+        const float* src = Pm + static_cast<int64_t>(p) * n * kZ + (c % kZ);
+        for (int v = 0; v < ti.z; ++v) {
+          const int64_t u = __shfl_sync(0xffffffffu, vid, v);
+          if (m >= 0) cp_async4(sP + m * kSpitch + v, src + u * zw);
+        }
+      }
+      cp_async_arrive(&full[b]);  // pending +1 now, -1 when this lane's copies land
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&full[b]);  // the expected arrival (vids / tinfo written)
+    }
+    return;
+  }
+  // -------------------------------------------------------------- consumers
+  const int total = nt * ngroups;
+  int item = 0;
+  if (lane == 0) item = atomicAdd(&next_item, 1);
+  item = __shfl_sync(0xffffffffu, item, 0);
+  while (item < total) {
+    const int i = item / ngroups, gi = item - i * ngroups;
+    const int b = i & 1;
+    mbar_wait(&full[b], static_cast<uint32_t>((i >> 1) & 1));
+    const float* sA = smem + b * bufsz;
+    const float* sP = sA + Wa * kSpitch;
+    const int4 ti = tinfo[b];
+    const int64_t v = vids[b][lane];
+    const int32_t* om = omap ? omap + static_cast<int64_t>(ti.x) * Ws : nullptr;
+    const GroupDesc gd = groups[gi];
+    float acc[kMaxAcc];
+#pragma unroll
+    for (int x = 0; x < kMaxAcc; ++x) acc[x] = 0.f;
+    for (int bb = gd.b0; bb < gd.b1;) {
+      const BlockDesc h = blocks[bb];
+      const int len = h.pad;
+      const int b = bb;
+      switch (h.ij) {
+        TCG_IJR(0, 1) TCG_IJR(0, 2) TCG_IJR(0, 3) TCG_IJR(0, 4) TCG_IJR(0, 5) TCG_IJR(0, 6)
+        TCG_IJR(1, 0) TCG_IJR(1, 1) TCG_IJR(1, 2) TCG_IJR(1, 3) TCG_IJR(1, 4) TCG_IJR(1, 5)
+        TCG_IJR(2, 0) TCG_IJR(2, 1) TCG_IJR(2, 2) TCG_IJR(2, 3) TCG_IJR(2, 4)
+        TCG_IJR(3, 0) TCG_IJR(3, 1) TCG_IJR(3, 2) TCG_IJR(3, 3)
+        TCG_IJR(4, 0) TCG_IJR(4, 1) TCG_IJR(4, 2)
+        TCG_IJR(5, 0) TCG_IJR(5, 1)
+        TCG_IJR(6, 0) TCG_IJR(0, 0)
+        default: break;
+      }
+      bb += len;
+    }
+    if (v >= 0) {
+      const int cnt = cbin_rt<kH1>(gd.s1);
+#pragma unroll
+      for (int x = 0; x < kMaxAcc; ++x)
+        if (x < cnt) {
+          const int col = gd.out_off + x;
+          out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
+        }
+    }
+    __syncwarp();
+    if (lane == 0) {
+      mbar_arrive(&empty[b]);  // one of the tile's ngroups items done (its smem reads are complete)
+      item = atomicAdd(&next_item, 1);
+    }
+    item = __shfl_sync(0xffffffffu, item, 0);
+  }
+}
+
 #undef TCG_IJR
 
 // Root on a same-color tile: fp64 dot product over the C(k-1, a-1) splits of
