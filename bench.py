@@ -54,6 +54,30 @@ CONFIGS = {
 }
 DEFAULT_CONFIG = "cfg3"
 L2_GATHER_PEAK_GBS = 19461.3  # measured: 128 B row gathers from a 64 MB L2-resident panel (profiles/r01_membench.txt)
+FP32_PEAK_TFLOPS = 71.6       # measured: FP32 FMA throughput (profiles/r01_membench.txt)
+
+
+def coloring_roofline(T, parents, n, nnz, hbm_gbs):
+    """per internal node, SpMM_bytes/BW + max(eMA_bytes/BW, eMA_FLOPs/FP32), summed --
+    the whole-coloring roofline the measured ms/coloring is compared against."""
+    from math import comb
+    plan = T.partition(T.template_from_parents(parents, 0))
+    k = len(parents)
+    bw, fp = hbm_gbs * 1e9, FP32_PEAK_TFLOPS * 1e12
+    tot = spmm_s = ema_s = 0.0
+    for nd in plan.nodes:
+        if nd.is_leaf():
+            continue
+        sa, sp = plan.node(nd.active_child).size, plan.node(nd.passive_child).size
+        ca, cp, cs = comb(k, sa), comb(k, sp), comb(k, nd.size)
+        sb = 4 * nnz + 8 * (n + 1) + 8 * n * cp
+        eb = 4 * n * ((0 if sa == 1 else ca) + cp) + (8 * n if nd.id == plan.full_node() else 4 * n * cs)
+        ef = 2 * n * cs * comb(nd.size, sa)
+        spmm_s += sb / bw
+        ema_s += max(eb / bw, ef / fp)
+    tot = spmm_s + ema_s
+    return {"roofline_ms": tot * 1e3, "spmm_roofline_ms": spmm_s * 1e3, "ema_roofline_ms": ema_s * 1e3,
+            "fp32_peak_tflops": FP32_PEAK_TFLOPS}
 
 
 def log(*a):
@@ -216,7 +240,7 @@ def ref_sample_desc(k):
             "physical cores): one full-graph SpMM batch of 16 and of 1 column, 32 ema() column pairs, "
             f"random_coloring and init_leaf_table timed in full, then summed over the k={k} plan's batches/pairs "
             "(ref_driver.cpp ref_time_sampled); checked against a full timed coloring in "
-            "profiles/r02_ref_full_vs_sampled.txt.  `bench.py --impl reference` times a FULL coloring.")
+            "profiles/r02_ref_full_vs_sampled_cfg3.txt.  `bench.py --impl reference` times a FULL coloring.")
 
 
 def run_reference(args, rank, world, local, dist):
@@ -385,6 +409,7 @@ def run_b200(args, rank, world, local, dist):
     if rank != 0:
         return
     hbm_peak, peak_src = peaks()
+    cr = coloring_roofline(T, parents, g.n, g.nnz(), hbm_peak)
     spmm_gbs = tm.spmm_alg_bytes / (tm.spmm_ms * 1e-3) / 1e9 if tm.spmm_ms else None
     per_launch_bytes = tm.spmm_alg_bytes / max(tm.spmm_launches, 1)
     per_launch_ms = tm.spmm_ms / max(tm.spmm_launches, 1)
@@ -416,6 +441,10 @@ def run_b200(args, rank, world, local, dist):
                      "ema": {"achieved_gbs": ema_gbs, "frac_hbm": ema_gbs / hbm_peak if ema_gbs else None,
                              "tflops": tm.ema_flops / (tm.ema_ms * 1e-3) / 1e12 if tm.ema_ms else None,
                              "ms_per_coloring": tm.ema_ms / args.steps}},
+        "coloring_roofline": dict(cr, measured_ms=ms_max / args.steps, frac=cr["roofline_ms"] / (ms_max / args.steps),
+                                  note="SURVEY 8(d): sum over internal nodes of SpMM_bytes/HBM + max(eMA_bytes/HBM, "
+                                       "eMA_FLOPs/FP32) at the compulsory fp32 bytes, against the measured "
+                                       "ms/coloring"),
         "phase_ms_per_coloring": {"spmm": tm.spmm_ms / args.steps, "ema": tm.ema_ms / args.steps,
                                   "other": (tm.total_ms - tm.spmm_ms - tm.ema_ms) / args.steps},
         "cpu_baseline": cpu,

@@ -1644,12 +1644,16 @@ void Engine::plan_arena_once(bool allow_stream) {
     const char* s = std::getenv("TCG_RT_TMA");
     return s ? std::atoi(s) : 0;
   }();
-  // default: the warp-specialized pipeline (two transposed tiles per SM, a
-  // producer warp staging with cp.async, one group queue across tiles) when
-  // two tiles fit and every tile has at least one group per consumer warp
+  // opt-in (TCG_RT_PIPE=1): the warp-specialized pipeline (two transposed
+  // tiles per SM, producer warps staging with 4-byte cp.async, one group queue
+  // across tiles) when two tiles fit and every tile has a group per consumer
+  // warp.  Measured on cfg3 node 1 (producer/consumer warps -> ms): 1/16 7.4,
+  // 2/16 4.9, 4/16 4.0, 8/12 3.45, 8/16 3.40, against 3.33-3.47 for the
+  // 2-CTA ema_rt_blocked: the 4-byte transposing copies, not the compute,
+  // bound it, so the simple kernel stays the default.
   static const int pipe_mode = [] {
     const char* s = std::getenv("TCG_RT_PIPE");
-    return s ? std::atoi(s) : 1;
+    return s ? std::atoi(s) : 0;
   }();
   for (auto& e : exec_) {
     e.rt_tma_smem = e.rt_pipe_smem = 0;
@@ -2058,10 +2062,11 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
         P, e.Cpt, d_colors_rt_, e.d_cmap, e.Cout, n_, vpb, L, out);
   } else if (e.rt_blocked && e.rt_pipe_smem) {
-    auto kern = dev::ema_rt_blocked_pipe;
+    auto kern = dev::ema_rt_blocked_pipe<dev::kRtPipeProducers, dev::kRtPipeConsumers>;
+    const int nthr = (dev::kRtPipeProducers + dev::kRtPipeConsumers) * 32;
     TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_pipe_smem)));
     const unsigned g = static_cast<unsigned>(std::max(1, std::min(max_tiles_, num_sms_)));
-    kern<<<g, (dev::kRtPipeConsumers + 1) * 32, e.rt_pipe_smem, stream_>>>(
+    kern<<<g, nthr, e.rt_pipe_smem, stream_>>>(
         A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_,
         static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups, static_cast<const dev::BlockDesc*>(e.d_rt_blocks),
         e.Ws, e.d_omap, e.Cout, n_, out);

@@ -761,8 +761,10 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 
-constexpr int kRtPipeConsumers = 16;
-__global__ void __launch_bounds__((kRtPipeConsumers + 1) * 32, 1)
+constexpr int kRtPipeConsumers = 12;  // consumer warps (>= 1 output group each per tile)
+constexpr int kRtPipeProducers = 8;   // producer warps: bytes in flight (one warp alone keeps too few)
+template <int NP, int NC>
+__global__ void __launch_bounds__((NP + NC) * 32, 1)
 ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
                     const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap, int Wp,
                     const int32_t* __restrict__ vsorted, const int4* __restrict__ tiles, int ntiles,
@@ -776,8 +778,8 @@ ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restr
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int bufsz = (Wa + Wp) * kSpitch;
   if (threadIdx.x == 0) {
-    mbar_init(&full[0], 1);
-    mbar_init(&full[1], 1);
+    mbar_init(&full[0], NP);
+    mbar_init(&full[1], NP);
     mbar_init(&empty[0], static_cast<uint32_t>(ngroups));
     mbar_init(&empty[1], static_cast<uint32_t>(ngroups));
     next_item = 0;
@@ -796,22 +798,26 @@ ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restr
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
   const int nt = ntile_cta;
-  if (warp == kRtPipeConsumers) {
-    // ------------------------------------------------------------ producer
+  if (warp >= NC) {
+    // ----------------------------------------------------------- producers
+    const int pw = warp - NC;
     for (int i = 0; i < nt; ++i) {
       const int b = i & 1;
       if (i >= 2) mbar_wait(&empty[b], static_cast<uint32_t>(((i >> 1) - 1) & 1));  // tile i-2 fully consumed
       const int t = blockIdx.x + i * static_cast<int>(gridDim.x);
       const int4 ti = tiles[t];
       const int vid = lane < ti.z ? vsorted[ti.y + lane] : -1;
-      if (lane == 0) tinfo[b] = ti;
-      vids[b][lane] = vid;
+      if (pw == 0) {
+        if (lane == 0) tinfo[b] = ti;
+        vids[b][lane] = vid;
+      }
       float* sA = smem + b * bufsz;
       float* sP = sA + Wa * kSpitch;
       const int32_t* am = amap ? amap + static_cast<int64_t>(ti.x) * Ca : nullptr;
       const int32_t* pm = pmap + static_cast<int64_t>(ti.x) * Cpt;
-      // lane = column (consecutive columns of one vertex row: coalesced reads)
-      for (int c0 = 0; c0 < Ca; c0 += 32) {
+      // lane = column (consecutive columns of one vertex row: coalesced
+      // reads); producer warp pw takes column chunks pw, pw + NP, ...
+      for (int c0 = pw * 32; c0 < Ca; c0 += NP * 32) {
         const int c = c0 + lane;
         const int m = c < Ca ? (am ? __ldg(am + c) : (c < Wa ? c : -1)) : -1;
         const int p = c / kZ, zw = panel_width(Ca, p);
@@ -821,7 +827,7 @@ ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restr
           if (m >= 0) cp_async4(sA + m * kSpitch + v, src + u * zw);
         }
       }
-      for (int c0 = 0; c0 < Cpt; c0 += 32) {
+      for (int c0 = pw * 32; c0 < Cpt; c0 += NP * 32) {
         const int c = c0 + lane;
         const int m = c < Cpt ? __ldg(pm + c) : -1;
         const int p = c / kZ, zw = panel_width(Cpt, p);
@@ -833,7 +839,7 @@ ema_rt_blocked_pipe(const float* __restrict__ Am, int Wa, const int32_t* __restr
       }
       cp_async_arrive(&full[b]);  // pending +1 now, -1 when this lane's copies land
       __syncwarp();
-      if (lane == 0) mbar_arrive(&full[b]);  // the expected arrival (vids / tinfo written)
+      if (lane == 0) mbar_arrive(&full[b]);  // this warp's expected arrival (vids / tinfo written)
     }
     return;
   }

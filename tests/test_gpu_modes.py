@@ -28,8 +28,9 @@ child process):
 * TCG_RT_TMA=1 -- the blocked rooted eMA as the persistent kernel with
   TMA-engine (cp.async.bulk) staging of the next tile (ema_rt_blocked_tma;
   measured slower, DESIGN.md 3, so not the default);
-* TCG_RT_PIPE=0 -- the blocked rooted eMA as one tile per CTA (stage, then
-  compute) instead of the warp-specialized cp.async pipeline;
+* TCG_RT_PIPE=1 -- the blocked rooted eMA as the warp-specialized cp.async
+  pipeline (ema_rt_blocked_pipe: producer warps, one group queue across
+  tiles; opt-in, DESIGN.md 3);
 * TCG_BATCH=0 -- no batched colorings (every coloring its own DP).
 
 Each child compares per-vertex counts, totals and every internal node table
@@ -100,11 +101,11 @@ print("OK")
                                  {"TCG_PAIR": "0"}, {"TCG_PAIR": "2"}, {"TCG_VIRT": "0"}, {"TCG_RELABEL": "0"},
                                  {"TCG_DEDUP": "0"}, {"TCG_EMA_BLOCKED": "0"}, {"TCG_RTV_PLEAF": "0"},
                                  {"TCG_RT_WARP": "0"}, {"TCG_ROOTED": "0", "TCG_PART_KB": "64"}, {"TCG_RT_TMA": "1"},
-                                 {"TCG_BATCH": "0"}, {"TCG_RT_PIPE": "0"}],
+                                 {"TCG_BATCH": "0"}, {"TCG_RT_PIPE": "1"}],
                          ids=["rt_vtx_all", "full_table_ema", "full_table_spmm", "pstream_all", "pstream_off",
                               "rooted_parts", "pair_off", "pair_all", "virt_off", "relabel_off", "dedup_off",
                               "blocked_off", "pleaf_off", "rt_warp_off", "full_table_parts", "rt_tma_on",
-                              "batch_off", "rt_pipe_off"])
+                              "batch_off", "rt_pipe_on"])
 def test_kernel_path_parity(env):
     code = CHILD.format(root=ROOT, tests=os.path.join(ROOT, "tests"))
     r = subprocess.run([sys.executable, "-c", code], env={**os.environ, **env}, capture_output=True, text=True,
