@@ -265,6 +265,16 @@ int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, v
  * enqueues every panel all-gather on a communication stream, double-buffered
  * against the SpMM of the previous group -- no host synchronization per panel. */
 #define TCG_NCCL_ID_BYTES 128
+/* In-process loopback transport: `world` contexts of THIS process (several may
+ * share one GPU) act as the ranks; panels move by device-to-device copies
+ * enqueued asynchronously exactly like the NCCL transport's all-gathers (so
+ * the pipelined sharded SpMM runs with world > 1 on one GPU).  Every rank's
+ * calls must come from its own host thread, concurrently (the hub's host
+ * barriers order the ranks' enqueues; no kernel waits on another rank). */
+typedef struct tcg_loopback tcg_loopback;
+int tcg_loopback_create(int world, tcg_loopback** out);
+void tcg_loopback_destroy(tcg_loopback* hub);   /* after every context using it */
+int tcg_set_shard_loopback(tcg_ctx* ctx, int rank, tcg_loopback* hub);
 int tcg_nccl_unique_id(uint8_t id[TCG_NCCL_ID_BYTES]);
 int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_NCCL_ID_BYTES]);
 

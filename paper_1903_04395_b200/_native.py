@@ -101,6 +101,9 @@ _SIGS = {
     "tcg_set_shard_host": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
     "tcg_nccl_unique_id": (C.c_int, [vp]),
     "tcg_create_multi": (C.c_int, [vp, vp, C.c_int, P(vp)]),
+    "tcg_loopback_create": (C.c_int, [C.c_int, P(vp)]),
+    "tcg_loopback_destroy": (None, [vp]),
+    "tcg_set_shard_loopback": (C.c_int, [vp, C.c_int, vp]),
     "tcg_device_count_of": (C.c_int, [vp]),
     "tcg_set_shard_nccl": (C.c_int, [vp, C.c_int, C.c_int, vp]),
 }

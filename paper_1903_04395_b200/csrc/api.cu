@@ -523,6 +523,33 @@ int tcg_set_shard_nccl(tcg_ctx* ctx, int rank, int world, const uint8_t id[TCG_N
   });
 }
 
+struct tcg_loopback {
+  std::shared_ptr<void> hub;
+};
+
+int tcg_loopback_create(int world, tcg_loopback** out) {
+  return guarded([&] {
+    need(out, "out");
+    auto l = std::make_unique<tcg_loopback>();
+    l->hub = tcg::make_loopback_hub(world);
+    *out = l.release();
+  });
+}
+
+void tcg_loopback_destroy(tcg_loopback* hub) { delete hub; }
+
+int tcg_set_shard_loopback(tcg_ctx* ctx, int rank, tcg_loopback* hub) {
+  return guarded([&] {
+    need(ctx, "ctx");
+    need(hub, "hub");
+    if (!ctx->peers.empty()) throw tcg::invalid_argument("a multi-device context spreads colorings; shard with one context per rank");
+    const int world = tcg::loopback_world(hub->hub);
+    if (rank < 0 || rank >= world) throw tcg::invalid_argument("bad shard rank/world");
+    cudaSetDevice(ctx->eng->device());
+    ctx->eng->set_shard(rank, world, tcg::make_loopback_transport(hub->hub, rank));
+  });
+}
+
 int tcg_set_shard_host(tcg_ctx* ctx, int rank, int world, tcg_allgather_fn fn, void* user) {
   return guarded([&] {
     need(ctx, "ctx");

@@ -136,6 +136,9 @@ struct Transport {
 void nccl_unique_id(uint8_t* out);   // TCG_NCCL_ID_BYTES bytes
 int nccl_version();
 std::unique_ptr<Transport> make_nccl_transport(int rank, int world, const uint8_t* id);
+std::shared_ptr<void> make_loopback_hub(int world);
+std::unique_ptr<Transport> make_loopback_transport(const std::shared_ptr<void>& hub, int rank);
+int loopback_world(const std::shared_ptr<void>& hub);
 std::unique_ptr<Transport> make_device_transport(tcg_allgather_fn fn, void* user);
 std::unique_ptr<Transport> make_host_transport(tcg_allgather_fn fn, void* user);
 void set_host_transport_world(Transport* t, int world);

@@ -14,6 +14,8 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <condition_variable>
+#include <mutex>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -137,7 +139,85 @@ struct NcclTransport : Transport {
   }
 };
 
+// ----------------------------------------------------------- loopback
+// In-process ranks (one engine per rank, several engines per GPU allowed)
+// exchanging panels by device-to-device copies: the async transport contract
+// of NcclTransport (everything enqueued on the caller's stream, ordered by
+// events) without NCCL, so the pipelined sharded SpMM can be run and checked
+// with world > 1 on ONE GPU.  Host barriers only order the ENQUEUES of the
+// ranks' copies; no kernel ever waits on another rank.
+struct LoopbackHub {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t gen = 0;
+  std::vector<const void*> send;
+  std::vector<cudaEvent_t> ready, done;
+  explicit LoopbackHub(int w) : world(w), send(w), ready(w), done(w) {}
+  void barrier() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      ++gen;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+
+struct LoopbackTransport : Transport {
+  std::shared_ptr<LoopbackHub> hub;
+  int rank;
+  cudaEvent_t ev_ready = nullptr, ev_done = nullptr;
+  LoopbackTransport(std::shared_ptr<LoopbackHub> h, int r) : hub(std::move(h)), rank(r) {
+    if (cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&ev_done, cudaEventDisableTiming) != cudaSuccess)
+      throw cuda_error("loopback transport: event creation failed");
+  }
+  ~LoopbackTransport() override {
+    if (ev_ready) cudaEventDestroy(ev_ready);
+    if (ev_done) cudaEventDestroy(ev_done);
+  }
+  bool async() const override { return true; }
+  void allgather(const void* d_send, size_t bytes, void* d_recv, cudaStream_t s) override {
+    auto ok = [](cudaError_t e) {
+      if (e != cudaSuccess) throw cuda_error(std::string("loopback transport: ") + cudaGetErrorString(e));
+    };
+    ok(cudaEventRecord(ev_ready, s));  // this rank's panel, in stream order
+    hub->send[rank] = d_send;
+    hub->ready[rank] = ev_ready;
+    hub->done[rank] = ev_done;
+    hub->barrier();
+    for (int r = 0; r < hub->world; ++r) {
+      ok(cudaStreamWaitEvent(s, hub->ready[r], 0));
+      ok(cudaMemcpyAsync(static_cast<char*>(d_recv) + static_cast<size_t>(r) * bytes, hub->send[r], bytes,
+                         cudaMemcpyDeviceToDevice, s));
+    }
+    ok(cudaEventRecord(ev_done, s));
+    hub->barrier();
+    for (int r = 0; r < hub->world; ++r)  // peers have read this rank's panel before it moves on
+      if (r != rank) ok(cudaStreamWaitEvent(s, hub->done[r], 0));
+    hub->barrier();  // every wait enqueued before any event is re-recorded
+  }
+};
+
 }  // namespace
+
+std::shared_ptr<void> make_loopback_hub(int world) {
+  if (world < 1) throw invalid_argument("world size must be >= 1");
+  return std::make_shared<LoopbackHub>(world);
+}
+
+std::unique_ptr<Transport> make_loopback_transport(const std::shared_ptr<void>& hub, int rank) {
+  auto h = std::static_pointer_cast<LoopbackHub>(hub);
+  if (rank < 0 || rank >= h->world) throw invalid_argument("bad loopback rank");
+  return std::make_unique<LoopbackTransport>(h, rank);
+}
+
+int loopback_world(const std::shared_ptr<void>& hub) { return std::static_pointer_cast<LoopbackHub>(hub)->world; }
 
 void nccl_unique_id(uint8_t* out) {
   ncclUniqueId id;

@@ -411,6 +411,11 @@ class Context:
         buf = (C.c_uint8 * N.TCG_NCCL_ID_BYTES).from_buffer_copy(ident)
         check(lib.tcg_set_shard_nccl(self._h, rank, world, buf))
 
+    def set_shard_loopback(self, rank: int, hub: "LoopbackHub") -> None:
+        """In-process rank of a LoopbackHub (tcg_set_shard_loopback)."""
+        self._hub = hub  # keep the hub alive as long as this context
+        check(lib.tcg_set_shard_loopback(self._h, rank, hub._h))
+
     def set_shard_host(self, rank: int, world: int, allgather) -> None:
         """Host transport: allgather(send: bytes-like np.uint8 array) -> np.uint8
         array of world*len(send) bytes in rank order (e.g. gloo)."""
@@ -530,6 +535,18 @@ class Context:
         totals = np.zeros(count, np.float64)
         check(lib.tcg_time_colorings(self._h, seed, count, int(per_kernel), _ptr(totals), C.byref(tm)))
         return tm, totals
+
+
+class LoopbackHub:
+    """`world` in-process ranks exchanging panels by device-to-device copies
+    (tcg_loopback_create); drive each rank's context from its own thread."""
+
+    def __init__(self, world: int):
+        h = C.c_void_p()
+        check(lib.tcg_loopback_create(world, C.byref(h)))
+        self._h = h
+        self.world = world
+        self._fin = weakref.finalize(self, lib.tcg_loopback_destroy, h)
 
 
 def _nccl_env() -> None:

@@ -215,3 +215,62 @@ def test_sharded_world1_library_nccl():
         assert abs(total - ot) <= 1e-4 * ot, name
         assert np.max(np.abs(pv - opv) / np.maximum(opv, 1)) <= 1e-4, name
         assert totals[0] == total
+
+
+def test_nccl_unique_id_on_host():
+    """The library resolves NCCL at run time (dlopen) and produces the 128-byte
+    bootstrap id rank 0 hands to the other ranks (tcg_nccl_unique_id) -- host
+    only, no GPU needed; two ids differ (fresh bootstrap each call)."""
+    import ctypes as C
+    from paper_1903_04395_b200 import _native as N
+    from paper_1903_04395_b200 import treecount as TC
+    TC._nccl_env()
+    a, b = (C.c_uint8 * N.TCG_NCCL_ID_BYTES)(), (C.c_uint8 * N.TCG_NCCL_ID_BYTES)()
+    assert N.lib.tcg_nccl_unique_id(a) == 0, N.lib.tcg_last_error()
+    assert N.lib.tcg_nccl_unique_id(b) == 0
+    assert any(bytes(a)) and bytes(a) != bytes(b)
+    assert N.lib.tcg_nccl_unique_id(None) == N.TCG_EINVAL
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+@pytest.mark.parametrize("name", ["cfg2", "cfg3"])
+def test_sharded_loopback_world_n(world, name):
+    """world in-process ranks on ONE GPU through the loopback transport, which
+    has the NCCL transport's async contract: the rooted SpMM's panels are
+    all-gathered on the communication stream, group g+1 while group g's
+    gathers run (double buffer, events only).  Every rank's context runs in
+    its own thread; results match the oracle and are identical across ranks."""
+    import threading
+    g = T.generate_rmat(T.RmatSpec(12, 24 << 12, .45, .15, .15, .25, 5))
+    parents = CFG_TEMPLATES[name]
+    hub = T.LoopbackHub(world)
+    ctxs = []
+    for r in range(world):
+        c = T.Context(0)
+        c.set_shard_loopback(r, hub)
+        c.set_graph(g)
+        c.set_template(T.template_from_parents(parents, 0))
+        ctxs.append(c)
+    out, err = [None] * world, []
+
+    def rank_main(r):
+        try:
+            total, pv, _ = ctxs[r].run_coloring(9, per_vertex=True)
+            totals, est, se, pve = ctxs[r].estimate(9, 2, per_vertex=True)
+            out[r] = (total, pv, list(totals), pve)
+        except Exception as ex:  # noqa: BLE001
+            err.append(ex)
+    th = [threading.Thread(target=rank_main, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join(timeout=600)
+    assert not err, err
+    ot, opv, _ = _ref(g, parents, 9)
+    for total, pv, totals, pve in out:
+        assert abs(total - ot) <= 1e-4 * ot
+        assert np.max(np.abs(pv - opv) / np.maximum(opv, 1)) <= 1e-4
+        assert totals[0] == total
+    assert all(o[0] == out[0][0] and o[2] == out[0][2] for o in out)
+    assert all(np.array_equal(o[3], out[0][3]) for o in out)
