@@ -243,7 +243,7 @@ Engine::~Engine() {
   dfree(d_scalars_);
   dfree(d_seeds_);
   dfree(d_colors_);
-  batch_.reset();
+  batches_.clear();
   tr_.reset();  // (a communicator before its streams)
   if (comm_) cudaStreamDestroy(comm_);
   for (cudaEvent_t e : {ev_in_, ev_g_[0], ev_g_[1], ev_u_[0], ev_u_[1]})
@@ -2499,8 +2499,21 @@ int Engine::pick_batch(int count) const {
 // The engine over the B-fold union of this engine's (internal) graph, same
 // template, same stream; rebuilt when the graph, the template or B changes.
 Engine* Engine::batch_engine(int B) {
-  if (!batch_ || batch_->batch_copies_ != B || batch_tpl_gen_ != tpl_gen_) {
-    batch_.reset();
+  // one engine per batch size in use (a handful at most: estimate/time calls
+  // with different counts do not rebuild each other's union)
+  Batch* slot = nullptr;
+  for (auto& x : batches_)
+    if (x.B == B) slot = &x;
+  if (slot && slot->tpl_gen != tpl_gen_) {
+    slot->eng.reset();
+    slot->graph_gen = ~0ull;
+  }
+  if (!slot) {
+    if (batches_.size() >= 4) batches_.erase(batches_.begin());  // oldest
+    batches_.push_back(Batch{B, nullptr, ~0ull, ~0ull});
+    slot = &batches_.back();
+  }
+  if (!slot->eng) {
     tcg_config c = cfg_;
     c.flags &= ~TCG_KEEP_TABLES;
     c.memory_budget = 0;
@@ -2514,11 +2527,11 @@ Engine* Engine::batch_engine(int B) {
       edges.push_back(pr.second);
     }
     be->set_template(tpl_.k, edges.data(), tpl_.root);
-    batch_ = std::move(be);
-    batch_tpl_gen_ = tpl_gen_;
-    batch_graph_gen_ = ~0ull;
+    slot->eng = std::move(be);
+    slot->tpl_gen = tpl_gen_;
+    slot->graph_gen = ~0ull;
   }
-  if (batch_graph_gen_ != graph_gen_) {
+  if (slot->graph_gen != graph_gen_) {
     // the union of this graph's copies, built on the device in scratch kept
     // across graphs (e2e: a new CSR per call), then handed to the batch engine
     const int64_t nU = static_cast<int64_t>(n_) * B, eU = nnz_ * B;
@@ -2536,11 +2549,11 @@ Engine* Engine::batch_engine(int B) {
     }
     dev::union_graph<<<148 * 4, 256, 0, stream_>>>(d_row_ptr_, d_col_, n_, nnz_, B, d_urp_, d_ucol_);
     TCG_CUDA(cudaGetLastError());
-    batch_->set_graph_ptrs(static_cast<int32_t>(nU), d_urp_, d_ucol_, false, eU);
-    batch_->ensure_arena();
-    batch_graph_gen_ = graph_gen_;
+    slot->eng->set_graph_ptrs(static_cast<int32_t>(nU), d_urp_, d_ucol_, false, eU);
+    slot->eng->ensure_arena();
+    slot->graph_gen = graph_gen_;
   }
-  return batch_.get();
+  return slot->eng.get();
 }
 
 // B colorings (caller order) as one DP over the union: the copies' totals

@@ -198,11 +198,16 @@ class Engine {
 
   // batched colorings: B colorings of a small graph as one DP
   // over the B-fold disjoint union, on a second engine sharing this stream
-  std::unique_ptr<Engine> batch_;
+  struct Batch {
+    int B;
+    std::unique_ptr<Engine> eng;
+    uint64_t tpl_gen, graph_gen;
+  };
+  std::vector<Batch> batches_;
   int batch_copies_ = 1;             // > 1: this engine holds a union of that many copies
   bool no_relabel_ = false;          // (batch engines: the union keeps its copies contiguous)
   bool own_stream_ = true;
-  uint64_t graph_gen_ = 0, tpl_gen_ = 0, batch_graph_gen_ = ~0ull, batch_tpl_gen_ = ~0ull;
+  uint64_t graph_gen_ = 0, tpl_gen_ = 0;
   int pick_batch(int count) const;
   int64_t* d_urp_ = nullptr;         // union CSR scratch (kept across graphs)
   int32_t* d_ucol_ = nullptr;
