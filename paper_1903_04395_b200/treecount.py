@@ -135,6 +135,8 @@ def single_vertex_template() -> TemplateTree:
 
 def template_from_parents(parents, root: int = 0) -> TemplateTree:
     """BASELINE.json parent array -> edges (p[v], v), rooted at `root`."""
+    if len(parents) == 1:  # k = 1 (templates.hpp single_vertex_template)
+        return single_vertex_template()
     return make_template([(int(parents[v]), v) for v in range(1, len(parents))], root)
 
 
