@@ -2493,6 +2493,8 @@ int Engine::pick_batch(int count) const {
     if (!e.p_leaf && !e.rooted && e.dup_of < 0 && e.pp_dup_of < 0) return 1;
   int64_t B = std::min<int64_t>({count, 64, (int64_t{1} << 20) / n_, (int64_t{1} << 26) / std::max<int64_t>(nnz_, 1),
                                  (int64_t{8} << 30) / std::max<int64_t>(arena_bytes_ + partial_bytes_, 1)});
+  if (cfg_.memory_budget > 0)  // the union's tables count against the caller's budget too
+    B = std::min<int64_t>(B, cfg_.memory_budget / std::max<int64_t>(arena_bytes_, 1));
   return B >= 2 ? static_cast<int>(B) : 1;
 }
 
