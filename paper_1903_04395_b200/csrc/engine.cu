@@ -128,7 +128,10 @@ void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
     if (s2 == h2mask) break;
   }
   if (total != binom()(k, s) * binom()(s, a)) throw logic_error("blocked eMA does not cover every split pair");
-  std::stable_sort(gs.begin(), gs.end(), [](const G& x, const G& y) { return x.work > y.work; });
+  // (work descending; equal work: by s1, so the groups of one shape stay together)
+  std::stable_sort(gs.begin(), gs.end(), [](const G& x, const G& y) {
+    return x.work > y.work || (x.work == y.work && x.d.s1 < y.d.s1);
+  });
   groups.clear();
   blocks.clear();
   for (auto& g : gs) {
@@ -144,6 +147,90 @@ void build_blocked(int k, int s, int a, std::vector<dev::GroupDesc>& groups,
     g.d.b1 = static_cast<int32_t>(blocks.size());
     groups.push_back(g.d);
   }
+}
+
+// Tasks of the vertex-per-CTA blocked eMA (kernels_rt.cuh ema_rtv_blocked): the
+// output groups of build_blocked, cut into tasks of gpt = 32 / V groups of one
+// SHAPE (same s1 and the same sequence of pattern runs), so a warp walks one
+// run list for all its lanes.  Descriptors {a_off | p_off << 16} are stored
+// step-major per task (step q of group gl at blk0 + q * gpt + gl).  Inside a
+// run any block order is valid; it is chosen greedily per step so that the
+// groups' A offsets (and P offsets) fall on distinct residues mod gpt -- the
+// lanes of a step then read distinct shared-memory banks (the V vertices of a
+// group sit 32 / V banks apart).  Padding lanes of a partial task repeat the
+// first group's descriptor (a broadcast read) and have gout = -1.
+struct RtvPlan {
+  std::vector<dev::RtvTask> tasks;
+  std::vector<int32_t> gout;
+  std::vector<uint32_t> runs, blocks;
+  int64_t steps = 0, conflicts = 0;  // (descriptor steps, steps with a bank collision: diagnostics)
+};
+RtvPlan build_rtv_tasks(int k, int s, int a, int h1, int V) {
+  std::vector<dev::GroupDesc> gr;
+  std::vector<dev::BlockDesc> bl;
+  build_blocked(k, s, a, gr, bl, h1, 16);
+  const int gpt = 32 / V;
+  RtvPlan P;
+  auto sig = [&](const dev::GroupDesc& g) {
+    std::vector<uint32_t> r;
+    for (int b = g.b0; b < g.b1; b += bl[b].pad)
+      r.push_back(static_cast<uint32_t>(bl[b].ij) | (static_cast<uint32_t>(bl[b].pad) << 8));
+    return r;
+  };
+  for (size_t gi = 0; gi < gr.size();) {
+    const std::vector<uint32_t> rs = sig(gr[gi]);
+    size_t ge = gi + 1;
+    while (ge < gr.size() && gr[ge].s1 == gr[gi].s1 && sig(gr[ge]) == rs) ++ge;
+    const int32_t run0 = static_cast<int32_t>(P.runs.size());
+    for (uint32_t rr : rs)  // {i * 16 + j | len << 8} -> {hcode(i, j) | len << 8}
+      P.runs.push_back(static_cast<uint32_t>(dev::hcode(static_cast<int>(rr & 0xFFu) / 16, static_cast<int>(rr & 0xFFu) % 16)) |
+                       (rr & ~0xFFu));
+    for (size_t c = gi; c < ge; c += gpt) {
+      const int ng = static_cast<int>(std::min<size_t>(gpt, ge - c));
+      P.tasks.push_back(dev::RtvTask{static_cast<int32_t>(P.blocks.size()), run0, static_cast<int32_t>(rs.size()),
+                                     gr[gi].s1});
+      for (int gl = 0; gl < gpt; ++gl) P.gout.push_back(gl < ng ? gr[c + gl].out_off : -1);
+      int boff = 0;
+      for (uint32_t rr : rs) {
+        const int ij = static_cast<int>(rr & 0xFFu), len = static_cast<int>(rr >> 8);
+        const int wa = dev::cbin(h1, ij / 16), wp = dev::cbin(h1, ij % 16);
+        std::vector<std::vector<char>> used(ng, std::vector<char>(len, 0));
+        std::vector<uint32_t> pick(gpt);
+        for (int q = 0; q < len; ++q) {
+          // residue -> offset already read at this step (-1: free); the same offset again is a
+          // broadcast, a different offset on the same residue is a bank conflict
+          int32_t ra[32], rp[32];
+          for (int r = 0; r < gpt; ++r) ra[r] = rp[r] = -1;
+          bool clash = false;
+          for (int gl = 0; gl < ng; ++gl) {
+            int best = -1, bestc = 1 << 30;
+            for (int b = 0; b < len && bestc > 0; ++b) {
+              if (used[gl][b]) continue;
+              const dev::BlockDesc& d = bl[gr[c + gl].b0 + boff + b];
+              const int32_t xa = ra[d.a_off % gpt], xp = rp[d.p_off % gpt];
+              const int cost = (xa >= 0 && xa != d.a_off ? wa : 0) + (xp >= 0 && xp != d.p_off ? wp : 0);
+              if (cost < bestc) bestc = cost, best = b;
+            }
+            used[gl][best] = 1;
+            const dev::BlockDesc& d = bl[gr[c + gl].b0 + boff + best];
+            if (d.a_off >= 65536 || d.p_off >= 65536) throw logic_error("blocked eMA offsets exceed 16 bits");
+            ra[d.a_off % gpt] = d.a_off;
+            rp[d.p_off % gpt] = d.p_off;
+            clash |= bestc > 0;
+            pick[gl] = static_cast<uint32_t>(d.a_off) | (static_cast<uint32_t>(d.p_off) << 16);
+          }
+          for (int gl = ng; gl < gpt; ++gl) pick[gl] = pick[0];
+          P.blocks.insert(P.blocks.end(), pick.begin(), pick.end());
+          ++P.steps;
+          P.conflicts += clash;
+        }
+        boff += len;
+      }
+    }
+    gi = ge;
+  }
+  P.blocks.insert(P.blocks.end(), 128, 0u);  // (the kernel loads up to three 32-word chunks past a task)
+  return P;
 }
 
 void release_schedule(PartSchedule& s) {
@@ -330,6 +417,9 @@ void Engine::release_template() {
     dfree(e.d_rt_groups);
     dfree(e.d_rt_blocks);
     dfree(e.d_rtv_blocks);
+    dfree(e.d_rtv_tasks);
+    dfree(e.d_rtv_gout);
+    dfree(e.d_rtv_runs);
     dfree(e.d_rtv_drop);
     dfree(e.d_emap);
     dfree(e.d_amap);
@@ -1320,24 +1410,20 @@ void Engine::setup_rooted_ema(int max_smem) {
         if (e.rt_vtx || (blocked_mode && k - 1 >= dev::kH1 && (e.rt_pairs >= 16 || blocked_mode == 2))) {
           std::vector<dev::GroupDesc> gr;
           std::vector<dev::BlockDesc> bl;
-          if (e.rt_vtx) {  // vertex-per-CTA: the widest H1 the (k-1) colors allow (<= 8)
-            // H = 6 (measured on cfg5 node 1 / node 2 eMA, H = 6 / 7 / 8: 308 / 433 / 353 ms
-            // and 120 / 167 / 321 ms -- 8 with the larger operand set streamed from
-            // shared memory)
+          if (e.rt_vtx) {
+            // vertex-per-CTA: tasks are built below, once V is known (build_rtv_tasks).
+            // H = 6: measured on cfg5 node 1 / node 2 and cfg4 node 1 with the task kernel,
+            // H = 6 / 7: 243 / 297, 114 / 110 and 114 / 135 ms (H = 8 spills)
             e.rtv_h = dev::kH1;
-            build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl, e.rtv_h, 16);
-            std::vector<uint2> b2(bl.size());  // packed 8 B descriptors
-            for (size_t i = 0; i < bl.size(); ++i)
-              b2[i] = make_uint2(static_cast<uint32_t>(bl[i].a_off) | (static_cast<uint32_t>(bl[i].p_off) << 16),
-                                 static_cast<uint32_t>(bl[i].ij) | (static_cast<uint32_t>(bl[i].pad) << 8));
-            e.d_rtv_blocks = dupload(b2, stream_);
           } else {
             build_blocked(k - 1, e.size - 1, e.sa - 1, gr, bl);
           }
           e.rt_blocked = true;
-          e.rt_ngroups = static_cast<int>(gr.size());
-          e.d_rt_groups = dupload(gr, stream_);
-          e.d_rt_blocks = dupload(bl, stream_);
+          if (!e.rt_vtx) {
+            e.rt_ngroups = static_cast<int>(gr.size());
+            e.d_rt_groups = dupload(gr, stream_);
+            e.d_rt_blocks = dupload(bl, stream_);
+          }
         }
       }
     }
@@ -1385,10 +1471,24 @@ void Engine::setup_rooted_ema(int max_smem) {
         const int64_t half = (max_smem - 4096) / 2;
         int V = 8;
         while (V > 1 && 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) > half) V /= 2;
+        // a third CTA per SM (80 registers) when the same V still fits (cfg4 node 1: 114 -> 109 ms;
+        // halving V for it loses: cfg5 node 1 at V = 1 291 -> 390 ms)
+        e.rtv_minb = 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) <= (max_smem - 4096) / 3 ? 3 : 2;
         e.rtv_V = V;
         e.rtv_sa = static_cast<int>(stride(row_floats(e.Wa), V));
         e.rtv_sp = static_cast<int>(stride(e.Wp, V));
         e.rt_smem = static_cast<size_t>(4 * V * (e.rtv_sa + e.rtv_sp));
+        if (!e.rtv_pleaf) {
+          const RtvPlan rp = build_rtv_tasks(k - 1, e.size - 1, e.sa - 1, e.rtv_h, V);
+          e.rtv_ntasks = static_cast<int>(rp.tasks.size());
+          e.d_rtv_tasks = dupload(rp.tasks, stream_);
+          e.d_rtv_gout = dupload(rp.gout, stream_);
+          e.d_rtv_runs = dupload(rp.runs, stream_);
+          e.d_rtv_blocks = dupload(rp.blocks, stream_);
+          if (std::getenv("TCG_VERBOSE"))
+            std::fprintf(stderr, "[tcg] node %d rtv tasks %d (V %d, %lld steps, %lld with a bank clash)\n", e.id,
+                         e.rtv_ntasks, V, static_cast<long long>(rp.steps), static_cast<long long>(rp.conflicts));
+        }
       }
       dfree(e.d_imap);
       continue;
@@ -2026,12 +2126,11 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
       dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
-      auto kern = dev::ema_rtv_blocked<6>;
+      auto kern = e.rtv_minb == 3 ? dev::ema_rtv_blocked<dev::kH1, 3> : dev::ema_rtv_blocked<dev::kH1, 2>;
       attr(reinterpret_cast<const void*>(kern));
       kern<<<vgrid, 256, e.rt_smem, stream_>>>(
-          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::GroupDesc*>(e.d_rt_groups), e.rt_ngroups,
-          static_cast<const uint2*>(e.d_rtv_blocks), e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V,
-          e.rtv_sa, e.rtv_sp);
+          A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::RtvTask*>(e.d_rtv_tasks), e.rtv_ntasks, e.d_rtv_gout,
+          e.d_rtv_runs, e.d_rtv_blocks, e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V, e.rtv_sa, e.rtv_sp);
     }
     return;
   }

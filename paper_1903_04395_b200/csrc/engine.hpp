@@ -94,7 +94,12 @@ struct NodeExec {
   size_t rt_pipe_smem = 0;        // > 0: ema_rt_blocked_pipe (two transposed tiles fit one SM)
   bool rt_vtx = false;            // vertex-per-CTA rooted eMA (the 32-vertex tile does not fit smem)
   int rtv_V = 1, rtv_sa = 0, rtv_sp = 0, rtv_h = 6;
-  void* d_rtv_blocks = nullptr;   // uint2 {a_off | p_off << 16, pattern} (ema_rtv_blocked)
+  // ema_rtv_blocked tasks (engine.cu build_rtv_tasks): 32 / V same-shape groups per task
+  void* d_rtv_tasks = nullptr;        // dev::RtvTask[ntasks]
+  int32_t* d_rtv_gout = nullptr;      // [ntasks][32 / V] output column offset of the group, -1 = padding lane
+  uint32_t* d_rtv_runs = nullptr;     // pattern runs {i * 16 + j | length << 8}, shared by the tasks of a shape
+  uint32_t* d_rtv_blocks = nullptr;   // step-major {a_off | p_off << 16} per (task, block step, group)
+  int rtv_ntasks = 0, rtv_minb = 2;
   bool rtv_pleaf = false;         // vertex-per-warp eMA over a leaf passive child (ema_rtv_pleaf)
   uint32_t* d_rtv_drop = nullptr; // [Ws][s-1] {A index of S' minus d | d << 16}
   bool rtv_packed = false;        // d_rtv_drop packed as one uint4 per output (s-1 <= 6, k-1 <= 16)

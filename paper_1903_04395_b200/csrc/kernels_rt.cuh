@@ -1047,16 +1047,30 @@ __device__ __forceinline__ void micro_block_h(const float* __restrict__ sa, cons
   }
 }
 
-// one run of blocks with the same pattern (I, J): descriptors {a_off | p_off << 16}
-// prefetched one block ahead
+// dense pattern code of (i, j), i + j <= 8, in TCG_HCASES order (a dense switch
+// compiles to one indexed branch)
+__host__ __device__ constexpr int hcode(int i, int j) { return i * 9 - i * (i - 1) / 2 + j; }
+
+// one run of blocks with the same pattern (I, J).  The task's descriptors
+// {a_off | p_off << 16} form one linear stream of 32-word chunks (32 / gpt
+// block steps each); lane l holds word l of the current chunk and of the two
+// chunks after it (loaded two chunks -- >= 4 blocks -- ahead: the stream
+// lives in L2), and a block's descriptor is a shuffle away.  Not unrolled:
+// the 45 pattern bodies already exceed the instruction cache.
 #define TCG_HC(I, J)                                                                 \
-  case I * 16 + J: {                                                                 \
-    uint32_t d = h.x;                                                                \
-    for (int q = 1;; ++q) {                                                          \
-      const uint32_t dn = q < len ? __ldg(&blocks[b + q].x) : 0u;                    \
+  case hcode(I, J): {                                                                \
+    _Pragma("unroll 1")                                                              \
+    for (int q = 0; q < len; ++q) {                                                  \
+      const uint32_t d = __shfl_sync(0xffffffffu, cur, sc + gl);                     \
+      sc += gpt;                                                                     \
+      if (sc == 32) {                                                                \
+        sc = 0;                                                                      \
+        cur = n1;                                                                    \
+        n1 = n2;                                                                     \
+        wp += 32;                                                                    \
+        n2 = __ldg(wp);                                                              \
+      }                                                                              \
       micro_block_h<H, I, J>(sA + (d & 0xFFFFu), sP + (d >> 16), acc);               \
-      if (q >= len) break;                                                           \
-      d = dn;                                                                        \
     }                                                                                \
   } break;
 #define TCG_HCASES                                                                                        \
@@ -1068,18 +1082,25 @@ __device__ __forceinline__ void micro_block_h(const float* __restrict__ sa, cons
   TCG_HC(6, 1) TCG_HC(6, 2) TCG_HC(7, 0) TCG_HC(7, 1) TCG_HC(8, 0)
 
 // V vertices per pass (staged at strides sa/sp floats, == 32/V mod 32 so the
-// V lanes sharing a group hit different banks).  Work items (group, vertex)
-// are ordered group-major over groups sorted by work; warps take TASKS of 32
-// consecutive items from a per-pass queue (largest first), so a warp runs
-// 32/V groups of one shape (convergent pattern dispatch, shared descriptors)
-// and the pass ends balanced.  Blocks come in runs of one pattern: packed
-// 8 B descriptors {a_off | p_off << 16, pattern | run length << 8 (at the
-// run's first block)}, one dispatch per run.
-template <int H>
-__global__ void __launch_bounds__(256, 2)
+// V lanes sharing a group hit different banks).  A TASK is 32/V output groups
+// of one shape (the same sequence of pattern runs, host build_rtv_tasks) x V
+// vertices: the warp walks ONE run list (uniform pattern dispatch, no
+// divergence), and only the operand offsets differ per lane -- one packed
+// 4 B descriptor {a_off | p_off << 16} per (block step, group), stored
+// step-major so a warp reads its task's descriptors as coalesced 128 B chunks.  The host orders
+// each group's blocks inside a run so that the groups' offsets of a step fall
+// on different banks (residues mod 32/V distinct where possible).  Warps take
+// tasks from a per-pass queue, largest first.
+struct RtvTask {
+  int32_t blk0, run0, nruns, s1;
+};
+
+template <int H, int MINB>
+__global__ void __launch_bounds__(256, MINB)
 ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                 const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
-                const GroupDesc* __restrict__ groups, int ngroups, const uint2* __restrict__ blocks, int Ws,
+                const RtvTask* __restrict__ tasks, int ntasks, const int32_t* __restrict__ gout,
+                const uint32_t* __restrict__ runs, const uint32_t* __restrict__ blocks, int Ws,
                 const int32_t* __restrict__ omap, int Cout, int32_t n, float* __restrict__ out, int V, int sa,
                 int sp) {
   constexpr int kAcc = cbin(H, H / 2);
@@ -1087,43 +1108,46 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
   __shared__ int next_task;
   float* sP0 = smem + V * sa;
   const int lane = threadIdx.x & 31;
-  const int items = ngroups * V;
-  const int ntasks = (items + 31) / 32;
+  const int gpt = 32 / V;
+  const int gl = lane / V, j = lane - gl * V;
+  const float* sA = smem + j * sa;
+  const float* sP = sP0 + j * sp;
   for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * V; v0 < n; v0 += static_cast<int64_t>(gridDim.x) * V) {
     __syncthreads();
     if (threadIdx.x == 0) next_task = blockDim.x >> 5;
-    for (int j = 0; j < V && v0 + j < n; ++j) {
-      if (amap) stage_row_pmap(Am, Ca, n, v0 + j, smem + j * sa, amap + static_cast<int64_t>(colors[v0 + j]) * Ca);
-      else stage_row(Am, Wa, n, v0 + j, smem + j * sa);
-      stage_row_pmap(Pm, Cpt, n, v0 + j, sP0 + j * sp, pmap + static_cast<int64_t>(colors[v0 + j]) * Cpt);
+    for (int jj = 0; jj < V && v0 + jj < n; ++jj) {
+      if (amap) stage_row_pmap(Am, Ca, n, v0 + jj, smem + jj * sa, amap + static_cast<int64_t>(colors[v0 + jj]) * Ca);
+      else stage_row(Am, Wa, n, v0 + jj, smem + jj * sa);
+      stage_row_pmap(Pm, Cpt, n, v0 + jj, sP0 + jj * sp, pmap + static_cast<int64_t>(colors[v0 + jj]) * Cpt);
     }
     __syncthreads();
+    const int64_t v = v0 + j;
     for (int task = threadIdx.x >> 5; task < ntasks;) {
-      const int it = task * 32 + lane;
-      const int gi = it / V, j = it - gi * V;
-      const int64_t v = v0 + j;
-      if (it < items && v < n) {
-        const float* sA = smem + j * sa;
-        const float* sP = sP0 + j * sp;
-        const GroupDesc gd = groups[gi];
-        float acc[kAcc];
+      const int4 t = __ldg(reinterpret_cast<const int4*>(tasks) + task);  // {blk0, run0, nruns, s1}
+      const int out_off = __ldg(gout + task * gpt + gl);
+      float acc[kAcc];
 #pragma unroll
-        for (int x = 0; x < kAcc; ++x) acc[x] = 0.f;
-        for (int b = gd.b0; b < gd.b1;) {
-          const uint2 h = __ldg(blocks + b);
-          const int len = static_cast<int>(h.y >> 8);
-          switch (h.y & 0xFFu) {
-            TCG_HCASES
-            default: break;
-          }
-          b += len;
+      for (int x = 0; x < kAcc; ++x) acc[x] = 0.f;
+      const uint32_t* wp = blocks + t.x + lane + 64;  // (the lane's word of the chunk loaded next)
+      uint32_t cur = __ldg(wp - 64), n1 = __ldg(wp - 32), n2 = __ldg(wp);
+      int sc = 0;                                     // first word of the current step in the chunk
+      uint32_t rr = __ldg(runs + t.y);
+      for (int r = 0; r < t.z; ++r) {
+        const uint32_t rn = r + 1 < t.z ? __ldg(runs + t.y + r + 1) : 0u;
+        const int len = static_cast<int>(rr >> 8);
+        switch (rr & 0xFFu) {
+          TCG_HCASES
+          default: break;
         }
+        rr = rn;
+      }
+      if (out_off >= 0 && v < n) {
         const int32_t* om = omap ? omap + static_cast<int64_t>(colors[v]) * Ws : nullptr;
-        const int cnt = cbin_rt<H>(gd.s1);
+        const int cnt = cbin_rt<H>(t.w);
 #pragma unroll
         for (int x = 0; x < kAcc; ++x)
           if (x < cnt) {
-            const int col = gd.out_off + x;
+            const int col = out_off + x;
             out[om ? panel_offset(Cout, n, v, __ldg(om + col)) : panel_offset(Ws, n, v, col)] = acc[x];
           }
       }
