@@ -2107,14 +2107,18 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
     const int cst = e.omap.empty() ? e.Ws : e.Cout;
     const int oslice = (cst + 31) / 32 * 32 + 1;
-    constexpr int pv = 1;  // vertices per CTA pass (measured cfg4 node 4, V = 1 / 2 / 4: 104.6 / 107.6 / 138.7 ms)
-    const size_t smem = static_cast<size_t>(pv) * (slice + oslice) * 4;
-    auto kern = dev::ema_rtv_pleaf<pv>;
+    // one vertex per CTA pass (measured cfg4 node 4 / node 7, V = 1 / 2 / 4: 61 / 63 / 89 and 18 / 16 / 14 ms)
+    const size_t smem = static_cast<size_t>(slice + oslice) * 4;
+    using PleafFn = void (*)(const float*, int, const int32_t*, int, const float*, int, const int32_t*, const uint8_t*,
+                             const uint32_t*, int, int, const int32_t*, int, int32_t, int, int, float*);
+    static const PleafFn kerns[7] = {dev::ema_rtv_pleaf<1, 0>, dev::ema_rtv_pleaf<1, 1>, dev::ema_rtv_pleaf<1, 2>,
+                                     dev::ema_rtv_pleaf<1, 3>, dev::ema_rtv_pleaf<1, 4>, dev::ema_rtv_pleaf<1, 5>,
+                                     dev::ema_rtv_pleaf<1, 6>};
+    const PleafFn kern = kerns[e.rtv_packed ? e.size - 1 : 0];
     TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-    const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>((n_ + pv - 1) / pv, 148 * 16)));
-    kern<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_,
-                                                      e.d_rtv_drop, e.size - 1, e.rtv_packed ? 1 : 0, e.Ws, e.d_omap, e.Cout, n_, slice,
-                                                      oslice, table_ptr(e.out_off));
+    const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n_, 148 * 16)));
+    kern<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rtv_drop, e.size - 1,
+                                        e.Ws, e.d_omap, e.Cout, n_, slice, oslice, table_ptr(e.out_off));
     return;
   }
   if (e.rt_vtx) {

@@ -399,11 +399,11 @@ ema_rt_node_w(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
 // accumulates all kPleafV vertices into the vertices' output rows staged in
 // smem (storage order: RR columns, or the RS slots of the parent's SpMM),
 // which warps then write as whole 128 B panel rows.
-template <int kPleafV>
+template <int kPleafV, int SP>  // SP: compile-time s' of the packed drop rows (1..6), 0 = unpacked rows
 __global__ void __launch_bounds__(256)
 ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca,
               const float* __restrict__ Pm, int Cpt, const int32_t* __restrict__ pmap,
-              const uint8_t* __restrict__ colors, const uint32_t* __restrict__ drop, int sp, int packed, int Ws,
+              const uint8_t* __restrict__ colors, const uint32_t* __restrict__ drop, int sp, int Ws,
               const int32_t* __restrict__ omap, int Cout, int32_t n, int slice, int oslice, float* __restrict__ out) {
   extern __shared__ float smem[];
   __shared__ int cvs[kPleafV];
@@ -414,36 +414,46 @@ ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
   for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * kPleafV; v0 < n; v0 += static_cast<int64_t>(gridDim.x) * kPleafV) {
     __syncthreads();
     if (threadIdx.x < kPleafV) cvs[threadIdx.x] = v0 + threadIdx.x < n ? colors[v0 + threadIdx.x] : 0;
-    // warp w stages vertices w, w + nw, ...: its A row (through amap when the
-    // table is packed or virtual) and its relabeled histogram
-    for (int vv = warp; vv < kPleafV; vv += nw) {
+    // the whole CTA stages the kPleafV A rows (through amap when the table is
+    // packed or virtual) -- every thread's loads are in flight at once -- and
+    // one warp per vertex its relabeled histogram
+    for (int idx = threadIdx.x; idx < kPleafV * tot4; idx += blockDim.x) {
+      const int vv = idx / tot4, f = idx - vv * tot4;
       const int64_t v = v0 + vv;
       float* sA = smem + static_cast<int64_t>(vv) * slice;
-      float* sH = sA + slice - 32;
+      const int c0 = f * 4, p = c0 / kZ, z4 = c0 % kZ;
       if (v >= n) {
-        for (int f = lane; f < slice; f += 32) sA[f] = 0.f;
+        if (c0 < Wa) sA[c0] = 0.f;
+        if (c0 + 1 < Wa) sA[c0 + 1] = 0.f;
+        if (c0 + 2 < Wa) sA[c0 + 2] = 0.f;
+        if (c0 + 3 < Wa) sA[c0 + 3] = 0.f;
+        continue;
+      }
+      const int zw = p == pa - 1 ? za : kZ;
+      const float4 x = __ldg(reinterpret_cast<const float4*>(Am + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
+      if (!amap) {
+        if (c0 < Wa) sA[c0] = x.x;
+        if (c0 + 1 < Wa) sA[c0 + 1] = x.y;
+        if (c0 + 2 < Wa) sA[c0 + 2] = x.z;
+        if (c0 + 3 < Wa) sA[c0 + 3] = x.w;
+      } else {
+        const int32_t* am = amap + static_cast<int64_t>(colors[v]) * Ca;
+        const int m0 = c0 < Ca ? __ldg(am + c0) : -1, m1 = c0 + 1 < Ca ? __ldg(am + c0 + 1) : -1;
+        const int m2 = c0 + 2 < Ca ? __ldg(am + c0 + 2) : -1, m3 = c0 + 3 < Ca ? __ldg(am + c0 + 3) : -1;
+        if (m0 >= 0) sA[m0] = x.x;
+        if (m1 >= 0) sA[m1] = x.y;
+        if (m2 >= 0) sA[m2] = x.z;
+        if (m3 >= 0) sA[m3] = x.w;
+      }
+    }
+    for (int vv = warp; vv < kPleafV; vv += nw) {
+      const int64_t v = v0 + vv;
+      float* sH = smem + static_cast<int64_t>(vv) * slice + slice - 32;
+      if (v >= n) {
+        sH[lane] = 0.f;
         continue;
       }
       const int c = colors[v];
-      const int32_t* am = amap ? amap + static_cast<int64_t>(c) * Ca : nullptr;
-      for (int f = lane; f < tot4; f += 32) {
-        const int c0 = f * 4, p = c0 / kZ, z4 = c0 % kZ;
-        const int zw = p == pa - 1 ? za : kZ;
-        const float4 x = __ldg(reinterpret_cast<const float4*>(Am + static_cast<int64_t>(p) * n * kZ + v * zw + z4));
-        if (!am) {
-          if (c0 < Wa) sA[c0] = x.x;
-          if (c0 + 1 < Wa) sA[c0 + 1] = x.y;
-          if (c0 + 2 < Wa) sA[c0 + 2] = x.z;
-          if (c0 + 3 < Wa) sA[c0 + 3] = x.w;
-        } else {
-          const int m0 = c0 < Ca ? __ldg(am + c0) : -1, m1 = c0 + 1 < Ca ? __ldg(am + c0 + 1) : -1;
-          const int m2 = c0 + 2 < Ca ? __ldg(am + c0 + 2) : -1, m3 = c0 + 3 < Ca ? __ldg(am + c0 + 3) : -1;
-          if (m0 >= 0) sA[m0] = x.x;
-          if (m1 >= 0) sA[m1] = x.y;
-          if (m2 >= 0) sA[m2] = x.z;
-          if (m3 >= 0) sA[m3] = x.w;
-        }
-      }
       if (lane < Cpt) {  // pmap: storage column -> d' (or -1 for c(v))
         const int d = __ldg(pmap + static_cast<int64_t>(c) * Cpt + lane);
         if (d >= 0) sH[d] = __ldg(Pm + v * panel_width(Cpt, 0) + lane);
@@ -454,16 +464,16 @@ ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
       float acc[kPleafV];
 #pragma unroll
       for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = 0.f;
-      if (packed) {  // (s' <= 6, k - 1 <= 16) six 16-bit A indices + six 4-bit colours in one 16 B load
+      if constexpr (SP > 0) {  // (s' <= 6, k - 1 <= 16) six 16-bit A indices + six 4-bit colours in one 16 B load
         const uint4 q = __ldg(reinterpret_cast<const uint4*>(drop) + j);
         const uint32_t w[3] = {q.x, q.y, q.z};
+        const float* sHh = smem + slice - 32;
 #pragma unroll
-        for (int i = 0; i < 6; ++i) {
-          if (i >= sp) break;
+        for (int i = 0; i < SP; ++i) {
           const int ia = static_cast<int>((w[i >> 1] >> ((i & 1) * 16)) & 0xFFFFu);
-          const int ih = static_cast<int>((q.w >> (4 * i)) & 0xFu) + slice - 32;
+          const int ih = static_cast<int>((q.w >> (4 * i)) & 0xFu);
 #pragma unroll
-          for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], smem[vv * slice + ih], acc[vv]);
+          for (int vv = 0; vv < kPleafV; ++vv) acc[vv] = fmaf(smem[vv * slice + ia], sHh[vv * slice + ih], acc[vv]);
         }
       } else {
         const uint32_t* dr = drop + static_cast<int64_t>(j) * sp;
@@ -485,14 +495,16 @@ ema_rtv_pleaf(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ 
     // whole panel rows: warp w writes (vertex, panel) rows w, w + nw, ...
     const int Cst = omap ? Cout : Ws;
     const int po = num_panels(Cst), zo = last_panel_width(Cst);
-    for (int r = warp; r < kPleafV * po; r += nw) {
-      const int vv = r / po, p = r % po;
+#pragma unroll
+    for (int vv = 0; vv < kPleafV; ++vv) {
       const int64_t v = v0 + vv;
-      if (v >= n) continue;
-      const int zp = p == po - 1 ? zo : kZ;
-      if (lane < zp) {
-        const int col = p * kZ + lane;
-        out[static_cast<int64_t>(p) * n * kZ + v * zp + lane] = col < Cst ? sO[vv * oslice + col] : 0.f;
+      if (v >= n) break;
+      for (int p = warp; p < po; p += nw) {
+        const int zp = p == po - 1 ? zo : kZ;
+        if (lane < zp) {
+          const int col = p * kZ + lane;
+          out[static_cast<int64_t>(p) * n * kZ + v * zp + lane] = col < Cst ? sO[vv * oslice + col] : 0.f;
+        }
       }
     }
   }
