@@ -1172,15 +1172,17 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
 #undef TCG_HCASES
 
 // Root, one vertex per CTA: fp64 dot product over the relabeled split pairs,
-// fixed-order block reduction -> root_out[v] (root_reduce then sums root_out).
+// fixed-order reduction (shuffle tree inside a warp, then the warps in order;
+// three barriers per vertex) -> root_out[v] (root_reduce then sums root_out).
 __global__ void __launch_bounds__(256)
 ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
              const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors, const int2* __restrict__ split,
              int pairs, int32_t n, double* __restrict__ root_out, double* __restrict__ root_acc) {
   extern __shared__ float smem[];
-  __shared__ double red[256];
+  __shared__ double red[8];
   float* sA = smem;
   float* sP = smem + row_floats(Wa);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int64_t v = blockIdx.x; v < n; v += gridDim.x) {
     const int c = colors[v];
     __syncthreads();
@@ -1193,15 +1195,15 @@ ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ a
       const int2 s = __ldg(split + p);
       acc = fma(static_cast<double>(sA[s.x]), static_cast<double>(sP[s.y]), acc);
     }
-    red[threadIdx.x] = acc;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+    if (lane == 0) red[warp] = acc;
     __syncthreads();
-    for (int o = blockDim.x / 2; o; o >>= 1) {
-      if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
-      __syncthreads();
-    }
     if (threadIdx.x == 0) {
-      root_out[v] = red[0];
-      if (root_acc) root_acc[v] += red[0];
+      double t = red[0];
+      for (int w = 1; w < 8; ++w) t += red[w];
+      root_out[v] = t;
+      if (root_acc) root_acc[v] += t;
     }
   }
 }
