@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <mutex>
 #include <thread>
 #include <type_traits>
 
@@ -34,6 +35,23 @@ namespace tcg {
   } while (0)
 
 namespace {
+// cudaFuncAttributeMaxDynamicSharedMemorySize is per (device, function), shared by every engine
+// of the process: engines driven by different host threads (tcg_create_multi with a device listed
+// twice, a batch engine next to its parent) launch the same kernel with different dynamic sizes,
+// so the limit is only ever RAISED (a launch below the limit is always valid).
+void smem_limit(const void* f, size_t bytes) {
+  static std::mutex mu;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  TCG_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lk(mu);
+  size_t& c = cur[{dev, f}];
+  if (bytes > c) {
+    TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    c = bytes;
+  }
+}
+
 constexpr int64_t kAlign = 256;
 int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
 
@@ -2015,7 +2033,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const bool vpx = ch && ch->virt_px;
     const int wx = vpx ? ch->Cpt : e.Wx;
     const size_t smem = static_cast<size_t>(4) * 32 * (wx + 1);
-    TCG_CUDA(cudaFuncSetAttribute(dev::pair_expand, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_limit(reinterpret_cast<const void*>(dev::pair_expand), smem);
     dev::pair_expand<<<static_cast<unsigned>((n_ + 31) / 32), 256, smem, stream_>>>(M, wx, d_colors, vpx ? e.d_xmap_v : e.d_xmap,
                                                                                       k, G, zw, n_, cp);
     ++launches_;
@@ -2026,7 +2044,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
     const int rf = static_cast<int>(dev::table_floats(e.Cp, 1));
     const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (96 << 10) / (4 * rf))));
     const size_t smem = static_cast<size_t>(vpb) * rf * 4;
-    TCG_CUDA(cudaFuncSetAttribute(dev::rooted_compress, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_limit(reinterpret_cast<const void*>(dev::rooted_compress), smem);
     dev::rooted_compress<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
         M, e.Cp, d_colors, e.d_slot_col, G, zw, n_, vpb, table_ptr(e.ct_off));
     ++launches_;
@@ -2045,7 +2063,7 @@ void Engine::rooted_spmm(const NodeExec& e, const float* M, float* Pp, const uin
   // pair: the rows in color order (this coloring's re-ordered schedule)
   const dev::Seg* segs = e.pair ? reinterpret_cast<const dev::Seg*>(arena_ + pseg_off_) : ps.d_segs;
   const uint8_t* rowc = e.pair ? d_colors : nullptr;
-  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rooted_smem)));
+  smem_limit(reinterpret_cast<const void*>(kern), e.rooted_smem);
   const int spw = 128 / zw;
   // sharded + async transport (NCCL): group g+1's panel is all-gathered on the
   // communication stream while group g's SpMM runs (two buffers; event
@@ -2133,7 +2151,7 @@ template <bool AL, bool ST>
 static void launch_node(const NodeExec& e, int k, cudaStream_t s, int32_t n, const float* A,
                         const float* P, const uint8_t* colors, float* out) {
   auto kern = dev::ema_node<AL, ST>;
-  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
+  smem_limit(reinterpret_cast<const void*>(kern), e.ema_smem);
   const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
   // one warp per 8-column output chunk (up to 16): light nodes get small CTAs,
   // so many tiles co-reside per SM and staging overlaps compute across CTAs
@@ -2147,7 +2165,7 @@ static void launch_root(const NodeExec& e, cudaStream_t s, int32_t n, const floa
                         const float* P, const uint8_t* colors, double* rout, double* racc,
                         double* tile_tot) {
   auto kern = dev::ema_root<AL, ST>;
-  TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.ema_smem)));
+  smem_limit(reinterpret_cast<const void*>(kern), e.ema_smem);
   const unsigned tiles = static_cast<unsigned>((n + dev::kTileV - 1) / dev::kTileV);
   kern<<<tiles, dev::kEmaWarps * 32, e.ema_smem, s>>>(A, P, colors, e.d_split, e.pairs, e.Ca, e.Cps,
                                                       n, rout, racc, tile_tot);
@@ -2159,7 +2177,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   const int4* tl = reinterpret_cast<const int4*>(arena_ + tiles_off_);
   const unsigned grid = static_cast<unsigned>(max_tiles_);
   auto attr = [&](const void* f) {
-    TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_smem)));
+    smem_limit(f, e.rt_smem);
   };
   if (e.rtv_pleaf) {  // vertex-per-warp over a leaf passive child
     const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
@@ -2173,7 +2191,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
                                      dev::ema_rtv_pleaf<1, 3>, dev::ema_rtv_pleaf<1, 4>, dev::ema_rtv_pleaf<1, 5>,
                                      dev::ema_rtv_pleaf<1, 6>};
     const PleafFn kern = kerns[e.rtv_packed ? e.size - 1 : 0];
-    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_limit(reinterpret_cast<const void*>(kern), smem);
     const unsigned pgrid = static_cast<unsigned>(std::max<int64_t>(1, std::min<int64_t>(n_, 148 * 16)));
     kern<<<pgrid, 256, smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rtv_drop, e.size - 1,
                                         e.Ws, e.d_omap, e.Cout, n_, slice, oslice, table_ptr(e.out_off));
@@ -2217,7 +2235,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     // (narrow rows: up to 128 vertices per CTA, so a CTA moves >= 16 KB)
     const int vpb = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(128, (48 << 10) / (4 * rf))));
     const size_t smem = static_cast<size_t>(vpb) * rf * 4;
-    TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_copy, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+    smem_limit(reinterpret_cast<const void*>(dev::ema_rt_copy), smem);
     int L = 1;  // lanes per row: enough for the row's float4s and the output panel's slots
     while (L < 32 && (L * 4 < rf || L < std::min(32, e.Cout))) L *= 2;
     dev::ema_rt_copy<<<static_cast<unsigned>((n_ + vpb - 1) / vpb), 256, smem, stream_>>>(
@@ -2225,7 +2243,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   } else if (e.rt_blocked && e.rt_pipe_smem) {
     auto kern = dev::ema_rt_blocked_pipe<dev::kRtPipeProducers, dev::kRtPipeConsumers>;
     const int nthr = (dev::kRtPipeProducers + dev::kRtPipeConsumers) * 32;
-    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_pipe_smem)));
+    smem_limit(reinterpret_cast<const void*>(kern), e.rt_pipe_smem);
     const unsigned g = static_cast<unsigned>(std::max(1, std::min(max_tiles_, num_sms_)));
     kern<<<g, nthr, e.rt_pipe_smem, stream_>>>(
         A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_,
@@ -2234,7 +2252,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
   } else if (e.rt_blocked && e.rt_tma_smem) {
     // persistent, TMA-engine staging double-buffered against the compute
     auto kern = dev::ema_rt_blocked_tma;
-    TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.rt_tma_smem)));
+    smem_limit(reinterpret_cast<const void*>(kern), e.rt_tma_smem);
     const int RA = dev::num_panels(e.Ca_in) * dev::kZ;
     const int RS = RA + dev::num_panels(e.Cpt) * dev::kZ;
     const unsigned g = static_cast<unsigned>(std::max(1, std::min(max_tiles_, num_sms_)));
@@ -2257,7 +2275,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int slice = (e.Wa + e.Wp + (e.d_imap ? e.Ws : 0)) * dev::kSpitch;
     const size_t wsmem = static_cast<size_t>(8) * slice * 4;
     if (warp_mode && wsmem <= (100u << 10)) {
-      TCG_CUDA(cudaFuncSetAttribute(dev::ema_rt_node_w, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(wsmem)));
+      smem_limit(reinterpret_cast<const void*>(dev::ema_rt_node_w), wsmem);
       dev::ema_rt_node_w<<<static_cast<unsigned>((max_tiles_ + 7) / 8), 256, wsmem, stream_>>>(
           A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, e.Wp, vs, tl, max_tiles_, e.d_rt_packed, e.rt_pairs, e.Ws,
           e.d_omap, e.d_imap, e.Cout, n_, slice, out);
@@ -2424,7 +2442,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
       const unsigned vgrid = static_cast<unsigned>(std::min<int64_t>(n_, 148 * 16));
       if (e.vtx) {
         auto smem_attr = [&](const void* f) {
-          TCG_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(e.vtx_smem)));
+          smem_limit(f, e.vtx_smem);
         };
         if (e.root) {
           double* rout = reinterpret_cast<double*>(arena_ + e.out_off);
@@ -2458,8 +2476,7 @@ void Engine::run_dp(const uint8_t* d_colors_in, double* d_total, double* d_root_
           else launch_node<true, false>(e, plan_.k, stream_, n_, A, P, d_colors, out);
         } else if (e.blocked) {
           auto kern = dev::ema_blocked<true>;
-          TCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(e.ema_smem)));
+          smem_limit(reinterpret_cast<const void*>(kern), e.ema_smem);
           kern<<<static_cast<unsigned>((n_ + dev::kTileV - 1) / dev::kTileV), 256, e.ema_smem, stream_>>>(
               A, P, static_cast<const dev::GroupDesc*>(e.d_groups), e.ngroups,
               static_cast<const dev::BlockDesc*>(e.d_blocks), e.Ca, e.Cp, e.Cs, n_, out, e.Cps,
