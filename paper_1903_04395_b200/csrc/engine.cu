@@ -1546,9 +1546,6 @@ void Engine::setup_rooted_ema(int max_smem) {
         const int64_t half = (max_smem - 4096) / 2;
         int V = 8;
         while (V > 1 && 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) > half) V /= 2;
-        // a third CTA per SM (80 registers) when the same V still fits (cfg4 node 1: 114 -> 109 ms;
-        // halving V for it loses: cfg5 node 1 at V = 1 291 -> 390 ms)
-        e.rtv_minb = 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) <= (max_smem - 4096) / 3 ? 3 : 2;
         e.rtv_V = V;
         e.rtv_sa = static_cast<int>(stride(row_floats(e.Wa), V));
         e.rtv_sp = static_cast<int>(stride(e.Wp, V));
@@ -2206,9 +2203,14 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
       dev::ema_rtv_root<<<vgrid, 256, e.rt_smem, stream_>>>(A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, e.d_rt_split,
                                                              e.rt_pairs, n_, rout, d_root_acc);
     } else {
-      auto kern = e.rtv_minb == 3 ? dev::ema_rtv_blocked<dev::kH1, 3> : dev::ema_rtv_blocked<dev::kH1, 2>;
+      // two CTAs of 14 warps per SM (72 registers, no spills).  Measured on cfg5 node 1 / node 2,
+      // threads per CTA 256 / 320 / 384 / 448 / 512: 238 / 232 / 230 / 217 / 230 and 111 / 103 / 102 /
+      // 100 / 101 ms (512: 64 registers, spills); three 256-thread CTAs when V allows: cfg4 node 1
+      // 103 against 102 ms
+      constexpr int thr = dev::kRtvThreads;
+      auto kern = dev::ema_rtv_blocked<dev::kH1, thr>;
       attr(reinterpret_cast<const void*>(kern));
-      kern<<<vgrid, 256, e.rt_smem, stream_>>>(
+      kern<<<vgrid, thr, e.rt_smem, stream_>>>(
           A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::RtvTask*>(e.d_rtv_tasks), e.rtv_ntasks, e.d_rtv_gout,
           e.d_rtv_runs, e.d_rtv_blocks, e.Ws, e.d_omap, e.Cout, n_, table_ptr(e.out_off), e.rtv_V, e.rtv_sa, e.rtv_sp);
     }

@@ -1045,16 +1045,27 @@ __device__ __forceinline__ void micro_fma_h(const float* a, const float* p, floa
    ...);
 }
 
+// shared-memory word at a 32-bit shared address plus a compile-time byte
+// offset (explicit ld.shared: the generic-pointer form recomputes the shared
+// window base and the row stride for every block)
+template <int OFF>
+__device__ __forceinline__ float lds_imm(uint32_t addr) {
+  float v;
+  asm("ld.shared.f32 %0, [%1+%2];" : "=f"(v) : "r"(addr), "n"(OFF));
+  return v;
+}
+template <int N, int... X>
+__device__ __forceinline__ void lds_row(float (&dst)[N], uint32_t addr, std::integer_sequence<int, X...>) {
+  ((dst[X] = lds_imm<X * 4>(addr)), ...);
+}
+
 template <int H, int I, int J>
-__device__ __forceinline__ void micro_block_h(const float* __restrict__ sa, const float* __restrict__ sp,
-                                              float* acc) {
+__device__ __forceinline__ void micro_block_h(uint32_t sa, uint32_t sp, float* acc) {
   if constexpr (I + J <= H) {
     constexpr int NA = cbin(H, I), NP = cbin(H, J);
     float a[NA], p[NP];
-#pragma unroll
-    for (int x = 0; x < NA; ++x) a[x] = sa[x];
-#pragma unroll
-    for (int x = 0; x < NP; ++x) p[x] = sp[x];
+    lds_row(a, sa, std::make_integer_sequence<int, NA>{});
+    lds_row(p, sp, std::make_integer_sequence<int, NP>{});
     micro_fma_h<H, I, J>(a, p, acc, std::make_integer_sequence<int, TripTab<H, I, J>::NT>{});
   }
 }
@@ -1079,10 +1090,10 @@ __host__ __device__ constexpr int hcode(int i, int j) { return i * 9 - i * (i - 
         sc = 0;                                                                      \
         cur = n1;                                                                    \
         n1 = n2;                                                                     \
-        wp += 32;                                                                    \
-        n2 = __ldg(wp);                                                              \
+        wo += 32;                                                                    \
+        n2 = __ldg(blocks + wo);                                                     \
       }                                                                              \
-      micro_block_h<H, I, J>(sA + (d & 0xFFFFu), sP + (d >> 16), acc);               \
+      micro_block_h<H, I, J>((d & 0xFFFFu) * 4u + aA, (d >> 16) * 4u + aP, acc);     \
     }                                                                                \
   } break;
 #define TCG_HCASES                                                                                        \
@@ -1107,8 +1118,9 @@ struct RtvTask {
   int32_t blk0, run0, nruns, s1;
 };
 
-template <int H, int MINB>
-__global__ void __launch_bounds__(256, MINB)
+constexpr int kRtvThreads = 448;  // 2 CTAs x 14 warps per SM at 72 registers
+template <int H, int THREADS>
+__global__ void __launch_bounds__(THREADS, 2)
 ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                 const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
                 const RtvTask* __restrict__ tasks, int ntasks, const int32_t* __restrict__ gout,
@@ -1122,8 +1134,7 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
   const int lane = threadIdx.x & 31;
   const int gpt = 32 / V;
   const int gl = lane / V, j = lane - gl * V;
-  const float* sA = smem + j * sa;
-  const float* sP = sP0 + j * sp;
+  const uint32_t aA = smem_u32(smem + j * sa), aP = smem_u32(sP0 + j * sp);  // the lane's vertex rows
   for (int64_t v0 = static_cast<int64_t>(blockIdx.x) * V; v0 < n; v0 += static_cast<int64_t>(gridDim.x) * V) {
     __syncthreads();
     if (threadIdx.x == 0) next_task = blockDim.x >> 5;
@@ -1140,8 +1151,8 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
       float acc[kAcc];
 #pragma unroll
       for (int x = 0; x < kAcc; ++x) acc[x] = 0.f;
-      const uint32_t* wp = blocks + t.x + lane + 64;  // (the lane's word of the chunk loaded next)
-      uint32_t cur = __ldg(wp - 64), n1 = __ldg(wp - 32), n2 = __ldg(wp);
+      uint32_t wo = static_cast<uint32_t>(t.x) + lane + 64;  // (the lane's word of the chunk loaded last)
+      uint32_t cur = __ldg(blocks + wo - 64), n1 = __ldg(blocks + wo - 32), n2 = __ldg(blocks + wo);
       int sc = 0;                                     // first word of the current step in the chunk
       uint32_t rr = __ldg(runs + t.y);
       for (int r = 0; r < t.z; ++r) {
