@@ -287,6 +287,36 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
   const int pin = num_panels(Cpt), zin = last_panel_width(Cpt);
   const int rf = (pin - 1) * kZ + zin;  // floats of one panel-padded row
   const int64_t u0 = static_cast<int64_t>(blockIdx.x) * vpb;
+  if (L == 32) {
+    // wide rows (one warp per row would leave warps idle whenever vpb is not a multiple of the
+    // warp count): every warp works on every row -- the whole CTA stages a row's float4s, and
+    // warp w writes output panels w, w + 8, ...
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int r = 0; r < vpb && u0 + r < n; ++r) {
+      const int64_t u = u0 + r;
+      for (int c4 = threadIdx.x * 4; c4 < rf; c4 += blockDim.x * 4) {
+        const int p = c4 >> 5, z = c4 & 31;
+        const int zp = p == pin - 1 ? zin : kZ;
+        *reinterpret_cast<float4*>(crow + r * rf + c4) =
+            __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+      }
+    }
+    __syncthreads();
+    const int pout = num_panels(Cout), zout = last_panel_width(Cout);
+    for (int r = 0; r < vpb && u0 + r < n; ++r) {
+      const int64_t u = u0 + r;
+      const int32_t* cm = cmap + static_cast<int64_t>(colors[u]) * Cout;
+      for (int p = warp; p < pout; p += nw) {
+        const int zp = p == pout - 1 ? zout : kZ;
+        if (lane < zp) {
+          const int col = p * kZ + lane;
+          const int src = col < Cout ? __ldg(cm + col) : -1;
+          out[static_cast<int64_t>(p) * n * kZ + u * zp + lane] = src >= 0 ? crow[r * rf + src] : 0.f;
+        }
+      }
+    }
+    return;
+  }
   for (int r = grp; r < vpb; r += ngrp) {  // stage: 128 B panel rows, float4 per lane
     const int64_t u = u0 + r;
     if (u >= n) break;
