@@ -2180,7 +2180,7 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
     const int slice = (e.Wa + 31) / 32 * 32 + 32 + 1;  // (+1: vertices' rows on different banks)
     const int cst = e.omap.empty() ? e.Ws : e.Cout;
     const int oslice = (cst + 31) / 32 * 32 + 1;
-    // one vertex per CTA pass (measured cfg4 node 4 / node 7, V = 1 / 2 / 4: 61 / 63 / 89 and 18 / 16 / 14 ms)
+    // one vertex per CTA pass (measured cfg4 node 4 / node 7, V = 1 / 2 / 4: 44 / 48 / 68 and 12.5 / 11.2 / 10.4 ms)
     const size_t smem = static_cast<size_t>(slice + oslice) * 4;
     using PleafFn = void (*)(const float*, int, const int32_t*, int, const float*, int, const int32_t*, const uint8_t*,
                              const uint32_t*, int, int, const int32_t*, int, int32_t, int, int, float*);

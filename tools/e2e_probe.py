@@ -31,3 +31,9 @@ for i in range(4):
     tot, est, se, pv = ctx.estimate(1 + i * ncol, ncol, per_vertex=True)
     t2 = time.perf_counter()
     print(f"{cfg} step {i}: set_graph_csr {1e3 * (t1 - t0):.1f} ms, estimate({ncol}) {1e3 * (t2 - t1):.1f} ms")
+# device time of the same colorings (CUDA events) next to the host wall clock of estimate()
+tm, _ = ctx.time(1, ncol, per_kernel=False)
+t0 = time.perf_counter()
+ctx.estimate(1, ncol, per_vertex=False)
+t1 = time.perf_counter()
+print(f"{cfg}: device time of {ncol} colorings {tm.total_ms:.1f} ms; estimate() without per-vertex {1e3 * (t1 - t0):.1f} ms")
