@@ -405,6 +405,12 @@ Engine::~Engine() {
   dfree(d_scalars_);
   dfree(d_seeds_);
   dfree(d_colors_);
+  if (next_.stream) cudaStreamSynchronize(next_.stream);
+  dfree(next_.d_buf[0]);
+  dfree(next_.d_buf[1]);
+  dfree(next_.d_seed);
+  if (next_.ready) cudaEventDestroy(next_.ready);
+  if (next_.stream) cudaStreamDestroy(next_.stream);
   batches_.clear();
   tr_.reset();  // (a communicator before its streams)
   if (comm_) cudaStreamDestroy(comm_);
@@ -1899,6 +1905,53 @@ void Engine::gen_colors(const uint64_t* seeds, int count, uint8_t* d_out) {
   TCG_CUDA(cudaGetLastError());
 }
 
+// The coloring of `seed`: the prefetched one when it matches this graph, template and rejection
+// limit (the DP then waits for the side stream's event), else generated on the engine stream.
+const uint8_t* Engine::take_or_generate(uint64_t seed) {
+  const uint64_t k = static_cast<uint64_t>(plan_.k);
+  const uint64_t limit = limit_override_ ? limit_override_ : (UINT64_MAX / k) * k;
+  if (next_.valid && next_.seed == seed && next_.n == nglob_ && next_.k == plan_.k && next_.limit == limit) {
+    next_.valid = false;
+    TCG_CUDA(cudaStreamWaitEvent(stream_, next_.ready, 0));
+    return next_.d_buf[next_.cur];
+  }
+  gen_colors(&seed, 1, d_colors_);
+  return d_colors_;
+}
+
+// Generate the coloring of `seed` on the side stream into the buffer the running DP does not read.
+void Engine::prefetch_next(uint64_t seed) {
+  // (small graphs: the generation is tens of microseconds, less than a second launch is worth)
+  if (nglob_ < (1 << 16) || exec_.empty()) return;
+  if (!next_.stream) {
+    TCG_CUDA(cudaStreamCreateWithFlags(&next_.stream, cudaStreamNonBlocking));
+    TCG_CUDA(cudaEventCreateWithFlags(&next_.ready, cudaEventDisableTiming));
+    TCG_CUDA(cudaMalloc(&next_.d_seed, sizeof(uint64_t)));
+  }
+  if (next_.cap < nglob_) {
+    TCG_CUDA(cudaStreamSynchronize(next_.stream));
+    for (auto& b : next_.d_buf) {
+      dfree(b);
+      TCG_CUDA(cudaMalloc(&b, nglob_));
+    }
+    next_.cap = nglob_;
+  }
+  const uint64_t k = static_cast<uint64_t>(plan_.k);
+  const uint64_t limit = limit_override_ ? limit_override_ : (UINT64_MAX / k) * k;
+  next_.cur ^= 1;
+  TCG_CUDA(cudaMemcpyAsync(next_.d_seed, &seed, sizeof(uint64_t), cudaMemcpyHostToDevice, next_.stream));
+  dev::mt_coloring<<<1, dev::kMtThreads, 0, next_.stream>>>(next_.d_seed, nglob_, plan_.k, limit, UINT64_MAX / k,
+                                                           next_.d_buf[next_.cur], nglob_);
+  ++launches_;
+  TCG_CUDA(cudaGetLastError());
+  TCG_CUDA(cudaEventRecord(next_.ready, next_.stream));
+  next_.valid = true;
+  next_.seed = seed;
+  next_.limit = limit;
+  next_.n = nglob_;
+  next_.k = plan_.k;
+}
+
 void Engine::coloring(uint64_t seed, uint8_t* host_colors) {
   require_ready();
   TCG_CUDA(cudaSetDevice(cfg_.device));
@@ -2542,10 +2595,10 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
     for (int32_t i = 0; i < nglob_; ++i)
       if (host_colors[i] >= plan_.k) throw invalid_argument("coloring value out of range [0, k)");
     TCG_CUDA(cudaMemcpyAsync(d_colors_, host_colors, nglob_, cudaMemcpyHostToDevice, stream_));
-  } else {
-    gen_colors(&seed, 1, d_colors_);
   }
-  run_dp(d_colors_, d_scalars_, nullptr, stats);
+  const uint8_t* dc = host_colors ? d_colors_ : take_or_generate(seed);
+  if (!host_colors) prefetch_next(seed + 1);  // (overlaps this coloring's DP)
+  run_dp(dc, d_scalars_, nullptr, stats);
   double total = 0;
   TCG_CUDA(cudaMemcpyAsync(&total, d_scalars_, sizeof(double), cudaMemcpyDeviceToHost, stream_));
   if (per_vertex && nglob_ > 0) {
@@ -2559,7 +2612,7 @@ double Engine::run_coloring(uint64_t seed, const uint8_t* host_colors, double* p
   }
   if (cfg_.flags & TCG_KEEP_TABLES) {
     last_colors_.resize(nglob_);
-    TCG_CUDA(cudaMemcpyAsync(last_colors_.data(), d_colors_, nglob_, cudaMemcpyDeviceToHost, stream_));
+    TCG_CUDA(cudaMemcpyAsync(last_colors_.data(), dc, nglob_, cudaMemcpyDeviceToHost, stream_));
   }
   TCG_CUDA(cudaStreamSynchronize(stream_));
   if (exec_.empty()) total = static_cast<double>(nloc_);
