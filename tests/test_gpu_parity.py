@@ -353,6 +353,30 @@ def test_given_coloring_matches_seeded(cfg1_golden):
     assert a == b == float(gold["totals_seeds1_10"][3])
 
 
+def test_prefetched_next_coloring_is_the_seeded_coloring():
+    """run_coloring(seed) generates the coloring of seed + 1 on a side stream (graphs of >= 65,536
+    vertices): consecutive seeds, a repeated seed, a jump, a template with another k in between and
+    a caller-given coloring must all give what a context that never prefetches gives."""
+    g = T.generate_rmat(T.RmatSpec(17, 4 << 17, .57, .19, .19, .05, 3))
+    t5 = T.template_from_parents([-1, 0, 1, 1, 3], 0)
+    t3 = T.template_from_parents([-1, 0, 0], 0)
+
+    def fresh(t, seed):  # (first call of a new context: nothing prefetched)
+        return ctx_for(g, t).run_coloring(seed)[0]
+
+    c = ctx_for(g, t5)
+    want = {s: fresh(t5, s) for s in (7, 8, 9, 20)}
+    assert [c.run_coloring(s)[0] for s in (7, 8, 9, 9, 20, 8)] == [want[s] for s in (7, 8, 9, 9, 20, 8)]
+    colors = O.random_coloring(g.n, 5, 9)
+    assert c.run_coloring(0, colors=colors)[0] == want[9]
+    assert np.array_equal(c.coloring(9), colors)
+    c.run_coloring(30)                       # leaves seed 31 of k = 5 prefetched
+    c.set_template(t3)
+    assert c.run_coloring(31)[0] == fresh(t3, 31)
+    c.set_template(t5)
+    assert c.run_coloring(32)[0] == fresh(t5, 32)
+
+
 def test_set_graph_buffer_reuse():
     """One context, a sequence of host-CSR graphs that grow, shrink and grow
     again (device graph buffers, the device-built schedules, the arena and the
