@@ -1040,6 +1040,22 @@ __device__ __forceinline__ void stage_row_pmap(const float* __restrict__ T, int 
   }
 }
 
+// stage_row with cp.async (LDGSTS.128): the copies of a thread are all in flight at once and
+// hold no registers; the caller waits with cp_async_wait_all() before its barrier.
+__device__ __forceinline__ void stage_row_async(const float* __restrict__ T, int C, int32_t n, int64_t v, float* dst) {
+  const int panels = num_panels(C);
+  const int zl = last_panel_width(C);
+  const int total4 = ((panels - 1) * kZ + zl) / 4;
+  const uint32_t d0 = smem_u32(dst);
+  for (int f = threadIdx.x; f < total4; f += blockDim.x) {
+    const int p = (f * 4) / kZ, z4 = (f * 4) % kZ;
+    const int zw = p == panels - 1 ? zl : kZ;
+    const float* src = T + static_cast<int64_t>(p) * n * kZ + v * zw + z4;
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(d0 + f * 16), "l"(src) : "memory");
+  }
+}
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_all;" ::: "memory"); }
+
 // ---- H-colour register blocking (H = 6/7/8), generic over H: the
 // H1-subset micro-patterns (i, j) of build_blocked(k', s', a', H), pattern
 // code i * 16 + j.  Triples (a1, p1, a1|p1) of a pattern are one constexpr
@@ -1170,9 +1186,10 @@ ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict_
     if (threadIdx.x == 0) next_task = blockDim.x >> 5;
     for (int jj = 0; jj < V && v0 + jj < n; ++jj) {
       if (amap) stage_row_pmap(Am, Ca, n, v0 + jj, smem + jj * sa, amap + static_cast<int64_t>(colors[v0 + jj]) * Ca);
-      else stage_row(Am, Wa, n, v0 + jj, smem + jj * sa);
+      else stage_row_async(Am, Wa, n, v0 + jj, smem + jj * sa);
       stage_row_pmap(Pm, Cpt, n, v0 + jj, sP0 + jj * sp, pmap + static_cast<int64_t>(colors[v0 + jj]) * Cpt);
     }
+    cp_async_wait_all();
     __syncthreads();
     const int64_t v = v0 + j;
     for (int task = threadIdx.x >> 5; task < ntasks;) {
@@ -1228,8 +1245,9 @@ ema_rtv_root(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ a
     const int c = colors[v];
     __syncthreads();
     if (amap) stage_row_pmap(Am, Ca, n, v, sA, amap + static_cast<int64_t>(c) * Ca);
-    else stage_row(Am, Wa, n, v, sA);
+    else stage_row_async(Am, Wa, n, v, sA);
     stage_row_pmap(Pm, Cpt, n, v, sP, pmap + static_cast<int64_t>(c) * Cpt);
+    cp_async_wait_all();
     __syncthreads();
     double acc = 0;
     for (int p = threadIdx.x; p < pairs; p += blockDim.x) {
