@@ -272,6 +272,12 @@ ema_rt_node(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ am
   }
 }
 
+// 16-byte global -> shared copy that bypasses registers (LDGSTS); wait with cp_async_wait_all_()
+__device__ __forceinline__ void cp_async16_(float* dst, const float* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(static_cast<uint32_t>(__cvta_generic_to_shared(dst))), "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all_() { asm volatile("cp.async.wait_all;" ::: "memory"); }
 // Active-leaf node: M_s[v,S] = P'[v, S minus c] -- a per-color column
 // permutation of the vertex's P' row: out[v, i] = P'[v, cmap[c][i]] (0 where
 // -1).  A CTA stages the full P' rows of `vpb` consecutive vertices in smem
@@ -297,10 +303,10 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
       for (int c4 = threadIdx.x * 4; c4 < rf; c4 += blockDim.x * 4) {
         const int p = c4 >> 5, z = c4 & 31;
         const int zp = p == pin - 1 ? zin : kZ;
-        *reinterpret_cast<float4*>(crow + r * rf + c4) =
-            __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+        cp_async16_(crow + r * rf + c4, Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z);
       }
     }
+    cp_async_wait_all_();
     __syncthreads();
     const int pout = num_panels(Cout), zout = last_panel_width(Cout);
     for (int r = 0; r < vpb && u0 + r < n; ++r) {
@@ -323,10 +329,10 @@ ema_rt_copy(const float* __restrict__ Pm, int Cpt, const uint8_t* __restrict__ c
     for (int c4 = sub * 4; c4 < rf; c4 += L * 4) {
       const int p = c4 >> 5, z = c4 & 31;
       const int zp = p == pin - 1 ? zin : kZ;
-      *reinterpret_cast<float4*>(crow + r * rf + c4) =
-          __ldg(reinterpret_cast<const float4*>(Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z));
+      cp_async16_(crow + r * rf + c4, Pm + static_cast<int64_t>(p) * n * kZ + u * zp + z);
     }
   }
+  cp_async_wait_all_();
   __syncthreads();
   const int pout = num_panels(Cout), zout = last_panel_width(Cout);
   for (int r = grp; r < vpb; r += ngrp) {  // write: consecutive lanes -> consecutive slots of a row
