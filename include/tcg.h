@@ -118,6 +118,13 @@ double tcg_colorful_probability(int k);
  * full_cols, store_cols}; optional perm[full_cols] (full column -> P' storage
  * column) and slot_col[k * groups * zw] (compressed slot -> full column or -1). */
 int tcg_rooted_layout(int k, int s, int32_t* info, int32_t* perm, int32_t* slot_col);
+/* Host-only self-check of the work layout of the vertex-per-CTA blocked eMA (k = 15/17 nodes; B200
+ * design, no reference counterpart): the (k, s, a) problem over V vertices per pass is
+ * cut into tasks of 32 / V same-shape output groups; every (group, block) of the split enumeration
+ * must appear exactly once at the position the kernel reads (TCG_ELOGIC otherwise).  info[6] =
+ * {tasks, groups, block steps, pattern runs, shared-load wavefronts of the chosen block order,
+ * conflict-free wavefronts}. */
+int tcg_rtv_task_layout(int k, int s, int a, int V, int64_t* info);
 
 /* ------------------------------------------------------------------------
  * Device engine (one GPU).  == the vectorized engine of engines.hpp:224-268.

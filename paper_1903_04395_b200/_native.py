@@ -78,6 +78,7 @@ _SIGS = {
     "tcg_estimate_bytes": (i64, [P(TcgPlan), i64]),
     "tcg_colorful_probability": (dbl, [C.c_int]),
     "tcg_rooted_layout": (C.c_int, [C.c_int, C.c_int, vp, vp, vp]),
+    "tcg_rtv_task_layout": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, vp]),
     "tcg_create": (C.c_int, [P(TcgConfig), P(vp)]),
     "tcg_destroy": (None, [vp]),
     "tcg_set_graph": (C.c_int, [vp, i32, vp, vp]),

@@ -256,6 +256,13 @@ int tcg_rooted_layout(int k, int s, int32_t* info, int32_t* perm, int32_t* slot_
   });
 }
 
+int tcg_rtv_task_layout(int k, int s, int a, int V, int64_t* info) {
+  return guarded([&] {
+    need(info, "info");
+    tcg::rtv_task_layout_check(k, s, a, V, info);
+  });
+}
+
 // ----------------------------------------------------------------- engine
 int tcg_create(const tcg_config* cfg, tcg_ctx** out) {
   return guarded([&] {

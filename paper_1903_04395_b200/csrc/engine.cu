@@ -367,6 +367,63 @@ PartSchedule build_schedule(const std::vector<int64_t>& lo, const std::vector<in
 }
 }  // namespace
 
+// Host-only self-check of the task layout of ema_rtv_blocked (tcg_rtv_task_layout): every
+// (group, block) of build_blocked appears exactly once, in a task whose groups share one run
+// list, at the descriptor position the kernel reads.  info = {tasks, groups, block steps, runs,
+// shared-load wavefronts, conflict-free wavefronts}.
+void rtv_task_layout_check(int k, int s, int a, int V, int64_t info[6]) {
+  if (k < 2 || k > kMaxK || s < 2 || s > k || a < 1 || a >= s) throw invalid_argument("need 2 <= s <= k <= 20 and 1 <= a < s");
+  if (V != 1 && V != 2 && V != 4 && V != 8) throw invalid_argument("V must be 1, 2, 4 or 8");
+  if (k < dev::kH1) throw invalid_argument("need k >= 6 (the colours of the register-blocked part)");
+  std::vector<dev::GroupDesc> gr;
+  std::vector<dev::BlockDesc> bl;
+  build_blocked(k, s, a, gr, bl, dev::kH1, 16);
+  const RtvPlan P = build_rtv_tasks(k, s, a, dev::kH1, V);
+  const int gpt = 32 / V;
+  std::map<int32_t, size_t> by_out;
+  for (size_t g = 0; g < gr.size(); ++g)
+    if (!by_out.emplace(gr[g].out_off, g).second) throw logic_error("two groups share an output offset");
+  std::vector<char> seen(gr.size(), 0);
+  if (P.gout.size() != P.tasks.size() * static_cast<size_t>(gpt)) throw logic_error("gout size");
+  for (size_t t = 0; t < P.tasks.size(); ++t) {
+    const dev::RtvTask& task = P.tasks[t];
+    for (int gl = 0; gl < gpt; ++gl) {
+      const int32_t oo = P.gout[t * gpt + gl];
+      if (oo < 0) continue;
+      const auto it = by_out.find(oo);
+      if (it == by_out.end() || seen[it->second]) throw logic_error("a task lists an unknown or repeated group");
+      seen[it->second] = 1;
+      const dev::GroupDesc& g = gr[it->second];
+      if (g.s1 != task.s1) throw logic_error("task and group differ in s1");
+      int64_t step = 0;
+      int b = g.b0;
+      for (int r = 0; r < task.nruns; ++r) {
+        const uint32_t rr = P.runs[task.run0 + r];
+        const int len = static_cast<int>(rr >> 8);
+        std::vector<uint32_t> want, got;
+        for (int q = 0; q < len; ++q, ++b, ++step) {
+          if (b >= g.b1) throw logic_error("a task's runs are longer than its group's block list");
+          if (static_cast<uint32_t>(dev::hcode(bl[b].ij / 16, bl[b].ij % 16)) != (rr & 0xFFu)) throw logic_error("run pattern differs from the group's blocks");
+          want.push_back(static_cast<uint32_t>(bl[b].a_off) | (static_cast<uint32_t>(bl[b].p_off) << 16));
+          got.push_back(P.blocks[task.blk0 + step * gpt + gl]);
+        }
+        std::sort(want.begin(), want.end());
+        std::sort(got.begin(), got.end());
+        if (want != got) throw logic_error("a run's descriptors are not a permutation of the group's blocks");
+      }
+      if (b != g.b1) throw logic_error("a task's runs do not cover its group's block list");
+    }
+  }
+  for (char c : seen)
+    if (!c) throw logic_error("a group is in no task");
+  info[0] = static_cast<int64_t>(P.tasks.size());
+  info[1] = static_cast<int64_t>(gr.size());
+  info[2] = P.steps;
+  info[3] = static_cast<int64_t>(P.runs.size());
+  info[4] = P.wavefronts;
+  info[5] = P.ideal;
+}
+
 Engine::Engine(const tcg_config& cfg, cudaStream_t shared_stream) : cfg_(cfg) {
   int ndev = 0;
   TCG_CUDA(cudaGetDeviceCount(&ndev));

@@ -23,6 +23,9 @@
 
 namespace tcg {
 
+// host-only self-check of the ema_rtv_blocked task layout (engine.cu); throws on an inconsistency
+void rtv_task_layout_check(int k, int s, int a, int V, int64_t info[6]);
+
 struct NodeExec {
   int id = -1, a = -1, p = -1;
   int size = 0, sa = 0, sp = 0;

@@ -251,3 +251,30 @@ def test_rooted_layout_partition(k, s):
     order = sorted(range(full), key=lambda x: perm[x])
     assert [grp[x] for x in order] == sorted(grp[x] for x in order)
     assert store % 8 == 0
+
+
+@pytest.mark.parametrize("k,s,a,V", [(16, 11, 7, 2), (16, 7, 3, 8), (14, 10, 7, 4), (16, 11, 7, 1),
+                                     (12, 8, 4, 8), (9, 5, 2, 4), (19, 9, 4, 2)])
+def test_rtv_task_layout(k, s, a, V):
+    """Work layout of the vertex-per-CTA blocked eMA (csrc/engine.cu build_rtv_tasks; the (k, s, a)
+    here are the rooted problems of cfg5 nodes 1 / 2 and cfg4 node 1, and smaller ones): the library
+    checks that every (group, block) of the split enumeration sits exactly once where the kernel
+    reads it; here also the counts (groups = the (S2, s1) classes over the k - 6 high colours,
+    block steps padded per task) and that the bank-aware order is no worse than 1.5x
+    conflict-free."""
+    from math import comb
+    info = np.zeros(6, np.int64)
+    N.check(N.lib.tcg_rtv_task_layout(k, s, a, V, info.ctypes.data))
+    tasks, groups, steps, runs, wave, ideal = (int(x) for x in info)
+    gpt = 32 // V
+    assert groups == sum(comb(k - 6, t) for t in range(k - 5) if 0 <= s - t <= 6)
+    assert -(-groups // gpt) <= tasks <= -(-groups // gpt) + 7     # (one partial task per shape at most)
+    assert steps >= 1 and runs >= 1
+    assert ideal <= wave <= 1.5 * ideal
+
+
+def test_rtv_task_layout_rejects_bad_arguments():
+    info = np.zeros(6, np.int64)
+    for bad in ((16, 11, 7, 3), (5, 3, 1, 2), (16, 1, 1, 2), (16, 11, 11, 2), (21, 11, 7, 2)):
+        with pytest.raises(T.InvalidArgument):
+            N.check(N.lib.tcg_rtv_task_layout(*bad, info.ctypes.data))
