@@ -1606,9 +1606,19 @@ void Engine::setup_rooted_ema(int max_smem) {
         e.rt_smem = static_cast<size_t>(4 * (row_floats(e.Wa) + e.Wp));
       } else {  // V vertices per pass: two CTAs per SM when V >= 2 fits
         auto stride = [](int64_t f, int V) { return (f + 31) / 32 * 32 + (V > 1 ? 32 / V : 0); };
-        const int64_t half = (max_smem - 4096) / 2;
-        int V = 8;
-        while (V > 1 && 4 * V * (stride(row_floats(e.Wa), V) + stride(e.Wp, V)) > half) V /= 2;
+        auto fit = [&](int64_t bytes) {
+          int v = 8;
+          while (v > 1 && 4 * v * (stride(row_floats(e.Wa), v) + stride(e.Wp, v)) > bytes) v /= 2;
+          return v;
+        };
+        int V = fit((max_smem - 4096) / 2);
+        // rows so wide that two CTAs hold <= 2 vertices each: ONE CTA of twice the threads over
+        // twice the vertices instead (same warps per SM; its 28 warps walk the same task classes
+        // together, so the pattern code is fetched once, not per CTA: cfg5 node 1 213 -> 181 ms;
+        // narrower rows lose the overlap of one CTA's staging with the other's FMAs: cfg5 node 2
+        // 100 -> 108 ms, cfg4 node 1 102 -> 103)
+        e.rtv_one_cta = V <= 2 && fit(max_smem - 4096) >= 2 * V;
+        if (e.rtv_one_cta) V = fit(max_smem - 4096);
         e.rtv_V = V;
         e.rtv_sa = static_cast<int>(stride(row_floats(e.Wa), V));
         e.rtv_sp = static_cast<int>(stride(e.Wp, V));
@@ -2317,8 +2327,9 @@ void Engine::launch_rt_ema(const NodeExec& e, const float* A, const float* P, do
       // threads per CTA 256 / 320 / 384 / 448 / 512: 238 / 232 / 230 / 217 / 230 and 111 / 103 / 102 /
       // 100 / 101 ms (512: 64 registers, spills); three 256-thread CTAs when V allows: cfg4 node 1
       // 103 against 102 ms
-      constexpr int thr = dev::kRtvThreads;
-      auto kern = dev::ema_rtv_blocked<dev::kH1, thr>;
+      const int thr = e.rtv_one_cta ? 2 * dev::kRtvThreads : dev::kRtvThreads;
+      auto kern = e.rtv_one_cta ? dev::ema_rtv_blocked<dev::kH1, 2 * dev::kRtvThreads>
+                                : dev::ema_rtv_blocked<dev::kH1, dev::kRtvThreads>;
       attr(reinterpret_cast<const void*>(kern));
       kern<<<vgrid, thr, e.rt_smem, stream_>>>(
           A, e.Wa, e.d_amap_in, e.Ca_in, P, e.Cpt, e.d_pmap, d_colors_rt_, static_cast<const dev::RtvTask*>(e.d_rtv_tasks), e.rtv_ntasks, e.d_rtv_gout,

@@ -103,6 +103,7 @@ struct NodeExec {
   uint32_t* d_rtv_runs = nullptr;     // pattern runs {i * 16 + j | length << 8}, shared by the tasks of a shape
   uint32_t* d_rtv_blocks = nullptr;   // step-major {a_off | p_off << 16} per (task, block step, group)
   int rtv_ntasks = 0;
+  bool rtv_one_cta = false;           // one 896-thread CTA per SM over twice the vertices (very wide rows)
   bool rtv_pleaf = false;         // vertex-per-warp eMA over a leaf passive child (ema_rtv_pleaf)
   uint32_t* d_rtv_drop = nullptr; // [Ws][s-1] {A index of S' minus d | d << 16}
   bool rtv_packed = false;        // d_rtv_drop packed as one uint4 per output (s-1 <= 6, k-1 <= 16)

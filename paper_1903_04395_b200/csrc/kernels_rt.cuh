@@ -1172,7 +1172,7 @@ struct RtvTask {
 
 constexpr int kRtvThreads = 448;  // 2 CTAs x 14 warps per SM at 72 registers
 template <int H, int THREADS>
-__global__ void __launch_bounds__(THREADS, 2)
+__global__ void __launch_bounds__(THREADS, THREADS > 512 ? 1 : 2)
 ema_rtv_blocked(const float* __restrict__ Am, int Wa, const int32_t* __restrict__ amap, int Ca, const float* __restrict__ Pm, int Cpt,
                 const int32_t* __restrict__ pmap, const uint8_t* __restrict__ colors,
                 const RtvTask* __restrict__ tasks, int ntasks, const int32_t* __restrict__ gout,
